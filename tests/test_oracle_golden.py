@@ -1,0 +1,229 @@
+"""Pin the CPU oracle (oracle/) to golden vectors from the real reference.
+
+Fixtures: tests/golden/*.npz, produced by tests/golden/make_golden.py running
+/root/reference/pkg/src/paradiff in the build container.  CPU only.
+"""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from oracle import paradiff_oracle as O
+from paper_2006_12883_b200 import problems as PB
+from pd_util import per_node_rel, rel_l2
+
+
+def test_tableau_matches_reference(golden):
+    g = golden("tableau")
+    for M in range(1, 6):
+        t = O.tableau(M)
+        for mine, key in ((t.nodes, "nodes"), (t.Q, "Q"), (t.QDI, "QDeltaImplicit"),
+                          (t.QDE, "QDeltaExplicit"), (t.Kq, "Kq"), (t.Mq, "Mq"), (t.Jq, "Jq")):
+            np.testing.assert_allclose(mine, g[f"M{M}_{key}"], rtol=0, atol=1e-14)
+        np.testing.assert_allclose(O.tableau(M, "lu-trick").QDI, g[f"M{M}_lutrick"], atol=1e-14)
+
+
+def test_fem_and_transfers_match_reference(golden):
+    g = golden("tableau")
+    Kh, mh = O.fem1d_operators(8)
+    np.testing.assert_array_equal(Kh.toarray(), g["fem8_Kh"])
+    np.testing.assert_array_equal(mh, g["fem8_mh"])
+    np.testing.assert_array_equal(O.vertex_restriction(9).toarray(), g["R9"])
+    np.testing.assert_array_equal(O.vertex_prolongation(9).toarray(), g["P9"])
+    np.testing.assert_array_equal(O.time_restriction(8).toarray(), g["Rt8"])
+    np.testing.assert_array_equal(O.time_prolongation(8).toarray(), g["Pt8"])
+    np.testing.assert_allclose(O.node_restriction(2, 3).toarray(), g["Rn23"], atol=1e-15)
+    np.testing.assert_allclose(O.node_prolongation(2, 3).toarray(), g["Pn23"], atol=1e-15)
+    np.testing.assert_allclose(O.node_eval(O.radau_right(5), O.radau_right(3)), g["Ne35"],
+                               atol=1e-14)
+
+
+def _golden_matrix(g):
+    return sp.csr_matrix((g["A_data"], g["A_indices"], g["A_indptr"]))
+
+
+def test_ilu0_bitwise_and_gmres(golden):
+    g = golden("linalg")
+    A = _golden_matrix(g)
+    ilu = O.OIlu0(A)
+    np.testing.assert_array_equal(ilu.val, g["ilu_data"])
+    np.testing.assert_array_equal(ilu.diag, g["ilu_diag"])
+    np.testing.assert_array_equal(ilu.solve(g["b"]), g["ilu_solve"])
+    bj = O.OBlockJacobi(A, 3, threads=2)
+    np.testing.assert_array_equal(bj.solve(g["b"]), g["bj_solve"])
+    x, rep = O.gmres(A, g["b"], M=ilu, tol_rel=1e-10, tol_abs=1e-12, restart=7, max_it=200)
+    assert rep.iterations == int(g["gm_its"]) and rep.converged
+    assert rel_l2(x, g["gm_x"]) < 1e-13
+    x2, rep2 = O.gmres(A, g["b"], M=bj, tol_rel=1e-10, tol_abs=1e-12, restart=5, max_it=200)
+    assert rep2.iterations == int(g["gm2_its"])
+    assert rel_l2(x2, g["gm2_x"]) < 1e-13
+
+
+def test_zero_pivot_reports_row():
+    A = sp.csr_matrix(np.array([[1.0, 0.0, 0.0], [0.0, 0.0, 1.0], [0.0, 1.0, 1.0]]))
+    with pytest.raises(O.OracleSolverError, match="row 1"):
+        O.OIlu0(A)
+
+
+def _mono_system(Nt=4, Nx=16, M=3, gamma=5.0, T=2.0):
+    Kh, mh = O.fem1d_operators(Nx, 10.0)
+    x = np.linspace(0.0, 10.0, Nx + 1)
+    u0 = 2.0 * np.exp(-(((x - 5.0) / 0.1) ** 2))
+    return O.OSystem(O.tableau(M), Kh, mh, Nt, T, gamma, u0)
+
+
+def test_spacetime_matches_reference(golden):
+    g = golden("spacetime")
+    s = _mono_system()
+    np.testing.assert_allclose(s.rhs(), g["rhs"], atol=1e-15)
+    np.testing.assert_allclose(s.residual(g["u"]), g["res"], rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(s.global_matrix() @ g["v"], g["Lv"], rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(s.jacobian(g["u"]) @ g["v"], g["Jv"], rtol=1e-13, atol=1e-13)
+    lin = _mono_system(gamma=0.0, T=1.0)
+    np.testing.assert_allclose(lin.solve_sequential(), g["seq"], rtol=1e-12, atol=1e-13)
+
+
+def _heat_u0(Nx):
+    x = np.linspace(0.0, 1.0, Nx + 1)
+    return sum(a * np.cos(k * np.pi * x) for k, a in ((1, 1.0), (3, 2.0), (4, 3.0)))
+
+
+@pytest.mark.parametrize("strategy", ["SMG", "STMG", "SMMG"])
+@pytest.mark.parametrize("P", [1, 4])
+def test_mg_fem1d_matches_reference(golden, strategy, P):
+    g = golden("mg_fem1d")
+    Kh, mh = O.fem1d_operators(64)
+    s = O.OSystem(O.tableau(3), Kh, mh, 16, 1.0, 0.0, _heat_u0(64))
+    mg = O.fem_hierarchy(s, strategy, 3, 3, partitions=P, threads=2)
+    x, rep = mg.solve(s.rhs(), tol_rel=1e-10, tol_abs=1e-10)
+    key = f"{strategy}_P{P}"
+    assert rep.iterations == int(g[key + "_its"])
+    assert per_node_rel(x, g[key + "_x"], (16, 3, 65)) < 1e-10
+    v1 = mg.vcycle(s.rhs(), np.zeros(s.size))
+    assert rel_l2(v1, g[key + "_v1"]) < 1e-12
+
+
+def c1_oracle_mg(cfg, strategy, P, L=4, nu=3, threads=1):
+    ops = PB.fd_space(cfg.spec)
+    s = O.OSystem(O.tableau(cfg.M), ops.Kh, ops.lumped_diagonal, cfg.Nt, cfg.T, 0.0, cfg.u0())
+    return s, fd_oracle_hierarchy(s, cfg.spec, strategy, L, nu, P, threads)
+
+
+def fd_oracle_hierarchy(s, spec, strategy, L, nu, P, threads=1):
+    specs = [spec]
+    for _ in range(L - 1):
+        specs.append(specs[-1].coarse())
+    dims = []
+    for l, sp_ in enumerate(specs):
+        nt = s.Nt // 2 ** l if strategy == "STMG" else s.Nt
+        m = max(s.tab.M - l, 1) if strategy == "SMMG" else s.tab.M
+        dims.append(O.Dims(nt, m, sp_.ndof))
+    pairs = [PB.fd_transfers(specs[l]) for l in range(L - 1)]
+    return O.OMultigrid(s.global_matrix(), dims, O.composite_transfers(dims, pairs), nu, P,
+                        threads=threads)
+
+
+@pytest.mark.parametrize("strategy", ["SMG", "STMG"])
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_c1_mg_matches_reference(golden, strategy, P):
+    g = golden("c1")
+    cfg = PB.baseline_config("C1")
+    np.testing.assert_array_equal(cfg.u0(), g["u0"])
+    s, mg = c1_oracle_mg(cfg, strategy, P)
+    x, rep = mg.solve(s.rhs(), tol_rel=1e-10, tol_abs=1e-10)
+    assert rep.iterations == int(g[f"{strategy}_P{P}_its"])
+    assert per_node_rel(x, g[f"{strategy}_P{P}_x"], (16, 3, 127)) < 1e-10
+
+
+def fd_oracle_pfasst(spec, M, Mc, dt, gamma, mode="implicit", reaction="cubic"):
+    spc = spec.coarse()
+    f_ops, c_ops = PB.fd_space(spec), PB.fd_space(spc)
+    tf, tc = O.tableau(M), O.tableau(Mc)
+    levels = [O.OSdcLevel(tf, f_ops.Kh, f_ops.lumped_diagonal, dt, gamma, mode, reaction),
+              O.OSdcLevel(tc, c_ops.Kh, c_ops.lumped_diagonal, dt, gamma, mode, reaction)]
+    Rs, Ps = PB.fd_transfers(spec)
+    tr = O.OTransfer(Rs, Ps, O.node_eval(tf.nodes, tc.nodes), O.node_eval(tc.nodes, tf.nodes))
+    return levels, [tr]
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_c1_pfasst_matches_reference(golden, P):
+    g = golden("c1")
+    cfg = PB.baseline_config("C1")
+    levels, trs = fd_oracle_pfasst(cfg.spec, 3, 2, cfg.dt, 0.0)
+    x, rep = O.pfasst(levels, trs, 1, cfg.u0(), cfg.Nt, P, tol_rel=1e-10, tol_abs=1e-10)
+    assert rep.iterations == int(g[f"PF_P{P}_its"])
+    assert rep.inner_iterations == g[f"PF_P{P}_inner"].tolist()
+    assert per_node_rel(x, g[f"PF_P{P}_x"], (16, 3, 127)) < 1e-10
+
+
+def test_pfasst_fem1d_matches_reference(golden):
+    g = golden("pfasst_fem1d")
+    u0 = _heat_u0(32)
+    for P in (1, 2, 4):
+        lv, trs = O.fem_pfasst_levels(3, 32, 1.0, 1.0 / 8, 0.0, 2)
+        x, rep = O.pfasst(lv, trs, 1, u0, 8, P, tol_rel=1e-10, tol_abs=1e-10)
+        assert rep.inner_iterations == g[f"heat_P{P}_inner"].tolist()
+        assert per_node_rel(x, g[f"heat_P{P}_x"], (8, 3, 33)) < 1e-10
+    lv, trs = O.fem_pfasst_levels(2, 32, 1.0, 1.0 / 8, 0.0, 3)
+    x, rep = O.pfasst(lv, trs, 1, u0, 8, 4, tol_rel=1e-10, tol_abs=1e-10)
+    assert rep.inner_iterations == g["heatL3_P4_inner"].tolist()
+    assert per_node_rel(x, g["heatL3_P4_x"], (8, 2, 33)) < 1e-10
+    xm = np.linspace(0.0, 10.0, 65)
+    u0m = 2.0 * np.exp(-(((xm - 5.0) / 0.1) ** 2))
+    for mode in ("imex", "implicit"):
+        lv, trs = O.fem_pfasst_levels(2, 64, 10.0, 2.0 / 16, 5.0, 2, mode)
+        x, rep = O.pfasst(lv, trs, 1, u0m, 16, 4, tol_rel=1e-9, tol_abs=1e-9)
+        assert rep.inner_iterations == g[f"mono_{mode}_inner"].tolist()
+        assert per_node_rel(x, g[f"mono_{mode}_x"], (16, 2, 65)) < 1e-9
+
+
+def test_sweep_and_fas_match_reference(golden):
+    g = golden("pfasst_fem1d")
+    lv, trs = O.fem_pfasst_levels(3, 32, 1.0, 1.0 / 8, 0.0, 2)
+    u0 = _heat_u0(32)
+    U = g["sweep_U_in"]
+    np.testing.assert_allclose(lv[0].sweep(U, u0, None), g["sweep_U_out"], atol=1e-12)
+    np.testing.assert_allclose(O.fas_tau(lv[0], lv[1], trs[0], U, None), g["fas_tau"], atol=1e-12)
+    assert abs(lv[0].res_norm(U, u0, None) - float(g["resnorm"])) < 1e-12
+    Kh, mh = O.fem1d_operators(64, 10.0)
+    lm = O.OSdcLevel(O.tableau(3), Kh, mh, 0.05, 5.0, "imex")
+    xm = np.linspace(0.0, 10.0, 65)
+    u0m = 2.0 * np.exp(-(((xm - 5.0) / 0.1) ** 2))
+    np.testing.assert_allclose(lm.sweep(np.tile(u0m, (3, 1)), u0m, None), g["imex_sweep"],
+                               atol=1e-12)
+    Us, rep = O.sdc_step(u0m, lm, tol_rel=1e-10, tol_abs=1e-10)
+    assert rep.iterations == int(g["sdc_step_its"])
+    np.testing.assert_allclose(Us, g["sdc_step_U"], atol=1e-10)
+
+
+def test_newton_matches_reference(golden):
+    g = golden("newton")
+    Kh, mh = O.fem1d_operators(32, 10.0)
+    xm = np.linspace(0.0, 10.0, 33)
+    s = O.OSystem(O.tableau(2), Kh, mh, 8, 2.0, 5.0, 2.0 * np.exp(-(((xm - 5.0) / 0.1) ** 2)))
+    mg = O.fem_hierarchy(s, "SMG", 3, 3)
+    x, rep = O.newton(s, O.mg_newton_solver(mg), tol=1e-9)
+    assert rep.iterations == int(g["its"])
+    assert rep.inner_iterations == g["inner"].tolist()
+    assert rep.damped_steps == int(g["damped"])
+    assert per_node_rel(x, g["x"], (8, 2, 33)) < 1e-9
+
+
+def test_c2_small_matches_reference(golden):
+    g = golden("c2_small")
+    spec = PB.StencilSpec(2, 15, "dirichlet", 1.0)
+    cfg = PB.BaselineConfig("C2", spec, 8, 8 / 64, 3, 2, 0.0, "cubic", 0, "reduced")
+    np.testing.assert_array_equal(cfg.u0(), g["u0"])
+    ops = PB.fd_space(spec)
+    s = O.OSystem(O.tableau(3), ops.Kh, ops.lumped_diagonal, 8, cfg.T, 0.0, cfg.u0())
+    for strat in ("SMG", "STMG"):
+        for P in (1, 4):
+            mg = fd_oracle_hierarchy(s, spec, strat, 3, 3, P)
+            x, rep = mg.solve(s.rhs(), tol_rel=1e-10, tol_abs=1e-10)
+            assert rep.iterations == int(g[f"{strat}_P{P}_its"]), (strat, P)
+            assert per_node_rel(x, g[f"{strat}_P{P}_x"], (8, 3, 225)) < 1e-10
+    levels, trs = fd_oracle_pfasst(spec, 3, 2, cfg.dt, 0.0)
+    x, rep = O.pfasst(levels, trs, 1, cfg.u0(), 8, 4, tol_rel=1e-9, tol_abs=1e-9)
+    assert rep.inner_iterations == g["PF_P4_inner"].tolist()
+    assert per_node_rel(x, g["PF_P4_x"], (8, 3, 225)) < 1e-10
