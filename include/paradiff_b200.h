@@ -1,0 +1,102 @@
+/*
+ * paradiff-b200 C ABI — the drop-in boundary of the B200 hot path.
+ *
+ * The reference (`paradiff`, /root/reference/pkg/src/paradiff) has no FFI: its
+ * seam is Python duck typing.  Each entry point below replaces
+ * one reference interface (cited file:line); the Python package
+ * `paper_2006_12883_b200` binds them with ctypes and keeps the reference's
+ * names, arguments, (Nt, M, S) C-order fp64 layout, SolveReport fields and
+ * exceptions.  Plain pointers and sizes only: device pointers are raw CUDA
+ * global-memory addresses (e.g. torch.Tensor.data_ptr()), host pointers are
+ * marked `host`.  All calls are asynchronous on the context's stream unless
+ * documented as synchronising.
+ *
+ * Status codes: PD_OK, PD_ERR_CONFIG (-> ConfigurationError), PD_ERR_SOLVER
+ * (-> SolverError; pd_last_error_index() carries the row/node), PD_ERR_CUDA.
+ * pd_last_error() returns the calling thread's last message.
+ */
+#ifndef PARADIFF_B200_H
+#define PARADIFF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { PD_OK = 0, PD_ERR_CONFIG = 1, PD_ERR_SOLVER = 2, PD_ERR_CUDA = 3 };
+
+typedef struct pd_solve_report {
+    int32_t iterations; /* V-cycles / GMRES iterations / PFASST max window iterations */
+    int32_t converged;
+    int32_t diverged;
+    int32_t hist_len;   /* entries written to the caller's history buffer */
+} pd_solve_report;
+
+const char *pd_last_error(void);
+int64_t pd_last_error_index(void);
+int pd_version(void);
+
+/* ---- context (one per GPU / rank; single-threaded) -------------------- */
+int pd_ctx_create(int device, void *stream, void **ctx_out);
+int pd_ctx_set_stream(void *ctx, void *stream);
+int pd_ctx_destroy(void *ctx);
+
+/* ---- CSR matrices (replaces scipy CSR `A @ x`, linalg.py:47-60 as_csr/kron
+ *      products, multigrid.py:245,262,286,296; spacetime.py:117-124) -------- */
+int pd_csr_create(void *ctx, int64_t nrows, int64_t ncols, int64_t nnz,
+                  const int64_t *rowptr, const int32_t *col, const double *val,
+                  int device_src, void **csr_out);
+int pd_csr_set_values(void *ctx, void *csr, const double *val, int device_src);
+/* mode 0: y = A x; 1: y = b - A x; 2: y = b + A x (y may alias b) */
+int pd_csr_spmv(void *ctx, void *csr, const double *x, double *y, int mode, const double *b);
+int pd_csr_destroy(void *csr);
+
+/* ---- ILU(0) / block-Jacobi ILU(0) (linalg.py:63-189: _ilu0_factor,
+ *      _ilu0_solve, Ilu0, BlockJacobiPrecond with contiguous n//P ranges) ---- */
+int pd_ilu0_create(void *ctx, void *csr, int nblocks, void **ilu_out); /* synchronising */
+int pd_ilu0_refactor(void *ctx, void *ilu);                            /* synchronising */
+int pd_ilu0_solve(void *ctx, void *ilu, const double *b, double *x);
+int pd_ilu0_levels(void *ilu, int32_t *lower_levels, int32_t *upper_levels); /* host out */
+int pd_ilu0_destroy(void *ilu);
+
+/* ---- dense LU of the coarsest level (linalg.py:196-209 DenseLU) ---------- */
+int pd_dense_lu_create(void *ctx, void *csr, void **lu_out); /* synchronising */
+int pd_dense_lu_solve(void *ctx, void *lu, const double *b, double *x);
+int pd_dense_lu_destroy(void *lu);
+
+/* ---- GMRES (linalg.py:215-311 gmres); ilu may be NULL (no preconditioner),
+ *      x0 may be NULL (zero start).  hist (host, hist_cap doubles) receives
+ *      SolveReport.residual_history.  Synchronising. ------------------------ */
+int pd_gmres(void *ctx, void *A, void *ilu, const double *b, const double *x0, double *x,
+             double tol_rel, double tol_abs, int restart, int max_it,
+             pd_solve_report *rep, double *hist, int hist_cap);
+
+/* ---- space-time multigrid (multigrid.py:197-305 MultigridHierarchy).
+ *      Takes ownership of the level matrices mats[0..L) (Galerkin products,
+ *      multigrid.py:232-233) and of R[0..L-1), P[0..L-1).  ---------------- */
+int pd_mg_create(void *ctx, int nlevels, void **mats, void **R, void **P, int nu,
+                 int partitions, int restart, int smooth_solves, void **mg_out);
+int pd_mg_level_matrix(void *mg, int level, void **csr_out); /* borrowed handle */
+int pd_mg_refactor(void *ctx, void *mg);                     /* after value updates */
+int pd_mg_vcycle(void *ctx, void *mg, const double *b, double *x); /* multigrid.py:268-273 */
+int pd_mg_solve(void *ctx, void *mg, const double *b, double *x, double tol_rel,
+                double tol_abs, int max_cycles, pd_solve_report *rep, double *hist,
+                int hist_cap); /* multigrid.py:275-305; synchronising */
+int pd_mg_destroy(void *mg);
+
+/* ---- space-time residual on CSR operators (spacetime.py:44-50,131-151):
+ *      out = L u - rhs + gamma * MR r(u), MR = I (x) Mqh (may be NULL when
+ *      gamma == 0); kind 0 none, 1 cubic u^3-u, 2 Fisher u^2-u; tmp: 2n doubles */
+int pd_st_residual_csr(void *ctx, void *L, void *MR, double gamma, int kind, const double *u,
+                       const double *rhs, double *out, double *tmp);
+int pd_reaction(void *ctx, int kind, int deriv, const double *u, double *out, int64_t n);
+int pd_axpy_to(void *ctx, double *y, const double *x, const double *d, double s, int64_t n);
+int pd_norm(void *ctx, const double *x, int64_t n, double *host_out); /* synchronising */
+int pd_scale(void *ctx, double *y, const double *x, double s, int64_t n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PARADIFF_B200_H */

@@ -1,0 +1,234 @@
+"""ctypes binding of the native library (`libparadiff_b200.so`, include/paradiff_b200.h).
+
+There is no CPU fallback: if the library is missing or no CUDA device is
+visible, every solver entry point raises.  Device buffers are torch CUDA
+tensors (torch is the allocator/stream plumbing); the C ABI sees raw device
+pointers only.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import ConfigurationError, DeviceError, SolverError
+
+LIB_PATH = Path(__file__).resolve().parent / "libparadiff_b200.so"
+
+PD_OK, PD_ERR_CONFIG, PD_ERR_SOLVER, PD_ERR_CUDA = 0, 1, 2, 3
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_int = ctypes.c_int
+_dbl = ctypes.c_double
+
+
+class SolveReportC(ctypes.Structure):
+    _fields_ = [("iterations", _i32), ("converged", _i32), ("diverged", _i32),
+                ("hist_len", _i32)]
+
+
+_SIGNATURES = {
+    "pd_last_error": (ctypes.c_char_p, []),
+    "pd_last_error_index": (_i64, []),
+    "pd_version": (_int, []),
+    "pd_ctx_create": (_int, [_int, _vp, ctypes.POINTER(_vp)]),
+    "pd_ctx_set_stream": (_int, [_vp, _vp]),
+    "pd_ctx_destroy": (_int, [_vp]),
+    "pd_csr_create": (_int, [_vp, _i64, _i64, _i64, _vp, _vp, _vp, _int, ctypes.POINTER(_vp)]),
+    "pd_csr_set_values": (_int, [_vp, _vp, _vp, _int]),
+    "pd_csr_spmv": (_int, [_vp, _vp, _vp, _vp, _int, _vp]),
+    "pd_csr_destroy": (_int, [_vp]),
+    "pd_ilu0_create": (_int, [_vp, _vp, _int, ctypes.POINTER(_vp)]),
+    "pd_ilu0_refactor": (_int, [_vp, _vp]),
+    "pd_ilu0_solve": (_int, [_vp, _vp, _vp, _vp]),
+    "pd_ilu0_levels": (_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
+    "pd_ilu0_destroy": (_int, [_vp]),
+    "pd_dense_lu_create": (_int, [_vp, _vp, ctypes.POINTER(_vp)]),
+    "pd_dense_lu_solve": (_int, [_vp, _vp, _vp, _vp]),
+    "pd_dense_lu_destroy": (_int, [_vp]),
+    "pd_gmres": (_int, [_vp, _vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _int, _int,
+                        ctypes.POINTER(SolveReportC), _vp, _int]),
+    "pd_mg_create": (_int, [_vp, _int, _vp, _vp, _vp, _int, _int, _int, _int,
+                            ctypes.POINTER(_vp)]),
+    "pd_mg_level_matrix": (_int, [_vp, _int, ctypes.POINTER(_vp)]),
+    "pd_mg_refactor": (_int, [_vp, _vp]),
+    "pd_mg_vcycle": (_int, [_vp, _vp, _vp, _vp]),
+    "pd_mg_solve": (_int, [_vp, _vp, _vp, _vp, _dbl, _dbl, _int, ctypes.POINTER(SolveReportC),
+                           _vp, _int]),
+    "pd_mg_destroy": (_int, [_vp]),
+    "pd_st_residual_csr": (_int, [_vp, _vp, _vp, _dbl, _int, _vp, _vp, _vp, _vp]),
+    "pd_reaction": (_int, [_vp, _int, _int, _vp, _vp, _i64]),
+    "pd_axpy_to": (_int, [_vp, _vp, _vp, _vp, _dbl, _i64]),
+    "pd_norm": (_int, [_vp, _vp, _i64, ctypes.POINTER(_dbl)]),
+    "pd_scale": (_int, [_vp, _vp, _vp, _dbl, _i64]),
+}
+
+_lock = threading.Lock()
+_LIB = None
+
+
+def exported_symbols() -> list[str]:
+    return sorted(_SIGNATURES)
+
+
+def load_library(path: Path | None = None) -> ctypes.CDLL:
+    """Load and type the native library (no GPU needed just to load it)."""
+    global _LIB
+    with _lock:
+        if _LIB is not None and path is None:
+            return _LIB
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise DeviceError(
+                f"native library {p} not built; run `python -c 'import __graft_entry__ as g; "
+                "g.build()'` (no CPU fallback exists)"
+            )
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in _SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _LIB = lib
+        return lib
+
+
+def check(status: int) -> None:
+    if status == PD_OK:
+        return
+    lib = load_library()
+    msg = (lib.pd_last_error() or b"").decode()
+    if status == PD_ERR_CONFIG:
+        raise ConfigurationError(msg)
+    if status == PD_ERR_SOLVER:
+        err = SolverError(msg)
+        err.index = int(lib.pd_last_error_index())
+        raise err
+    raise DeviceError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load_library(), name)(*args))
+
+
+# ------------------------------------------------------------------ device context
+_torch = None
+
+
+def torch_mod():
+    global _torch
+    if _torch is None:
+        import torch
+
+        _torch = torch
+    return _torch
+
+
+class Context:
+    """One native context per CUDA device, bound to torch's current stream."""
+
+    def __init__(self, device: int):
+        torch = torch_mod()
+        self.device = device
+        self.torch_device = torch.device("cuda", device)
+        self._stream = torch.cuda.current_stream(self.torch_device)
+        h = _vp()
+        call("pd_ctx_create", device, _vp(self._stream.cuda_stream), ctypes.byref(h))
+        self.handle = h
+
+    def sync_stream(self) -> None:
+        """Rebind to torch's current stream (cheap; call before enqueueing)."""
+        torch = torch_mod()
+        s = torch.cuda.current_stream(self.torch_device)
+        if s.cuda_stream != self._stream.cuda_stream:
+            self._stream = s
+            call("pd_ctx_set_stream", self.handle, _vp(s.cuda_stream))
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                load_library().pd_ctx_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_contexts: dict[int, Context] = {}
+
+
+def require_cuda() -> None:
+    torch = torch_mod()
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device visible: paradiff-b200 has no CPU fallback")
+
+
+def context(device: int | None = None) -> Context:
+    require_cuda()
+    torch = torch_mod()
+    if device is None:
+        device = torch.cuda.current_device()
+    ctx = _contexts.get(device)
+    if ctx is None:
+        load_library()
+        ctx = Context(device)
+        _contexts[device] = ctx
+    ctx.sync_stream()
+    return ctx
+
+
+# ------------------------------------------------------------------ array helpers
+def ptr(t) -> _vp:
+    return _vp(t.data_ptr()) if t is not None else _vp()
+
+
+def to_device(x, ctx: Context | None = None):
+    """numpy / torch -> contiguous float64 CUDA tensor on the context's device."""
+    torch = torch_mod()
+    ctx = ctx or context()
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=ctx.torch_device, dtype=torch.float64)
+        return t.contiguous()
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    return torch.from_numpy(a).to(ctx.torch_device)
+
+
+def empty(n: int, ctx: Context | None = None):
+    torch = torch_mod()
+    ctx = ctx or context()
+    return torch.empty(int(n), dtype=torch.float64, device=ctx.torch_device)
+
+
+def zeros(n: int, ctx: Context | None = None):
+    torch = torch_mod()
+    ctx = ctx or context()
+    return torch.zeros(int(n), dtype=torch.float64, device=ctx.torch_device)
+
+
+def norm(x, ctx: Context | None = None) -> float:
+    """||x||_2 of a CUDA tensor via the native deterministic reduction."""
+    ctx = ctx or context()
+    out = _dbl()
+    call("pd_norm", ctx.handle, ptr(x), int(x.numel()), ctypes.byref(out))
+    return float(out.value)
+
+
+def scale_into(y, x, s: float, ctx: Context | None = None):
+    ctx = ctx or context()
+    call("pd_scale", ctx.handle, ptr(y), ptr(x), float(s), int(x.numel()))
+    return y
+
+
+def is_tensor(x) -> bool:
+    torch = torch_mod()
+    return isinstance(x, torch.Tensor)
+
+
+def like_input(result, template):
+    """Return a CUDA tensor if the caller passed one, numpy otherwise."""
+    if is_tensor(template):
+        return result
+    return result.cpu().numpy()

@@ -1,0 +1,221 @@
+// extern "C" boundary: status codes, thread-local error text, handle casts.
+#include "../../include/paradiff_b200.h"
+#include "pd_krylov.h"
+
+#include <cstring>
+#include <string>
+
+namespace {
+thread_local std::string g_err;
+thread_local int64_t g_err_index = -1;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return PD_OK;
+    } catch (const pd::ConfigError& e) {
+        g_err = e.what();
+        g_err_index = -1;
+        return PD_ERR_CONFIG;
+    } catch (const pd::SolverError& e) {
+        g_err = e.what();
+        g_err_index = e.index;
+        return PD_ERR_SOLVER;
+    } catch (const pd::CudaError& e) {
+        g_err = e.what();
+        g_err_index = -1;
+        return PD_ERR_CUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        g_err_index = -1;
+        return PD_ERR_CUDA;
+    }
+}
+
+pd::Ctx* C(void* p) {
+    if (!p) throw pd::ConfigError("null context");
+    return static_cast<pd::Ctx*>(p);
+}
+template <class T>
+T* H(void* p, const char* what) {
+    if (!p) throw pd::ConfigError(std::string("null ") + what + " handle");
+    return static_cast<T*>(p);
+}
+
+void fill_report(pd_solve_report* rep, int its, bool conv, bool div,
+                 const std::vector<double>& hist, double* out, int cap) {
+    if (rep) {
+        rep->iterations = its;
+        rep->converged = conv ? 1 : 0;
+        rep->diverged = div ? 1 : 0;
+        rep->hist_len = (int)std::min<size_t>(hist.size(), (size_t)std::max(cap, 0));
+    }
+    if (out && cap > 0)
+        std::memcpy(out, hist.data(), std::min<size_t>(hist.size(), (size_t)cap) * sizeof(double));
+}
+}  // namespace
+
+extern "C" {
+
+const char* pd_last_error(void) { return g_err.c_str(); }
+int64_t pd_last_error_index(void) { return g_err_index; }
+int pd_version(void) { return 1; }
+
+int pd_ctx_create(int device, void* stream, void** out) {
+    return guarded([&] { *out = new pd::Ctx(device, static_cast<cudaStream_t>(stream)); });
+}
+int pd_ctx_set_stream(void* ctx, void* stream) {
+    return guarded([&] { C(ctx)->stream = static_cast<cudaStream_t>(stream); });
+}
+int pd_ctx_destroy(void* ctx) {
+    return guarded([&] { delete static_cast<pd::Ctx*>(ctx); });
+}
+
+int pd_csr_create(void* ctx, int64_t nrows, int64_t ncols, int64_t nnz, const int64_t* rowptr,
+                  const int32_t* col, const double* val, int device_src, void** out) {
+    return guarded([&] {
+        if (nrows < 0 || ncols < 0 || nnz < 0) throw pd::ConfigError("negative CSR size");
+        if (ncols > INT32_MAX) throw pd::ConfigError("column count exceeds int32 index range");
+        *out = pd::csr_upload(*C(ctx), nrows, ncols, nnz, rowptr, col, val, device_src != 0)
+                   .release();
+    });
+}
+int pd_csr_set_values(void* ctx, void* csr, const double* val, int device_src) {
+    return guarded(
+        [&] { pd::csr_update_values(*C(ctx), *H<pd::Csr>(csr, "csr"), val, device_src != 0); });
+}
+int pd_csr_spmv(void* ctx, void* csr, const double* x, double* y, int mode, const double* b) {
+    return guarded([&] {
+        if (mode < 0 || mode > 2) throw pd::ConfigError("bad spmv mode");
+        if (mode != 0 && !b) throw pd::ConfigError("spmv mode needs b");
+        pd::csr_spmv(*C(ctx), *H<pd::Csr>(csr, "csr"), x, y, mode, b);
+    });
+}
+int pd_csr_destroy(void* csr) {
+    return guarded([&] { delete static_cast<pd::Csr*>(csr); });
+}
+
+int pd_ilu0_create(void* ctx, void* csr, int nblocks, void** out) {
+    return guarded(
+        [&] { *out = pd::ilu0_create(*C(ctx), *H<pd::Csr>(csr, "csr"), nblocks).release(); });
+}
+int pd_ilu0_refactor(void* ctx, void* ilu) {
+    return guarded([&] { pd::ilu0_refactor(*C(ctx), *H<pd::Ilu0>(ilu, "ilu")); });
+}
+int pd_ilu0_solve(void* ctx, void* ilu, const double* b, double* x) {
+    return guarded([&] { pd::ilu0_solve(*C(ctx), *H<pd::Ilu0>(ilu, "ilu"), b, x); });
+}
+int pd_ilu0_levels(void* ilu, int32_t* lo, int32_t* up) {
+    return guarded([&] {
+        auto* f = H<pd::Ilu0>(ilu, "ilu");
+        if (lo) *lo = f->nlevels_lo;
+        if (up) *up = f->nlevels_up;
+    });
+}
+int pd_ilu0_destroy(void* ilu) {
+    return guarded([&] { delete static_cast<pd::Ilu0*>(ilu); });
+}
+
+int pd_dense_lu_create(void* ctx, void* csr, void** out) {
+    return guarded(
+        [&] { *out = pd::dense_lu_from_csr(*C(ctx), *H<pd::Csr>(csr, "csr")).release(); });
+}
+int pd_dense_lu_solve(void* ctx, void* lu, const double* b, double* x) {
+    return guarded([&] { pd::dense_lu_solve(*C(ctx), *H<pd::DenseLU>(lu, "lu"), b, x); });
+}
+int pd_dense_lu_destroy(void* lu) {
+    return guarded([&] { delete static_cast<pd::DenseLU*>(lu); });
+}
+
+int pd_gmres(void* ctx, void* A, void* ilu, const double* b, const double* x0, double* x,
+             double tol_rel, double tol_abs, int restart, int max_it, pd_solve_report* rep,
+             double* hist, int hist_cap) {
+    return guarded([&] {
+        pd::Ctx& c = *C(ctx);
+        pd::Csr& M = *H<pd::Csr>(A, "matrix");
+        if (M.nrows != M.ncols) throw pd::ConfigError("GMRES needs a square matrix");
+        if (max_it < 0) throw pd::ConfigError("max_it must be nonnegative");
+        const int64_t n = M.nrows;
+        pd::Gmres g(c, &M, static_cast<pd::Ilu0*>(ilu), n, restart, std::max(max_it, 1));
+        // r0 = b - A x0 (x0 = 0 when absent: r0 = b, exactly as b - A@0)
+        pd::DevBuf<double> r0(std::max<int64_t>(n, 1)), zero;
+        const double* xs = x0;
+        if (!xs) {
+            zero.alloc(std::max<int64_t>(n, 1));
+            pd::vec_fill(c, zero.p, n, 0.0);
+            xs = zero.p;
+        }
+        pd::csr_spmv(c, M, xs, r0.p, pd::SPMV_RESID, b, nullptr, 0, c.scalars.p + 16, nullptr);
+        g.enqueue_init(r0.p, c.scalars.p + 16, tol_rel, tol_abs, x0);
+        pd::GmDev s = g.read_state();
+        // host mirrors (phase, j) after every Arnoldi step; guards cover the rest
+        int slot = 0;
+        while (s.phase != pd::GM_DONE && s.total < std::max(max_it, 1)) {
+            const int j_eff = (s.phase == pd::GM_START) ? 0 : s.j;
+            g.enqueue_slot(slot++, j_eff + 2, b);
+            s = g.read_state();
+        }
+        if (s.err == 1) throw pd::SolverError("non-finite initial residual in GMRES");
+        if (s.err == 2) throw pd::SolverError("non-finite residual in GMRES iteration");
+        if (s.err == 3) throw pd::SolverError("non-finite residual in GMRES restart");
+        // the engine accumulates x = x0 + psolve(V y) per cycle, as the reference
+        if (s.cycles > 0) {
+            pd::vec_copy(c, x, g.x(), n);
+        } else {
+            if (x0) pd::vec_copy(c, x, x0, n);
+            else pd::vec_fill(c, x, n, 0.0);
+        }
+        auto h = g.history(s.total);
+        PD_CUDA(cudaStreamSynchronize(c.stream));
+        fill_report(rep, s.total, s.converged != 0, s.diverged != 0, h, hist, hist_cap);
+    });
+}
+
+int pd_mg_create(void* ctx, int nlevels, void** mats, void** R, void** P, int nu, int partitions,
+                 int restart, int smooth_solves, void** out) {
+    return guarded([&] {
+        if (nlevels < 1) throw pd::ConfigError("need at least one level");
+        std::vector<std::unique_ptr<pd::Csr>> m, r, p;
+        for (int l = 0; l < nlevels; ++l) m.emplace_back(H<pd::Csr>(mats[l], "level matrix"));
+        for (int l = 0; l + 1 < nlevels; ++l) {
+            r.emplace_back(H<pd::Csr>(R[l], "restriction"));
+            p.emplace_back(H<pd::Csr>(P[l], "prolongation"));
+        }
+        *out = new pd::Multigrid(*C(ctx), std::move(m), std::move(r), std::move(p), nu, partitions,
+                                 restart, smooth_solves);
+    });
+}
+int pd_mg_level_matrix(void* mg, int level, void** out) {
+    return guarded([&] {
+        auto* M = H<pd::Multigrid>(mg, "multigrid");
+        if (level < 0 || level >= M->num_levels()) throw pd::ConfigError("bad level index");
+        *out = &M->level_matrix(level);
+    });
+}
+int pd_mg_refactor(void* ctx, void* mg) {
+    (void)ctx;
+    return guarded([&] { H<pd::Multigrid>(mg, "multigrid")->refactor(); });
+}
+int pd_mg_vcycle(void* ctx, void* mg, const double* b, double* x) {
+    return guarded([&] {
+        auto* M = H<pd::Multigrid>(mg, "multigrid");
+        M->enqueue_vcycle(b, x);
+        M->check_errors();
+        if (pd::vec_has_nonfinite(*C(ctx), x, M->fine_size()))
+            throw pd::SolverError("V-cycle produced non-finite values");
+    });
+}
+int pd_mg_solve(void* ctx, void* mg, const double* b, double* x, double tol_rel, double tol_abs,
+                int max_cycles, pd_solve_report* rep, double* hist, int hist_cap) {
+    (void)ctx;
+    return guarded([&] {
+        auto r = H<pd::Multigrid>(mg, "multigrid")->solve(b, x, tol_rel, tol_abs, max_cycles);
+        fill_report(rep, r.iterations, r.converged, r.diverged, r.hist, hist, hist_cap);
+    });
+}
+int pd_mg_destroy(void* mg) {
+    return guarded([&] { delete static_cast<pd::Multigrid*>(mg); });
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// Device-side helpers shared by the paradiff-b200 kernels (sm_100a, fp64).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace pd {
+namespace dev {
+
+// Guarded kernels: the device-resident solver state decides whether a
+// launched kernel does anything, so whole V-cycles run without host syncs
+// (and can be captured into CUDA graphs).
+__device__ __forceinline__ bool guard_off(const int* guard, int want) {
+    return guard != nullptr && *((volatile const int*)guard) != want;
+}
+
+// Loads that bypass L1 (values produced by other SMs inside the same launch).
+__device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ int64_t ldcg(const int64_t* p) {
+    return (int64_t)__ldcg((const long long*)p);
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Wait until flag >= target (monotone epochs).
+__device__ __forceinline__ void wait_flag(const int* f, int target) {
+    while (ld_acquire(f) < target) {
+        __nanosleep(20);
+    }
+}
+
+// Separately rounded multiply/subtract/add: keeps the reference's (non-FMA)
+// rounding so CSR products and ILU factors reproduce scipy/numba bitwise.
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+
+// Deterministic block reduction (fixed tree) of one double.
+template <int BS>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (w == 0) {
+        s = (lane < BS / 32) ? sh[lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    }
+    __syncthreads();
+    return s;  // valid in thread 0
+}
+
+// Grid-wide deterministic sum: each block writes its partial; the last block
+// to arrive sums the partials in index order and stores *out (then resets the
+// counter so the slot can be reused by the next kernel on the stream).
+template <int BS>
+__device__ __forceinline__ void grid_sum_finish(double v, double* partials, unsigned int* counter,
+                                                double* out) {
+    __shared__ double sh[BS / 32];
+    __shared__ bool last;
+    double s = block_sum<BS>(v, sh);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = s;
+        __threadfence();
+        unsigned int prev = atomicAdd(counter, 1u);
+        last = (prev == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double t = 0.0;
+    for (unsigned int i = threadIdx.x; i < gridDim.x; i += BS) t += __ldcg(partials + i);
+    t = block_sum<BS>(t, sh);
+    if (threadIdx.x == 0) {
+        *out = t;
+        *counter = 0u;
+    }
+}
+
+}  // namespace dev
+}  // namespace pd

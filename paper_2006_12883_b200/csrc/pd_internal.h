@@ -1,0 +1,144 @@
+// Internal host-side declarations of the paradiff-b200 native library.
+// Everything crossing the C ABI lives in include/paradiff_b200.h; this header
+// is the C++ runtime's view (contexts, device buffers, solver objects).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace pd {
+
+struct ConfigError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct SolverError : std::runtime_error {
+    int64_t index;
+    explicit SolverError(const std::string& m, int64_t i = -1) : std::runtime_error(m), index(i) {}
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define PD_CUDA(call)                                                                        \
+    do {                                                                                     \
+        cudaError_t pd_e_ = (call);                                                          \
+        if (pd_e_ != cudaSuccess)                                                            \
+            throw ::pd::CudaError(std::string(#call) + ": " + cudaGetErrorString(pd_e_));   \
+    } while (0)
+
+#define PD_LAUNCH_CHECK() PD_CUDA(cudaGetLastError())
+
+// Owning device allocation (cudaMalloc/cudaFree; allocation happens at
+// plan/setup time only, never inside a solve).
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    explicit DevBuf(size_t count) { alloc(count); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        if (count) PD_CUDA(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    T* get() const { return p; }
+};
+
+constexpr int kReduceMaxBlocks = 1024;
+
+// Per-device context: one stream, a reduction workspace and a device
+// property cache.  Single-threaded by contract (one context per GPU/rank).
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sms = 148;
+    DevBuf<double> red_partials;      // kReduceMaxBlocks * 4
+    DevBuf<unsigned int> red_counter; // 4 counters
+    DevBuf<double> scalars;           // small result slots
+    DevBuf<int> flags;                // misc device flags
+    explicit Ctx(int dev, cudaStream_t s);
+    int grid_for(int64_t n, int bs, int per_sm = 8) const;
+};
+
+// CSR on device: int64 row pointers (nnz may exceed 2^31 at C3/C5 sizes),
+// int32 column indices, fp64 values.  Column indices sorted per row.
+struct Csr {
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    DevBuf<int64_t> rowptr;
+    DevBuf<int32_t> col;
+    DevBuf<double> val;
+};
+
+// ILU(0) factors with level schedules (see pd_sparse.cu).
+struct Ilu0 {
+    int64_t n = 0;
+    const Csr* pattern = nullptr;   // pattern source (owned elsewhere) unless masked
+    Csr masked;                     // block-Jacobi masked copy (pattern + values)
+    bool use_masked = false;
+    DevBuf<double> fac;             // factor values on the pattern
+    DevBuf<int64_t> diag;           // diagonal positions
+    DevBuf<int32_t> order_lo;       // rows in lower-solve level order
+    DevBuf<int32_t> order_up;       // rows in upper-solve level order
+    DevBuf<int> flag;               // per-row completion epochs
+    DevBuf<unsigned long long> counter;
+    DevBuf<int> ep;                 // device-resident sweep epoch
+    int nlevels_lo = 0, nlevels_up = 0;
+    std::vector<std::pair<int64_t, int64_t>> ranges;
+    const Csr& pat() const { return use_masked ? masked : *pattern; }
+};
+
+struct DenseLU {
+    int64_t n = 0;
+    DevBuf<double> lu;   // column-major n x n
+    DevBuf<int32_t> piv; // LAPACK-style row interchanges (0-based)
+};
+
+// ------------------------------------------------------------------ kernels (host wrappers)
+// vector ops
+void vec_fill(Ctx& c, double* x, int64_t n, double v);
+void vec_copy(Ctx& c, double* y, const double* x, int64_t n);
+void vec_axpy_inplace(Ctx& c, double* y, const double* x, int64_t n);  // y = y + x
+// out = sqrt(sum x^2) written to device slot; returns nothing (async)
+void vec_dot(Ctx& c, const double* x, const double* y, int64_t n, double* out_dev);
+double vec_norm_host(Ctx& c, const double* x, int64_t n);  // synchronizing helper
+bool vec_has_nonfinite(Ctx& c, const double* x, int64_t n);  // synchronizing
+
+// CSR
+enum SpmvMode { SPMV_SET = 0, SPMV_RESID = 1, SPMV_ADD = 2 };
+void csr_spmv(Ctx& c, const Csr& A, const double* x, double* y, int mode, const double* b,
+              const int* guard = nullptr, int want = 0, double* norm2_out = nullptr,
+              int* nonfinite_flag = nullptr);
+std::unique_ptr<Csr> csr_upload(Ctx& c, int64_t nrows, int64_t ncols, int64_t nnz,
+                                const int64_t* rowptr, const int32_t* col, const double* val,
+                                bool device_src);
+void csr_update_values(Ctx& c, Csr& A, const double* val, bool device_src);
+
+// ILU(0)
+std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks);
+void ilu0_refactor(Ctx& c, Ilu0& f);  // recompute numeric factor from the pattern's values
+void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard = nullptr,
+                int want = 0);
+
+// dense LU
+std::unique_ptr<DenseLU> dense_lu_from_csr(Ctx& c, const Csr& A);
+void dense_lu_solve(Ctx& c, const DenseLU& f, const double* b, double* x);
+
+}  // namespace pd

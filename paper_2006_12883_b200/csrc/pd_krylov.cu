@@ -1,0 +1,475 @@
+// Device-resident GMRES engine and V-cycle runtime (see pd_krylov.h).
+//
+//   Gmres              <- linalg.py:215-311 (restarted, right-preconditioned,
+//                         MGS orthogonalisation, Givens, happy breakdown at
+//                         1e-14*max(1,beta), true-residual check per restart,
+//                         divergence when beta > 10*min)
+//   enqueue_gmres_smooth <- multigrid.py:243-256 (_smooth)
+//   Multigrid          <- multigrid.py:197-305 (_cycle, vcycle, solve)
+//
+// Scalar bookkeeping (Hessenberg, rotations, thresholds) runs in one-thread
+// kernels on the device; vector kernels read the phase word and exit early
+// when their stage is inactive.  The host only enqueues.
+#include "pd_device.cuh"
+#include "pd_krylov.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace pd {
+
+using namespace dev;
+
+constexpr int KB = 256;
+
+__device__ __forceinline__ int vphase(const GmDev* s) { return *((volatile const int*)&s->phase); }
+
+__global__ void k_gm_init(GmDev* s, const double* norm2, double tol_rel, double tol_abs,
+                          int max_it, int restart, double* hist, int has_x0) {
+    const double beta = sqrt(*norm2);
+    s->has_x0 = has_x0;
+    s->max_it = max_it;
+    s->restart = restart;
+    s->tol_rel = tol_rel;
+    s->tol_abs = tol_abs;
+    s->total = 0;
+    s->cycles = 0;
+    s->j = 0;
+    s->k = 0;
+    s->err = 0;
+    s->converged = 0;
+    s->diverged = 0;
+    s->vec_idx = -1;
+    s->vec_slot = -1;
+    s->beta = beta;
+    s->beta0 = beta;
+    s->last_res = beta;
+    if (hist) hist[0] = beta;
+    if (!isfinite(beta)) {
+        s->err = 1;
+        s->phase = GM_DONE;
+        return;
+    }
+    const double thr = fmax(tol_abs, mul(tol_rel, beta));
+    s->thr = thr;
+    s->lowest = beta;
+    if (beta <= thr) {
+        s->converged = 1;
+        s->phase = GM_DONE;
+    } else {
+        s->phase = GM_START;
+    }
+}
+
+// V0 = r / beta (first cycle reads the initial residual r0, restarts read rg)
+__global__ void k_gm_start_vec(const GmDev* s, const double* r0, const double* rg, double* V,
+                               double* vcur, int64_t n) {
+    if (vphase(s) != GM_START) return;
+    const double beta = s->beta;
+    const double* src = s->cycles == 0 ? r0 : rg;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = src[i] / beta;
+        V[i] = v;
+        vcur[i] = v;
+    }
+}
+
+__global__ void k_gm_start(GmDev* s) {
+    if (s->phase != GM_START) return;
+    const int R = s->restart;
+    for (int i = 0; i < (R + 1) * R; ++i) s->H[i] = 0.0;
+    for (int i = 0; i <= R; ++i) s->g[i] = 0.0;
+    s->g[0] = s->beta;
+    s->j = 0;
+    s->phase = GM_RUN;
+}
+
+// MGS pass i: (w -= h_{i-1} V_{i-1}) then dot(w, V_i) (or |w|^2 on the last pass)
+__global__ void k_gm_mgs(GmDev* s, int i, double* w, const double* V, int64_t n,
+                         double* partials, unsigned int* counter) {
+    if (vphase(s) != GM_RUN) return;
+    const int j = s->j;
+    if (i > j + 1) return;
+    double acc = 0.0;
+    if (i == 0) {
+        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+             t += (int64_t)gridDim.x * blockDim.x)
+            acc = fma(w[t], V[t], acc);
+    } else {
+        const double h = s->dots[i - 1];
+        const double* Vp = V + (int64_t)(i - 1) * n;
+        const double* Vi = V + (int64_t)i * n;
+        const bool last = (i == j + 1);
+        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+             t += (int64_t)gridDim.x * blockDim.x) {
+            const double wv = sub(w[t], mul(h, Vp[t]));
+            w[t] = wv;
+            acc = fma(wv, last ? wv : Vi[t], acc);
+        }
+    }
+    grid_sum_finish<KB>(acc, partials, counter, &s->dots[i]);
+}
+
+// Hessenberg column, Givens rotations, residual estimate, stop decision.
+__global__ void k_gm_arnoldi(GmDev* s, int slot, double* hist) {
+    if (s->phase != GM_RUN) return;
+    const int j = s->j, R = s->restart;
+    double* H = s->H;
+#define HH(r, c) H[(r) * R + (c)]
+    for (int i = 0; i <= j; ++i) HH(i, j) = s->dots[i];
+    const double hn = sqrt(s->dots[j + 1]);
+    HH(j + 1, j) = hn;
+    const bool happy = hn <= mul(1e-14, fmax(1.0, s->beta));
+    s->hn = hn;
+    s->vec_idx = happy ? -1 : j + 1;
+    s->vec_slot = slot;
+    for (int i = 0; i < j; ++i) {
+        const double t = add(mul(s->cs[i], HH(i, j)), mul(s->sn[i], HH(i + 1, j)));
+        HH(i + 1, j) = add(mul(-s->sn[i], HH(i, j)), mul(s->cs[i], HH(i + 1, j)));
+        HH(i, j) = t;
+    }
+    const double denom = hypot(HH(j, j), HH(j + 1, j));
+    if (denom == 0.0) {
+        s->cs[j] = 1.0;
+        s->sn[j] = 0.0;
+    } else {
+        s->cs[j] = HH(j, j) / denom;
+        s->sn[j] = HH(j + 1, j) / denom;
+    }
+    HH(j, j) = denom;
+    HH(j + 1, j) = 0.0;
+    s->g[j + 1] = mul(-s->sn[j], s->g[j]);
+    s->g[j] = mul(s->cs[j], s->g[j]);
+    const double res = fabs(s->g[j + 1]);
+    if (!isfinite(res)) {
+        s->err = 2;
+        s->phase = GM_DONE;
+        return;
+    }
+    s->total += 1;
+    s->last_res = res;
+    if (hist) hist[s->total] = res;
+    if (res <= s->thr || happy || s->total >= s->max_it) {
+        s->k = j + 1;
+        s->phase = GM_FINISH;
+    } else {
+        s->j = j + 1;
+    }
+#undef HH
+}
+
+// V[j+1] = w / hn (and the preconditioner input buffer)
+__global__ void k_gm_newvec(const GmDev* s, int slot, const double* w, double* V, double* vcur,
+                            int64_t n) {
+    if (s->vec_slot != slot || s->vec_idx < 0) return;
+    const int ph = vphase(s);
+    if (ph != GM_RUN && ph != GM_FINISH) return;
+    const double hn = s->hn;
+    double* dst = V + (int64_t)s->vec_idx * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double v = w[i] / hn;
+        dst[i] = v;
+        vcur[i] = v;
+    }
+}
+
+// y = H[:k,:k]^{-1} g[:k]  (column-oriented back substitution, dtrsm order)
+__global__ void k_gm_finish_y(GmDev* s) {
+    if (s->phase != GM_FINISH) return;
+    const int k = s->k, R = s->restart;
+    for (int i = 0; i < k; ++i) s->y[i] = s->g[i];
+    for (int c = k - 1; c >= 0; --c) {
+        if (s->y[c] != 0.0) {
+            s->y[c] = s->y[c] / s->H[c * R + c];
+            const double yc = s->y[c];
+            for (int i = 0; i < c; ++i) s->y[i] = sub(s->y[i], mul(yc, s->H[i * R + c]));
+        }
+    }
+}
+
+// u = V[:k]^T y
+__global__ void k_gm_combine(const GmDev* s, const double* V, double* u, int64_t n) {
+    if (vphase(s) != GM_FINISH) return;
+    const int k = s->k;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int l = 0; l < k; ++l) acc = add(acc, mul(s->y[l], V[(int64_t)l * n + i]));
+        u[i] = acc;
+    }
+}
+
+__global__ void k_gm_update_x(const GmDev* s, double* xg, const double* du, int64_t n) {
+    if (vphase(s) != GM_FINISH) return;
+    const bool first = s->cycles == 0 && !s->has_x0;  // x = 0 + du exactly
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        xg[i] = first ? du[i] : add(xg[i], du[i]);
+}
+
+__global__ void k_gm_restart(GmDev* s, const double* norm2, double* hist) {
+    if (s->phase != GM_FINISH) return;
+    const double beta = sqrt(*norm2);
+    s->cycles += 1;
+    if (!isfinite(beta)) {
+        s->err = 3;
+        s->phase = GM_DONE;
+        return;
+    }
+    s->beta = beta;
+    s->last_res = beta;
+    if (hist) hist[s->total] = beta;
+    s->lowest = fmin(s->lowest, beta);
+    if (beta <= s->thr) {
+        s->converged = 1;
+        s->phase = GM_DONE;
+    } else if (s->total >= s->max_it || beta > mul(10.0, s->lowest)) {
+        s->diverged = 1;
+        s->phase = GM_DONE;
+    } else {
+        s->phase = GM_START;
+    }
+}
+
+// x += dx after the smoother's GMRES (x + 0 when no cycle ran)
+__global__ void k_gm_apply(const GmDev* s, double* x, const double* xg, int64_t n) {
+    if (s->cycles == 0) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = add(x[i], xg[i]);
+}
+
+// ------------------------------------------------------------------ Gmres
+Gmres::Gmres(Ctx& c_, const Csr* A_, Ilu0* M_, int64_t n_, int restart_, int max_it_)
+    : c(c_), A(A_), M(M_), n(n_), max_it(max_it_) {
+    restart = std::max<int64_t>(1, std::min<int64_t>(restart_, n_));
+    if (restart > kGmMaxRestart)
+        throw ConfigError("GMRES restart length above " + std::to_string(kGmMaxRestart));
+    st.alloc(1);
+    PD_CUDA(cudaMemset(st.p, 0, sizeof(GmDev)));
+    V.alloc((size_t)(restart + 1) * std::max<int64_t>(n, 1));
+    w.alloc(std::max<int64_t>(n, 1));
+    z.alloc(std::max<int64_t>(n, 1));
+    u.alloc(std::max<int64_t>(n, 1));
+    rg.alloc(std::max<int64_t>(n, 1));
+    xg.alloc(std::max<int64_t>(n, 1));
+    vcur.alloc(std::max<int64_t>(n, 1));
+    norm2.alloc(1);
+    hist.alloc(std::max(max_it, 1) + 2);
+}
+
+void Gmres::enqueue_init(const double* r0_, const double* norm2_dev, double tol_rel,
+                         double tol_abs, const double* x0) {
+    r0 = r0_;
+    if (x0) vec_copy(c, xg.p, x0, n);
+    k_gm_init<<<1, 1, 0, c.stream>>>(st.p, norm2_dev, tol_rel, tol_abs, max_it, restart, hist.p,
+                                     x0 ? 1 : 0);
+    PD_LAUNCH_CHECK();
+}
+
+void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
+    const int g = c.grid_for(n, KB, 8);
+    const int gr = std::min(c.grid_for(n, KB, 4), kReduceMaxBlocks);
+    const int* ph = &st.p->phase;
+    k_gm_start_vec<<<g, KB, 0, c.stream>>>(st.p, r0, rg.p, V.p, vcur.p, n);
+    k_gm_start<<<1, 1, 0, c.stream>>>(st.p);
+    const double* zin = vcur.p;
+    if (M) {
+        ilu0_solve(c, *M, vcur.p, z.p, ph, GM_RUN);
+        zin = z.p;
+    }
+    csr_spmv(c, *A, zin, w.p, SPMV_SET, nullptr, ph, GM_RUN);
+    const int passes = std::min(mgs_passes, restart + 1);
+    for (int i = 0; i < passes; ++i)
+        k_gm_mgs<<<gr, KB, 0, c.stream>>>(st.p, i, w.p, V.p, n, c.red_partials.p,
+                                          c.red_counter.p);
+    k_gm_arnoldi<<<1, 1, 0, c.stream>>>(st.p, slot, hist.p);
+    k_gm_newvec<<<g, KB, 0, c.stream>>>(st.p, slot, w.p, V.p, vcur.p, n);
+    // cycle finish (active only when this step ended the cycle)
+    k_gm_finish_y<<<1, 1, 0, c.stream>>>(st.p);
+    k_gm_combine<<<g, KB, 0, c.stream>>>(st.p, V.p, u.p, n);
+    const double* du = u.p;
+    if (M) {
+        ilu0_solve(c, *M, u.p, z.p, ph, GM_FINISH);
+        du = z.p;
+    }
+    k_gm_update_x<<<g, KB, 0, c.stream>>>(st.p, xg.p, du, n);
+    csr_spmv(c, *A, xg.p, rg.p, SPMV_RESID, b, ph, GM_FINISH, norm2.p, nullptr);
+    k_gm_restart<<<1, 1, 0, c.stream>>>(st.p, norm2.p, hist.p);
+    PD_LAUNCH_CHECK();
+}
+
+GmDev Gmres::read_state() {
+    GmDev h;
+    PD_CUDA(cudaMemcpyAsync(&h, st.p, sizeof(GmDev), cudaMemcpyDeviceToHost, c.stream));
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    return h;
+}
+
+std::vector<double> Gmres::history(int total) {
+    std::vector<double> h(total + 1);
+    PD_CUDA(cudaMemcpyAsync(h.data(), hist.p, (total + 1) * sizeof(double), cudaMemcpyDeviceToHost,
+                            c.stream));
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    return h;
+}
+
+void enqueue_gmres_smooth(Ctx& c, Gmres& g, const Csr& A, const double* b, double* x,
+                          double* r_work, int nu) {
+    const int64_t n = A.nrows;
+    // r = b - A x with |r|^2 (the GMRES initial residual; x0 = 0 so r0 = r)
+    csr_spmv(c, A, x, r_work, SPMV_RESID, b, nullptr, 0, c.scalars.p + 8, nullptr);
+    g.enqueue_init(r_work, c.scalars.p + 8, 1e-13, 0.0);
+    for (int s = 0; s < nu; ++s) g.enqueue_slot(s, s + 2, r_work);
+    k_gm_apply<<<c.grid_for(n, KB, 8), KB, 0, c.stream>>>(g.dev(), x, g.x(), n);
+    PD_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------ Multigrid
+Multigrid::Multigrid(Ctx& c_, std::vector<std::unique_ptr<Csr>> mats,
+                     std::vector<std::unique_ptr<Csr>> R, std::vector<std::unique_ptr<Csr>> P,
+                     int nu_, int partitions_, int restart_, int smooth_solves_)
+    : c(c_), nu(nu_), partitions(partitions_), restart(restart_), smooth_solves(smooth_solves_) {
+    const int L = (int)mats.size();
+    if (L < 1) throw ConfigError("need at least one level");
+    if ((int)R.size() != L - 1 || (int)P.size() != L - 1)
+        throw ConfigError("need one restriction/prolongation per level transition");
+    if (nu < 1) throw ConfigError("need at least one smoothing iteration");
+    lv.resize(L);
+    for (int l = 0; l < L; ++l) {
+        MgLevel& m = lv[l];
+        m.A = std::move(mats[l]);
+        m.n = m.A->nrows;
+        if (m.A->nrows != m.A->ncols) throw ConfigError("level matrices must be square");
+        if (l < L - 1) {
+            m.R = std::move(R[l]);
+            m.P = std::move(P[l]);
+            if (m.R->ncols != m.n || m.P->nrows != m.n)
+                throw ConfigError("transfer shapes do not match level " + std::to_string(l + 1));
+        }
+        if (l > 0) {
+            m.b.alloc(std::max<int64_t>(m.n, 1));
+            m.x.alloc(std::max<int64_t>(m.n, 1));
+        }
+        m.r.alloc(std::max<int64_t>(m.n, 1));
+    }
+    for (int l = 0; l + 1 < L; ++l)
+        if (lv[l].R->nrows != lv[l + 1].n)
+            throw ConfigError("restriction output does not match level " + std::to_string(l + 2));
+    res2.alloc(1);
+    nonfinite.alloc(1);
+    refactor();
+}
+
+void Multigrid::refactor() {
+    const int L = (int)lv.size();
+    for (int l = 0; l + 1 < L; ++l) {
+        MgLevel& m = lv[l];
+        const int blocks = (int)std::min<int64_t>(partitions, m.n);
+        if (!m.pre) {
+            m.pre = ilu0_create(c, *m.A, std::max(blocks, 1));
+            m.gm = std::make_unique<Gmres>(c, m.A.get(), m.pre.get(), m.n,
+                                           std::min(nu, restart), nu);
+        } else {
+            ilu0_refactor(c, *m.pre);
+        }
+    }
+    coarse = dense_lu_from_csr(c, *lv[L - 1].A);
+}
+
+void Multigrid::cycle(int l) {
+    MgLevel& m = lv[l];
+    const int L = (int)lv.size();
+    double* b = m.b.p;
+    double* x = m.x.p;
+    if (l == L - 1) {
+        dense_lu_solve(c, *coarse, b, x);
+        return;
+    }
+    for (int s = 0; s < smooth_solves; ++s) enqueue_gmres_smooth(c, *m.gm, *m.A, b, x, m.r.p, nu);
+    csr_spmv(c, *m.A, x, m.r.p, SPMV_RESID, b);
+    MgLevel& nx = lv[l + 1];
+    csr_spmv(c, *m.R, m.r.p, nx.b.p, SPMV_SET, nullptr);
+    if (l + 1 < L - 1) vec_fill(c, nx.x.p, nx.n, 0.0);
+    cycle(l + 1);
+    csr_spmv(c, *m.P, nx.x.p, x, SPMV_ADD, x);
+    for (int s = 0; s < smooth_solves; ++s) enqueue_gmres_smooth(c, *m.gm, *m.A, b, x, m.r.p, nu);
+}
+
+void Multigrid::enqueue_vcycle(const double* b, double* x) {
+    // level 0 works directly on the caller's vectors
+    MgLevel& m = lv[0];
+    double* sb = m.b.p;
+    double* sx = m.x.p;
+    m.b.p = const_cast<double*>(b);
+    m.x.p = x;
+    try {
+        cycle(0);
+    } catch (...) {
+        m.b.p = sb;
+        m.x.p = sx;
+        throw;
+    }
+    m.b.p = sb;
+    m.x.p = sx;
+}
+
+void Multigrid::check_errors() {
+    const int L = (int)lv.size();
+    std::vector<GmDev> h(L > 1 ? L - 1 : 0);
+    for (int l = 0; l + 1 < L; ++l)
+        PD_CUDA(cudaMemcpyAsync(&h[l], lv[l].gm->dev(), offsetof(GmDev, H),
+                                cudaMemcpyDeviceToHost, c.stream));
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    for (int l = 0; l + 1 < L; ++l) {
+        if (h[l].err == 1) throw SolverError("non-finite initial residual in GMRES");
+        if (h[l].err == 2) throw SolverError("non-finite residual in GMRES iteration");
+        if (h[l].err == 3) throw SolverError("non-finite residual in GMRES restart");
+    }
+}
+
+Multigrid::Report Multigrid::solve(const double* b, double* x, double tol_rel, double tol_abs,
+                                   int max_cycles) {
+    Report rep;
+    MgLevel& f = lv[0];
+    const int64_t n = f.n;
+    double* r = f.r.p;
+    csr_spmv(c, *f.A, x, r, SPMV_RESID, b, nullptr, 0, res2.p, nullptr);
+    double h2 = 0.0;
+    PD_CUDA(cudaMemcpyAsync(&h2, res2.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    double res = std::sqrt(h2);
+    rep.hist.push_back(res);
+    const double thr = std::max(tol_abs, tol_rel * res);
+    double lowest = res;
+    while (res > thr) {
+        if (rep.iterations >= max_cycles) {
+            rep.diverged = true;
+            break;
+        }
+        enqueue_vcycle(b, x);
+        PD_CUDA(cudaMemsetAsync(nonfinite.p, 0, sizeof(int), c.stream));
+        csr_spmv(c, *f.A, x, r, SPMV_RESID, b, nullptr, 0, res2.p, nonfinite.p);
+        int bad = 0;
+        PD_CUDA(cudaMemcpyAsync(&h2, res2.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        PD_CUDA(cudaMemcpyAsync(&bad, nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+        check_errors();  // synchronises
+        if (bad) throw SolverError("V-cycle produced non-finite values");
+        res = std::sqrt(h2);
+        rep.iterations += 1;
+        rep.hist.push_back(res);
+        if (!std::isfinite(res) || res > 10.0 * lowest) {
+            rep.diverged = true;
+            break;
+        }
+        lowest = std::min(lowest, res);
+    }
+    rep.converged = res <= thr;
+    (void)n;
+    return rep;
+}
+
+}  // namespace pd

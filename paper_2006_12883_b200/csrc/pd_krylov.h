@@ -1,0 +1,95 @@
+// Device-resident restarted GMRES (right preconditioning, MGS, Givens) and the
+// space-time multigrid V-cycle built on it.  Host C++ only enqueues kernels;
+// all control decisions of linalg.py:215-311 live in a device struct, so a
+// smoother pass (multigrid.py:243-256) needs no host synchronisation.
+#pragma once
+
+#include "pd_internal.h"
+
+namespace pd {
+
+constexpr int kGmMaxRestart = 64;
+enum GmPhase { GM_START = 0, GM_RUN = 1, GM_FINISH = 2, GM_DONE = 3 };
+
+struct GmDev {
+    int phase, j, k, total, cycles, vec_idx, vec_slot, err, converged, diverged, max_it, restart,
+        has_x0;
+    double beta, thr, lowest, hn, last_res, tol_rel, tol_abs, beta0;
+    double H[(kGmMaxRestart + 1) * kGmMaxRestart];  // row-major (restart+1) x restart
+    double cs[kGmMaxRestart], sn[kGmMaxRestart], g[kGmMaxRestart + 1], y[kGmMaxRestart];
+    double dots[kGmMaxRestart + 2];
+};
+
+class Gmres {
+   public:
+    Gmres(Ctx& c, const Csr* A, Ilu0* M, int64_t n, int restart, int max_it);
+    // init from r0 = b - A x0 whose squared norm is at *norm2_dev; x0 may be
+    // null (zero start, as in the smoother)
+    void enqueue_init(const double* r0, const double* norm2_dev, double tol_rel, double tol_abs,
+                      const double* x0 = nullptr);
+    // one Arnoldi step slot (mgs_passes = max j + 2 this slot can need) plus
+    // the guarded cycle-finish block; `b` = the GMRES right-hand side
+    void enqueue_slot(int slot, int mgs_passes, const double* b);
+    GmDev read_state();  // synchronising
+    double* x() { return xg.p; }
+    int64_t size() const { return n; }
+    GmDev* dev() { return st.p; }
+    std::vector<double> history(int total);
+
+   private:
+    Ctx& c;
+    const Csr* A;
+    Ilu0* M;
+    int64_t n;
+    int restart, max_it;
+    DevBuf<GmDev> st;
+    DevBuf<double> V, w, z, u, rg, xg, vcur, norm2, hist;
+    const double* r0 = nullptr;
+};
+
+// Enqueue x += GMRES(A, b - A x) with ILU/block-Jacobi right preconditioning,
+// restart=min(nu,restart), max_it=nu, tol_rel=1e-13, tol_abs=0: exactly one
+// smoothing solve of multigrid.py:243-256.  No host synchronisation.
+void enqueue_gmres_smooth(Ctx& c, Gmres& g, const Csr& A, const double* b, double* x,
+                          double* r_work, int nu);
+
+struct MgLevel {
+    std::unique_ptr<Csr> A, R, P;  // R/P: transfer to the next coarser level (unused on coarsest)
+    std::unique_ptr<Ilu0> pre;
+    std::unique_ptr<Gmres> gm;
+    DevBuf<double> b, x, r;
+    int64_t n = 0;
+};
+
+class Multigrid {
+   public:
+    Multigrid(Ctx& c, std::vector<std::unique_ptr<Csr>> mats, std::vector<std::unique_ptr<Csr>> R,
+              std::vector<std::unique_ptr<Csr>> P, int nu, int partitions, int restart,
+              int smooth_solves);
+    // replace level matrix values (same patterns) and refactor (Newton refresh)
+    void refactor();
+    Csr& level_matrix(int l) { return *lv[l].A; }
+    int num_levels() const { return (int)lv.size(); }
+    int64_t fine_size() const { return lv[0].n; }
+    // x <- V-cycle(b, x)  (device pointers, n = fine size); no host sync
+    void enqueue_vcycle(const double* b, double* x);
+    // full solve; returns iterations/flags, fills history; x in/out
+    struct Report {
+        int iterations = 0;
+        bool converged = false, diverged = false;
+        std::vector<double> hist;
+    };
+    Report solve(const double* b, double* x, double tol_rel, double tol_abs, int max_cycles);
+    void check_errors();  // synchronising: raise SolverError on device-side failures
+
+   private:
+    void cycle(int l);
+    Ctx& c;
+    std::vector<MgLevel> lv;
+    std::unique_ptr<DenseLU> coarse;
+    int nu, partitions, restart, smooth_solves;
+    DevBuf<double> res2;
+    DevBuf<int> nonfinite;
+};
+
+}  // namespace pd

@@ -1,0 +1,687 @@
+// Sparse and dense linear-algebra kernels of the P-ref (reference-exact) path.
+//
+//   csr_spmv      <- scipy csr_matvec used by every `A @ x` in multigrid.py /
+//                    linalg.py (row sums in CSR order, separately rounded, so
+//                    the products reproduce scipy bitwise)
+//   ilu0_*        <- linalg.py:63-145 (_ilu0_factor/_ilu0_solve/Ilu0) and the
+//                    block-Jacobi masking of linalg.py:152-189
+//   dense_lu_*    <- linalg.py:196-209 (LAPACK getrf/getrs on the coarsest level)
+//
+// ILU(0) on the GPU: the dependency DAG of the CSR pattern is analysed once
+// (sync-free, per-row level = 1 + max level of its lower/upper neighbours),
+// rows are radix-sorted by level, and factor/solve kernels process rows in
+// that order with per-row completion flags (acquire/release).  Rows are
+// fetched dynamically in topological order, so every waited-on row is owned
+// by a thread that is already running: no deadlock for any grid size.  Each
+// row's arithmetic follows the reference's sequential order exactly.
+#include "pd_device.cuh"
+#include "pd_internal.h"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+namespace pd {
+
+using namespace dev;
+
+Ctx::Ctx(int dev_, cudaStream_t s) : device(dev_), stream(s) {
+    PD_CUDA(cudaSetDevice(device));
+    PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+    red_partials.alloc(kReduceMaxBlocks * 4);
+    red_counter.alloc(4);
+    PD_CUDA(cudaMemset(red_counter.p, 0, 4 * sizeof(unsigned int)));
+    scalars.alloc(64);
+    flags.alloc(64);
+    PD_CUDA(cudaMemset(flags.p, 0, 64 * sizeof(int)));
+}
+
+int Ctx::grid_for(int64_t n, int bs, int per_sm) const {
+    int64_t g = (n + bs - 1) / bs;
+    int64_t cap = (int64_t)sms * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+// ------------------------------------------------------------------ vector kernels
+constexpr int BS = 256;
+
+__global__ void k_fill(double* x, int64_t n, double v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = v;
+}
+
+__global__ void k_axpy_inplace(double* y, const double* x, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = add(y[i], x[i]);
+}
+
+__global__ void k_dot(const double* x, const double* y, int64_t n, double* partials,
+                      unsigned int* counter, double* out) {
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        s = fma(x[i], y[i], s);
+    grid_sum_finish<BS>(s, partials, counter, out);
+}
+
+__global__ void k_nonfinite(const double* x, int64_t n, int* flag) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        if (!isfinite(x[i])) bad = true;
+    if (bad) atomicOr(flag, 1);
+}
+
+bool vec_has_nonfinite(Ctx& c, const double* x, int64_t n) {
+    PD_CUDA(cudaMemsetAsync(c.flags.p, 0, sizeof(int), c.stream));
+    if (n > 0) k_nonfinite<<<c.grid_for(n, BS), BS, 0, c.stream>>>(x, n, c.flags.p);
+    int h = 0;
+    PD_CUDA(cudaMemcpyAsync(&h, c.flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    return h != 0;
+}
+
+void vec_fill(Ctx& c, double* x, int64_t n, double v) {
+    if (n <= 0) return;
+    k_fill<<<c.grid_for(n, BS), BS, 0, c.stream>>>(x, n, v);
+    PD_LAUNCH_CHECK();
+}
+
+void vec_copy(Ctx& c, double* y, const double* x, int64_t n) {
+    if (n <= 0 || y == x) return;
+    PD_CUDA(cudaMemcpyAsync(y, x, n * sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+}
+
+void vec_axpy_inplace(Ctx& c, double* y, const double* x, int64_t n) {
+    if (n <= 0) return;
+    k_axpy_inplace<<<c.grid_for(n, BS), BS, 0, c.stream>>>(y, x, n);
+    PD_LAUNCH_CHECK();
+}
+
+void vec_dot(Ctx& c, const double* x, const double* y, int64_t n, double* out_dev) {
+    int g = std::min(c.grid_for(n, BS, 4), kReduceMaxBlocks);
+    k_dot<<<g, BS, 0, c.stream>>>(x, y, n, c.red_partials.p, c.red_counter.p, out_dev);
+    PD_LAUNCH_CHECK();
+}
+
+double vec_norm_host(Ctx& c, const double* x, int64_t n) {
+    vec_dot(c, x, x, n, c.scalars.p);
+    double h = 0.0;
+    PD_CUDA(cudaMemcpyAsync(&h, c.scalars.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    return std::sqrt(h);
+}
+
+// ------------------------------------------------------------------ CSR SpMV
+// One thread per row, CSR order, sum starting at 0.0 like scipy's csr_matvec.
+// mode: 0 y = Ax, 1 y = b - Ax, 2 y = b + Ax.  Optional fused sum of y^2 and a
+// non-finite flag on x (the V-cycle's isfinite check, multigrid.py:271).
+template <bool REDUCE>
+__global__ void k_spmv(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                       const double* __restrict__ v, const double* __restrict__ x,
+                       double* y, int mode, const double* b,  // y may alias b (x += P xc)
+                       const int* guard, int want, double* partials, unsigned int* counter,
+                       double* norm2, int* nonfinite) {
+    if (guard_off(guard, want)) return;
+    double acc2 = 0.0;
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        const int64_t e = rp[i + 1];
+        for (int64_t p = rp[i]; p < e; ++p) s = add(s, mul(v[p], x[ci[p]]));
+        double out = s;
+        if (mode == 1) out = sub(b[i], s);
+        else if (mode == 2) out = add(b[i], s);
+        y[i] = out;
+        if (REDUCE) {
+            acc2 = fma(out, out, acc2);
+            if (nonfinite && !isfinite(x[i])) bad = true;
+        }
+    }
+    if (REDUCE) {
+        if (bad) atomicOr(nonfinite, 1);
+        grid_sum_finish<BS>(acc2, partials, counter, norm2);
+    }
+}
+
+void csr_spmv(Ctx& c, const Csr& A, const double* x, double* y, int mode, const double* b,
+              const int* guard, int want, double* norm2_out, int* nonfinite_flag) {
+    if (A.nrows <= 0) return;
+    if (norm2_out) {
+        int g = std::min(c.grid_for(A.nrows, BS, 8), kReduceMaxBlocks);
+        k_spmv<true><<<g, BS, 0, c.stream>>>(A.nrows, A.rowptr.p, A.col.p, A.val.p, x, y, mode,
+                                             b, guard, want, c.red_partials.p, c.red_counter.p,
+                                             norm2_out, nonfinite_flag);
+    } else {
+        int g = c.grid_for(A.nrows, BS, 16);
+        k_spmv<false><<<g, BS, 0, c.stream>>>(A.nrows, A.rowptr.p, A.col.p, A.val.p, x, y, mode,
+                                              b, guard, want, nullptr, nullptr, nullptr, nullptr);
+    }
+    PD_LAUNCH_CHECK();
+}
+
+std::unique_ptr<Csr> csr_upload(Ctx& c, int64_t nrows, int64_t ncols, int64_t nnz,
+                                const int64_t* rowptr, const int32_t* col, const double* val,
+                                bool device_src) {
+    auto A = std::make_unique<Csr>();
+    A->nrows = nrows;
+    A->ncols = ncols;
+    A->nnz = nnz;
+    A->rowptr.alloc(nrows + 1);
+    A->col.alloc(std::max<int64_t>(nnz, 1));
+    A->val.alloc(std::max<int64_t>(nnz, 1));
+    auto kind = device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    PD_CUDA(cudaMemcpyAsync(A->rowptr.p, rowptr, (nrows + 1) * sizeof(int64_t), kind, c.stream));
+    if (nnz) {
+        PD_CUDA(cudaMemcpyAsync(A->col.p, col, nnz * sizeof(int32_t), kind, c.stream));
+        PD_CUDA(cudaMemcpyAsync(A->val.p, val, nnz * sizeof(double), kind, c.stream));
+    }
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    return A;
+}
+
+void csr_update_values(Ctx& c, Csr& A, const double* val, bool device_src) {
+    if (!A.nnz) return;
+    PD_CUDA(cudaMemcpyAsync(A.val.p, val, A.nnz * sizeof(double),
+                            device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                            c.stream));
+}
+
+// ------------------------------------------------------------------ block-Jacobi masking
+// Keep only entries whose column lies in the row's block (linalg.py:166-171:
+// A[r0:r1, r0:r1] per block).  ILU(0) of the block-diagonal matrix equals the
+// per-block ILU(0)s exactly, so one factorization serves all blocks.
+__device__ __forceinline__ int64_t block_of(int64_t i, int64_t size, int64_t nblocks) {
+    int64_t b = i / size;
+    return b < nblocks - 1 ? b : nblocks - 1;
+}
+
+__global__ void k_mask_count(int64_t n, const int64_t* rp, const int32_t* ci, int64_t size,
+                             int64_t nblocks, int64_t* cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t bi = block_of(i, size, nblocks), k = 0;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+            if (block_of(ci[p], size, nblocks) == bi) ++k;
+        cnt[i + 1] = k;
+    }
+}
+
+__global__ void k_mask_copy(int64_t n, const int64_t* rp, const int32_t* ci, const double* v,
+                            int64_t size, int64_t nblocks, const int64_t* orp, int32_t* oci,
+                            double* ov) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t bi = block_of(i, size, nblocks), q = orp[i];
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+            if (block_of(ci[p], size, nblocks) == bi) {
+                oci[q] = ci[p];
+                ov[q] = v[p];
+                ++q;
+            }
+    }
+}
+
+// ------------------------------------------------------------------ level analysis
+__device__ __forceinline__ int64_t fetch_batch(unsigned long long* counter) {
+    __shared__ long long base;
+    if (threadIdx.x == 0) base = (long long)atomicAdd(counter, (unsigned long long)blockDim.x);
+    __syncthreads();
+    long long b = base;
+    __syncthreads();
+    return b;
+}
+
+// level[i] = 1 + max(level of lower neighbours); natural order fetch.
+__global__ void k_levels_lower(int64_t n, const int64_t* rp, const int32_t* ci, int* level,
+                               unsigned long long* counter) {
+    for (;;) {
+        int64_t base = fetch_batch(counter);
+        if (base >= n) return;
+        int64_t i = base + threadIdx.x;
+        if (i < n) {
+            int lev = 0;
+            for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+                int64_t cc = ci[p];
+                if (cc >= i) break;
+                int lc;
+                while ((lc = ld_acquire(level + cc)) < 0) __nanosleep(32);
+                lev = max(lev, lc + 1);
+            }
+            st_release(level + i, lev);
+        }
+    }
+}
+
+// upper DAG: row i depends on its columns > i; processed from the last row.
+__global__ void k_levels_upper(int64_t n, const int64_t* rp, const int32_t* ci, int* level,
+                               unsigned long long* counter) {
+    for (;;) {
+        int64_t base = fetch_batch(counter);
+        if (base >= n) return;
+        int64_t t = base + threadIdx.x;
+        if (t < n) {
+            int64_t i = n - 1 - t;
+            int lev = 0;
+            for (int64_t p = rp[i + 1] - 1; p >= rp[i]; --p) {
+                int64_t cc = ci[p];
+                if (cc <= i) break;
+                int lc;
+                while ((lc = ld_acquire(level + cc)) < 0) __nanosleep(32);
+                lev = max(lev, lc + 1);
+            }
+            st_release(level + i, lev);
+        }
+    }
+}
+
+__global__ void k_iota(int32_t* x, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = (int32_t)i;
+}
+
+__global__ void k_fill_int(int* x, int64_t n, int v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = v;
+}
+
+__global__ void k_max_int(const int* x, int64_t n, int* out) {
+    int m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, x[i]);
+    atomicMax(out, m);
+}
+
+// ------------------------------------------------------------------ ILU(0) factorization
+// Per row, exactly linalg.py:73-96: for each lower entry k (ascending):
+// l_ik = a_ik / u_kk; a_ij -= l_ik * u_kj over the intersection of row k's
+// upper pattern with row i (two-pointer merge instead of the position map).
+__global__ void k_ilu0_factor(int64_t n, const int64_t* __restrict__ rp,
+                              const int32_t* __restrict__ ci, double* fac, int64_t* diag,
+                              const int32_t* __restrict__ order, int* flag, const int* ep,
+                              unsigned long long* counter, unsigned long long* bad) {
+    const int epoch = *((volatile const int*)ep);
+    for (;;) {
+        int64_t base = fetch_batch(counter);
+        if (base >= n) return;
+        int64_t t = base + threadIdx.x;
+        if (t < n) {
+            const int64_t i = order[t];
+            const int64_t a = rp[i], e = rp[i + 1];
+            int64_t d = -1;
+            for (int64_t p = a; p < e; ++p)
+                if (ci[p] == i) { d = p; break; }
+            unsigned long long mybad = ~0ull;
+            for (int64_t pk = a; pk < e; ++pk) {
+                const int64_t k = ci[pk];
+                if (k >= i) break;
+                wait_flag(flag + k, epoch);
+                const int64_t dk = ldcg(diag + k);
+                const double ukk = ldcg(fac + dk);
+                if (ukk == 0.0 && mybad == ~0ull) mybad = (unsigned long long)k;
+                const double lik = fac[pk] / ukk;
+                fac[pk] = lik;
+                const int64_t ke = rp[k + 1];
+                int64_t q = pk + 1;
+                for (int64_t p = dk + 1; p < ke; ++p) {
+                    const int32_t cp = ci[p];
+                    while (q < e && ci[q] < cp) ++q;
+                    if (q >= e) break;
+                    if (ci[q] == cp) fac[q] = sub(fac[q], mul(lik, ldcg(fac + p)));
+                }
+            }
+            if (mybad == ~0ull && (d < 0 || fac[d] == 0.0)) mybad = (unsigned long long)i;
+            if (mybad != ~0ull) atomicMin(bad, mybad);
+            diag[i] = d < 0 ? a : d;  // keep a valid index; error is reported
+            __threadfence();
+            st_release(flag + i, epoch);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ ILU(0) triangular solves
+// lower: x_i = b_i - sum_{p < diag} L_p x_col (unit diagonal), linalg.py:104-108
+__global__ void k_trsv_lower(int64_t n, const int64_t* __restrict__ rp,
+                             const int32_t* __restrict__ ci, const double* __restrict__ fac,
+                             const int64_t* __restrict__ diag, const int32_t* __restrict__ order,
+                             const double* __restrict__ b, double* x, int* flag, const int* ep,
+                             unsigned long long* counter, const int* guard, int want) {
+    if (guard_off(guard, want)) return;
+    const int epoch = *((volatile const int*)ep);
+    for (;;) {
+        int64_t base = fetch_batch(counter);
+        if (base >= n) return;
+        int64_t t = base + threadIdx.x;
+        if (t < n) {
+            const int64_t i = order[t];
+            double s = b[i];
+            const int64_t d = diag[i];
+            for (int64_t p = rp[i]; p < d; ++p) {
+                const int32_t cc = ci[p];
+                wait_flag(flag + cc, epoch);
+                s = sub(s, mul(fac[p], ldcg(x + cc)));
+            }
+            x[i] = s;
+            __threadfence();
+            st_release(flag + i, epoch);
+        }
+    }
+}
+
+// upper: x_i = (x_i - sum_{p > diag} U_p x_col) / U_diag, linalg.py:109-113
+__global__ void k_trsv_upper(int64_t n, const int64_t* __restrict__ rp,
+                             const int32_t* __restrict__ ci, const double* __restrict__ fac,
+                             const int64_t* __restrict__ diag, const int32_t* __restrict__ order,
+                             double* x, int* flag, const int* ep, unsigned long long* counter,
+                             const int* guard, int want) {
+    if (guard_off(guard, want)) return;
+    const int epoch = *((volatile const int*)ep);
+    for (;;) {
+        int64_t base = fetch_batch(counter);
+        if (base >= n) return;
+        int64_t t = base + threadIdx.x;
+        if (t < n) {
+            const int64_t i = order[t];
+            const int64_t d = diag[i];
+            double s = ldcg(x + i);
+            const int64_t e = rp[i + 1];
+            for (int64_t p = d + 1; p < e; ++p) {
+                const int32_t cc = ci[p];
+                wait_flag(flag + cc, epoch);
+                s = sub(s, mul(fac[p], ldcg(x + cc)));
+            }
+            x[i] = s / fac[d];
+            __threadfence();
+            st_release(flag + i, epoch);
+        }
+    }
+}
+
+// Starts one sync-free sweep: bumps the device-resident epoch (so CUDA-graph
+// replays never see stale completion flags) and rewinds the task counter.
+__global__ void k_begin_sweep(int* ep, unsigned long long* c, const int* guard, int want) {
+    if (guard_off(guard, want)) return;
+    *c = 0ull;
+    *ep = *ep + 1;
+}
+
+static void sort_by_level(Ctx& c, int* level, int64_t n, DevBuf<int32_t>& order, int& nlev) {
+    DevBuf<int> level_sorted(n);
+    DevBuf<int32_t> idx(n);
+    order.alloc(n);
+    k_iota<<<c.grid_for(n, BS), BS, 0, c.stream>>>(idx.p, n);
+    // number of key bits from the max level
+    DevBuf<int> mx(1);
+    PD_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), c.stream));
+    k_max_int<<<c.grid_for(n, BS), BS, 0, c.stream>>>(level, n, mx.p);
+    int hmax = 0;
+    PD_CUDA(cudaMemcpyAsync(&hmax, mx.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    nlev = hmax + 1;
+    int bits = 1;
+    while ((1 << bits) <= hmax) ++bits;
+    size_t tmp_bytes = 0;
+    PD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, level, level_sorted.p, idx.p,
+                                            order.p, (int64_t)n, 0, bits, c.stream));
+    DevBuf<unsigned char> tmp(tmp_bytes);
+    PD_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, tmp_bytes, level, level_sorted.p, idx.p,
+                                            order.p, (int64_t)n, 0, bits, c.stream));
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks) {
+    if (A.nrows != A.ncols) throw ConfigError("ILU(0) needs a square matrix");
+    const int64_t n = A.nrows;
+    if (nblocks < 1 || nblocks > std::max<int64_t>(n, 1))
+        throw ConfigError("num_blocks must be in [1, " + std::to_string(n) + "], got " +
+                          std::to_string(nblocks));
+    auto f = std::make_unique<Ilu0>();
+    f->n = n;
+    f->pattern = &A;
+    const int64_t size = n / nblocks;
+    for (int b = 0; b < nblocks; ++b)
+        f->ranges.emplace_back(b * size, b < nblocks - 1 ? (b + 1) * size : n);
+    if (nblocks > 1) {
+        f->use_masked = true;
+        Csr& M = f->masked;
+        M.nrows = M.ncols = n;
+        M.rowptr.alloc(n + 1);
+        PD_CUDA(cudaMemsetAsync(M.rowptr.p, 0, sizeof(int64_t), c.stream));
+        k_mask_count<<<c.grid_for(n, BS), BS, 0, c.stream>>>(n, A.rowptr.p, A.col.p, size,
+                                                             nblocks, M.rowptr.p);
+        size_t tb = 0;
+        PD_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, M.rowptr.p, M.rowptr.p, n + 1,
+                                              c.stream));
+        DevBuf<unsigned char> tmp(tb);
+        PD_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, M.rowptr.p, M.rowptr.p, n + 1,
+                                              c.stream));
+        PD_CUDA(cudaMemcpyAsync(&M.nnz, M.rowptr.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                c.stream));
+        PD_CUDA(cudaStreamSynchronize(c.stream));
+        M.col.alloc(std::max<int64_t>(M.nnz, 1));
+        M.val.alloc(std::max<int64_t>(M.nnz, 1));
+        k_mask_copy<<<c.grid_for(n, BS), BS, 0, c.stream>>>(n, A.rowptr.p, A.col.p, A.val.p,
+                                                            size, nblocks, M.rowptr.p, M.col.p,
+                                                            M.val.p);
+        PD_LAUNCH_CHECK();
+    }
+    const Csr& P = f->pat();
+    f->fac.alloc(std::max<int64_t>(P.nnz, 1));
+    f->diag.alloc(std::max<int64_t>(n, 1));
+    f->flag.alloc(std::max<int64_t>(n, 1));
+    f->counter.alloc(1);
+    f->ep.alloc(1);
+    PD_CUDA(cudaMemsetAsync(f->flag.p, 0, std::max<int64_t>(n, 1) * sizeof(int), c.stream));
+    PD_CUDA(cudaMemsetAsync(f->ep.p, 0, sizeof(int), c.stream));
+    if (n > 0) {
+        DevBuf<int> level(n);
+        int g = c.grid_for(n, BS, 8);
+        // lower levels
+        k_fill_int<<<c.grid_for(n, BS), BS, 0, c.stream>>>(level.p, n, -1);
+        PD_CUDA(cudaMemsetAsync(f->counter.p, 0, sizeof(unsigned long long), c.stream));
+        k_levels_lower<<<g, BS, 0, c.stream>>>(n, P.rowptr.p, P.col.p, level.p, f->counter.p);
+        PD_LAUNCH_CHECK();
+        sort_by_level(c, level.p, n, f->order_lo, f->nlevels_lo);
+        k_fill_int<<<c.grid_for(n, BS), BS, 0, c.stream>>>(level.p, n, -1);
+        PD_CUDA(cudaMemsetAsync(f->counter.p, 0, sizeof(unsigned long long), c.stream));
+        k_levels_upper<<<g, BS, 0, c.stream>>>(n, P.rowptr.p, P.col.p, level.p, f->counter.p);
+        PD_LAUNCH_CHECK();
+        sort_by_level(c, level.p, n, f->order_up, f->nlevels_up);
+    }
+    ilu0_refactor(c, *f);
+    return f;
+}
+
+void ilu0_refactor(Ctx& c, Ilu0& f) {
+    const Csr& P = f.pat();
+    const int64_t n = f.n;
+    if (n == 0) return;
+    if (f.use_masked) {
+        // refresh masked values from the source matrix (pattern unchanged)
+        const Csr& A = *f.pattern;
+        const int64_t size = n / (int64_t)f.ranges.size();
+        k_mask_copy<<<c.grid_for(n, BS), BS, 0, c.stream>>>(
+            n, A.rowptr.p, A.col.p, A.val.p, size, (int64_t)f.ranges.size(), P.rowptr.p,
+            f.masked.col.p, f.masked.val.p);
+        PD_LAUNCH_CHECK();
+    }
+    PD_CUDA(cudaMemcpyAsync(f.fac.p, P.val.p, P.nnz * sizeof(double), cudaMemcpyDeviceToDevice,
+                            c.stream));
+    DevBuf<unsigned long long> bad(1);
+    PD_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), c.stream));
+    k_begin_sweep<<<1, 1, 0, c.stream>>>(f.ep.p, f.counter.p, nullptr, 0);
+    k_ilu0_factor<<<c.grid_for(n, BS, 8), BS, 0, c.stream>>>(n, P.rowptr.p, P.col.p, f.fac.p,
+                                                              f.diag.p, f.order_lo.p, f.flag.p,
+                                                              f.ep.p, f.counter.p, bad.p);
+    PD_LAUNCH_CHECK();
+    unsigned long long hbad = 0;
+    PD_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(hbad), cudaMemcpyDeviceToHost, c.stream));
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    if (hbad != ~0ull) {
+        int64_t row = (int64_t)hbad;
+        if (f.use_masked) {  // report the row relative to its block (per-block Ilu0)
+            for (auto& r : f.ranges)
+                if (row >= r.first && row < r.second) { row -= r.first; break; }
+        }
+        throw SolverError("zero pivot in ILU(0) at row " + std::to_string(row), row);
+    }
+}
+
+void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int want) {
+    const int64_t n = f.n;
+    if (n == 0) return;
+    const Csr& P = f.pat();
+    const int g = c.grid_for(n, BS, 8);
+    k_begin_sweep<<<1, 1, 0, c.stream>>>(f.ep.p, f.counter.p, guard, want);
+    k_trsv_lower<<<g, BS, 0, c.stream>>>(n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
+                                         f.order_lo.p, b, x, f.flag.p, f.ep.p, f.counter.p, guard,
+                                         want);
+    k_begin_sweep<<<1, 1, 0, c.stream>>>(f.ep.p, f.counter.p, guard, want);
+    k_trsv_upper<<<g, BS, 0, c.stream>>>(n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
+                                         f.order_up.p, x, f.flag.p, f.ep.p, f.counter.p, guard,
+                                         want);
+    PD_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------ dense LU (coarsest level)
+__global__ void k_csr_to_dense_colmajor(int64_t n, const int64_t* rp, const int32_t* ci,
+                                        const double* v, double* A) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) A[i + (int64_t)ci[p] * n] += v[p];
+}
+
+// pivot search (first max |a_ik|, like idamax), full-row interchange and
+// column scaling by the reciprocal pivot (dgetf2).
+__global__ void k_lu_pivot(double* A, int64_t n, int64_t k, int32_t* piv, int* info) {
+    __shared__ double sv[1024];
+    __shared__ int64_t si[1024];
+    double best = -1.0;
+    int64_t bi = k;
+    for (int64_t i = k + threadIdx.x; i < n; i += blockDim.x) {
+        double a = fabs(A[i + k * n]);
+        if (a > best) { best = a; bi = i; }
+    }
+    sv[threadIdx.x] = best;
+    si[threadIdx.x] = bi;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            double o = sv[threadIdx.x + s];
+            int64_t oi = si[threadIdx.x + s];
+            if (o > sv[threadIdx.x] || (o == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+                sv[threadIdx.x] = o;
+                si[threadIdx.x] = oi;
+            }
+        }
+        __syncthreads();
+    }
+    const int64_t p = si[0];
+    if (threadIdx.x == 0) piv[k] = (int32_t)p;
+    if (p != k)
+        for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+            double t = A[k + j * n];
+            A[k + j * n] = A[p + j * n];
+            A[p + j * n] = t;
+        }
+    __syncthreads();
+    const double akk = A[k + k * n];
+    if (akk == 0.0) {
+        if (threadIdx.x == 0 && *info == 0) *info = (int)(k + 1);
+        return;
+    }
+    const double r = 1.0 / akk;
+    for (int64_t i = k + 1 + threadIdx.x; i < n; i += blockDim.x) A[i + k * n] *= r;
+}
+
+__global__ void k_lu_update(double* A, int64_t n, int64_t k) {
+    const int64_t m = n - k - 1;
+    const int64_t tot = m * m;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = k + 1 + t % m, j = k + 1 + t / m;
+        A[i + j * n] -= A[i + k * n] * A[k + j * n];
+    }
+}
+
+std::unique_ptr<DenseLU> dense_lu_from_csr(Ctx& c, const Csr& A) {
+    if (A.nrows != A.ncols) throw ConfigError("dense LU needs a square matrix");
+    const int64_t n = A.nrows;
+    if (n > 29000) throw ConfigError("coarsest level too large for dense LU: n=" + std::to_string(n));
+    auto f = std::make_unique<DenseLU>();
+    f->n = n;
+    f->lu.alloc(std::max<int64_t>(n * n, 1));
+    f->piv.alloc(std::max<int64_t>(n, 1));
+    PD_CUDA(cudaMemsetAsync(f->lu.p, 0, n * n * sizeof(double), c.stream));
+    k_csr_to_dense_colmajor<<<c.grid_for(n, BS), BS, 0, c.stream>>>(n, A.rowptr.p, A.col.p,
+                                                                    A.val.p, f->lu.p);
+    DevBuf<int> info(1);
+    PD_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), c.stream));
+    for (int64_t k = 0; k < n; ++k) {
+        k_lu_pivot<<<1, 1024, 0, c.stream>>>(f->lu.p, n, k, f->piv.p, info.p);
+        const int64_t m = n - k - 1;
+        if (m > 0) k_lu_update<<<c.grid_for(m * m, BS, 16), BS, 0, c.stream>>>(f->lu.p, n, k);
+    }
+    PD_LAUNCH_CHECK();
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    // A singular coarse matrix is not an exception in the reference either
+    // (LAPACK getrf info>0 only warns); the solve then yields non-finite values
+    // and the V-cycle raises SolverError (multigrid.py:270-271).
+    return f;
+}
+
+// Single-CTA substitution: LAPACK getrs order (row interchanges, unit-lower
+// column sweep, upper column sweep).  The vector lives in shared memory.
+__global__ void k_lu_solve(const double* __restrict__ LU, const int32_t* __restrict__ piv,
+                           int64_t n, const double* __restrict__ b, double* __restrict__ xout) {
+    extern __shared__ double xs[];
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) xs[i] = b[i];
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int64_t i = 0; i < n; ++i) {
+            int64_t p = piv[i];
+            if (p != i) { double t = xs[i]; xs[i] = xs[p]; xs[p] = t; }
+        }
+    __syncthreads();
+    for (int64_t k = 0; k < n; ++k) {
+        const double xk = xs[k];
+        for (int64_t i = k + 1 + threadIdx.x; i < n; i += blockDim.x)
+            xs[i] -= LU[i + k * n] * xk;
+        __syncthreads();
+    }
+    for (int64_t k = n - 1; k >= 0; --k) {
+        if (threadIdx.x == 0) xs[k] = xs[k] / LU[k + k * n];
+        __syncthreads();
+        const double xk = xs[k];
+        for (int64_t i = threadIdx.x; i < k; i += blockDim.x) xs[i] -= LU[i + k * n] * xk;
+        __syncthreads();
+    }
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) xout[i] = xs[i];
+}
+
+void dense_lu_solve(Ctx& c, const DenseLU& f, const double* b, double* x) {
+    const int64_t n = f.n;
+    if (n == 0) return;
+    size_t sm = n * sizeof(double);
+    static bool attr_set = false;
+    if (!attr_set) {
+        PD_CUDA(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024));
+        attr_set = true;
+    }
+    if (sm > 227 * 1024) throw ConfigError("coarsest level too large for the dense solve");
+    k_lu_solve<<<1, 1024, sm, c.stream>>>(f.lu.p, f.piv.p, n, b, x);
+    PD_LAUNCH_CHECK();
+}
+
+}  // namespace pd

@@ -1,0 +1,242 @@
+"""Device-backed sparse kernels (drop-in for paradiff/linalg.py).
+
+Same names and arguments as the reference module; numpy in -> numpy out (and
+CUDA tensors in -> CUDA tensors out).  The work runs in the native library:
+CSR SpMV, level-scheduled ILU(0) factor/solve, block-Jacobi masking, dense
+LU and a device-resident GMRES (see csrc/).  `kron`/`as_csr` stay host-side
+setup helpers exactly as in the reference (linalg.py:47-60).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _native as N
+from .errors import ConfigurationError
+from .report import SolveReport
+
+THREAD_CAP_ENV = "PARADIFF_MAX_THREADS"
+GROWTH_FACTOR = 10.0
+_SIZE_LIMIT = 2**31 - 1
+
+
+def thread_cap(default: int = 16) -> int:
+    """Kept for API compatibility (linalg.py:27-34); the GPU path ignores it."""
+    raw = os.environ.get(THREAD_CAP_ENV, "")
+    try:
+        cap = int(raw) if raw else default
+    except ValueError:
+        cap = default
+    return max(1, min(cap, os.cpu_count() or 1))
+
+
+def as_csr(A) -> sp.csr_matrix:
+    A = sp.csr_matrix(A)
+    A.sum_duplicates()
+    A.sort_indices()
+    return A
+
+
+def kron(A, B) -> sp.csr_matrix:
+    A, B = sp.coo_matrix(A), sp.coo_matrix(B)
+    if A.shape[0] * B.shape[0] > _SIZE_LIMIT or A.shape[1] * B.shape[1] > _SIZE_LIMIT:
+        raise ConfigurationError("Kronecker product dimensions overflow index range")
+    return as_csr(sp.kron(A, B, format="csr"))
+
+
+class DeviceCsr:
+    """A CSR matrix resident in HBM (int64 row pointers, int32 columns, fp64)."""
+
+    def __init__(self, A, ctx: N.Context | None = None):
+        self.ctx = ctx or N.context()
+        A = as_csr(A)
+        self.shape = A.shape
+        self.nnz = int(A.nnz)
+        rp = np.ascontiguousarray(A.indptr, dtype=np.int64)
+        ci = np.ascontiguousarray(A.indices, dtype=np.int32)
+        va = np.ascontiguousarray(A.data, dtype=np.float64)
+        h = ctypes.c_void_p()
+        N.call("pd_csr_create", self.ctx.handle, A.shape[0], A.shape[1], self.nnz,
+               rp.ctypes.data_as(ctypes.c_void_p), ci.ctypes.data_as(ctypes.c_void_p),
+               va.ctypes.data_as(ctypes.c_void_p), 0, ctypes.byref(h))
+        self.handle = h
+        self._owned = True
+        self._indptr, self._indices = rp, ci
+
+    @classmethod
+    def borrowed(cls, handle, shape, nnz, ctx):
+        self = cls.__new__(cls)
+        self.ctx, self.handle, self.shape, self.nnz, self._owned = ctx, handle, shape, nnz, False
+        self._indptr = self._indices = None
+        return self
+
+    def same_pattern(self, A: sp.csr_matrix) -> bool:
+        return (self._indptr is not None and A.nnz == self.nnz and A.shape == self.shape
+                and np.array_equal(A.indptr, self._indptr) and np.array_equal(A.indices,
+                                                                             self._indices))
+
+    def set_values(self, data) -> None:
+        d = np.ascontiguousarray(data, dtype=np.float64)
+        N.call("pd_csr_set_values", self.ctx.handle, self.handle,
+               d.ctypes.data_as(ctypes.c_void_p), 0)
+
+    def release(self):
+        """Transfer ownership to a native object (e.g. the multigrid hierarchy)."""
+        self._owned = False
+        return self.handle
+
+    def matvec_dev(self, x, out=None, mode=0, b=None):
+        ctx = self.ctx
+        ctx.sync_stream()
+        out = N.empty(self.shape[0], ctx) if out is None else out
+        N.call("pd_csr_spmv", ctx.handle, self.handle, N.ptr(x), N.ptr(out), mode,
+               N.ptr(b) if b is not None else ctypes.c_void_p())
+        return out
+
+    def dot(self, x):
+        xd = N.to_device(x, self.ctx)
+        return N.like_input(self.matvec_dev(xd), x)
+
+    __matmul__ = dot
+
+    def __del__(self):
+        try:
+            if getattr(self, "_owned", False) and self.handle:
+                N.load_library().pd_csr_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def device_csr(A, ctx=None) -> DeviceCsr:
+    return A if isinstance(A, DeviceCsr) else DeviceCsr(A, ctx)
+
+
+class Ilu0:
+    """ILU(0) factors on the GPU (linalg.py:116-145): level-scheduled factor and solves."""
+
+    def __init__(self, A, _nblocks: int = 1):
+        self.ctx = N.context()
+        if isinstance(A, DeviceCsr):
+            self._A = A
+        else:
+            A = as_csr(A)
+            if A.shape[0] != A.shape[1]:
+                raise ConfigurationError("ILU(0) needs a square matrix")
+            self._A = DeviceCsr(A, self.ctx)
+        self.n = self._A.shape[0]
+        h = ctypes.c_void_p()
+        N.call("pd_ilu0_create", self.ctx.handle, self._A.handle, int(_nblocks), ctypes.byref(h))
+        self.handle = h
+
+    def levels(self) -> tuple[int, int]:
+        lo, up = ctypes.c_int32(), ctypes.c_int32()
+        N.call("pd_ilu0_levels", self.handle, ctypes.byref(lo), ctypes.byref(up))
+        return lo.value, up.value
+
+    def solve_dev(self, b, out=None):
+        self.ctx.sync_stream()
+        out = N.empty(self.n, self.ctx) if out is None else out
+        N.call("pd_ilu0_solve", self.ctx.handle, self.handle, N.ptr(b), N.ptr(out))
+        return out
+
+    def solve(self, b):
+        return N.like_input(self.solve_dev(N.to_device(b, self.ctx)), b)
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                N.load_library().pd_ilu0_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def ilu0(A) -> Ilu0:
+    return Ilu0(A)
+
+
+class BlockJacobiPrecond(Ilu0):
+    """Block-Jacobi ILU(0) over contiguous ranges (linalg.py:152-189).
+
+    The ranges follow the reference rule (size n//P, the last absorbs the
+    remainder).  On the GPU all blocks are one masked factorization, so the
+    result is independent of any worker count by construction; ``parallel``
+    is accepted for API compatibility.
+    """
+
+    def __init__(self, A, num_blocks: int, parallel: bool | None = None):
+        n = A.shape[0]
+        if num_blocks < 1 or num_blocks > n:
+            raise ConfigurationError(f"num_blocks must be in [1, {n}], got {num_blocks}")
+        size = n // num_blocks
+        self.ranges = [(b * size, (b + 1) * size if b < num_blocks - 1 else n)
+                       for b in range(num_blocks)]
+        self.parallel = parallel
+        super().__init__(A, num_blocks)
+
+
+def block_jacobi(A, num_blocks: int, parallel: bool | None = None) -> BlockJacobiPrecond:
+    return BlockJacobiPrecond(A, num_blocks, parallel)
+
+
+class DenseLU:
+    """Coarsest-level dense LU with partial pivoting, factored and solved on device."""
+
+    def __init__(self, A):
+        self.ctx = N.context()
+        self._A = device_csr(A if not isinstance(A, np.ndarray) else sp.csr_matrix(A), self.ctx)
+        if self._A.shape[0] != self._A.shape[1]:
+            raise ConfigurationError("dense LU needs a square matrix")
+        self.n = self._A.shape[0]
+        h = ctypes.c_void_p()
+        N.call("pd_dense_lu_create", self.ctx.handle, self._A.handle, ctypes.byref(h))
+        self.handle = h
+
+    def solve(self, b):
+        bd = N.to_device(b, self.ctx)
+        out = N.empty(self.n, self.ctx)
+        N.call("pd_dense_lu_solve", self.ctx.handle, self.handle, N.ptr(bd), N.ptr(out))
+        return N.like_input(out, b)
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                N.load_library().pd_dense_lu_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def _report_from(rep: N.SolveReportC, hist: np.ndarray) -> SolveReport:
+    return SolveReport(iterations=int(rep.iterations), converged=bool(rep.converged),
+                       diverged=bool(rep.diverged),
+                       residual_history=[float(v) for v in hist[: rep.hist_len]])
+
+
+def gmres(A, b, precond=None, x0=None, tol_rel: float = 1e-9, tol_abs: float = 1e-9,
+          restart: int = 30, max_it: int = 1000):
+    """Restarted right-preconditioned GMRES on the GPU (linalg.py:215-311).
+
+    ``A``: scipy sparse matrix or DeviceCsr; ``precond``: Ilu0 /
+    BlockJacobiPrecond / None.  Arbitrary Python callables are not accepted
+    (their work could not run on the device).
+    """
+    if callable(A) and not hasattr(A, "dot"):
+        raise ConfigurationError("device GMRES needs a sparse matrix, not a callable")
+    if precond is not None and not isinstance(precond, Ilu0):
+        raise ConfigurationError("device GMRES preconditioner must be Ilu0/BlockJacobiPrecond")
+    Ad = device_csr(A)
+    ctx = Ad.ctx
+    ctx.sync_stream()
+    bd = N.to_device(b, ctx)
+    n = bd.numel()
+    x0d = N.to_device(x0, ctx) if x0 is not None else None
+    out = N.empty(n, ctx)
+    rep = N.SolveReportC()
+    hist = np.zeros(int(max(max_it, 1)) + 2)
+    N.call("pd_gmres", ctx.handle, Ad.handle, precond.handle if precond is not None else None,
+           N.ptr(bd), N.ptr(x0d), N.ptr(out), float(tol_rel), float(tol_abs), int(restart),
+           int(max_it), ctypes.byref(rep), hist.ctypes.data_as(ctypes.c_void_p), hist.size)
+    return N.like_input(out, b), _report_from(rep, hist)

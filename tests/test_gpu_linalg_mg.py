@@ -1,0 +1,153 @@
+"""GPU parity: sparse kernels, GMRES and multigrid vs golden fixtures + oracle.
+
+Bar: CSR products and ILU(0) solves bitwise equal to the reference (same
+per-row order, separately rounded); solves equal iteration counts and
+per-time-node relative L2 <= 1e-10 (BASELINE north_star tolerance).
+"""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import paper_2006_12883_b200 as pd
+from oracle import paradiff_oracle as O
+from pd_util import per_node_rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _A(g):
+    return sp.csr_matrix((g["A_data"], g["A_indices"], g["A_indptr"]))
+
+
+def test_spmv_bitwise_scipy(golden):
+    g = golden("linalg")
+    A = _A(g)
+    x = g["b"]
+    np.testing.assert_array_equal(pd.DeviceCsr(A).dot(x), A @ x)
+
+
+def test_ilu0_solve_bitwise(golden):
+    g = golden("linalg")
+    ilu = pd.Ilu0(_A(g))
+    np.testing.assert_array_equal(ilu.solve(g["b"]), g["ilu_solve"])
+    bj = pd.block_jacobi(_A(g), 3)
+    assert bj.ranges == [(0, 100), (100, 200), (200, 300)]
+    np.testing.assert_array_equal(bj.solve(g["b"]), g["bj_solve"])
+
+
+def test_zero_pivot_row_reported():
+    A = sp.csr_matrix(np.array([[1.0, 0.0, 0.0], [0.0, 0.0, 1.0], [0.0, 1.0, 1.0]]))
+    with pytest.raises(pd.SolverError, match="row 1"):
+        pd.Ilu0(A)
+
+
+def test_gmres_matches_reference(golden):
+    g = golden("linalg")
+    A = _A(g)
+    x, rep = pd.gmres(A, g["b"], precond=pd.Ilu0(A), tol_rel=1e-10, tol_abs=1e-12, restart=7,
+                      max_it=200)
+    assert rep.converged and rep.iterations == int(g["gm_its"])
+    assert rel_l2(x, g["gm_x"]) < 1e-12
+    np.testing.assert_allclose(rep.residual_history, g["gm_hist"], rtol=1e-8, atol=1e-14)
+    x2, rep2 = pd.gmres(A, g["b"], precond=pd.block_jacobi(A, 3), tol_rel=1e-10, tol_abs=1e-12,
+                        restart=5, max_it=200)
+    assert rep2.iterations == int(g["gm2_its"])
+    assert rel_l2(x2, g["gm2_x"]) < 1e-12
+
+
+def test_gmres_x0_and_unpreconditioned():
+    rng = np.random.default_rng(3)
+    n = 200
+    A = sp.diags([np.full(n - 1, -1.0), np.full(n, 4.0), np.full(n - 1, -1.0)], [-1, 0, 1],
+                 format="csr")
+    b = rng.standard_normal(n)
+    x0 = rng.standard_normal(n)
+    for M in (None, "ilu"):
+        pre_d = pd.Ilu0(A) if M else None
+        pre_o = O.OIlu0(A) if M else None
+        x, rep = pd.gmres(A, b, precond=pre_d, x0=x0, tol_rel=1e-12, tol_abs=0.0, restart=6,
+                          max_it=100)
+        xo, repo = O.gmres(A, b, M=pre_o, x0=x0, tol_rel=1e-12, tol_abs=0.0, restart=6,
+                           max_it=100)
+        assert rep.iterations == repo.iterations
+        assert rel_l2(x, xo) < 1e-12
+
+
+def _heat(Nx=64, Nt=16, M=3):
+    prob = pd.heat_problem()
+    mesh = pd.SpaceMesh(Nx, 1.0)
+    return pd.assemble_system(pd.make_tableau(M), pd.assemble_space(mesh), pd.TimeGrid(Nt, 1.0),
+                              0.0, prob.u0(mesh.vertices))
+
+
+@pytest.mark.parametrize("strategy", ["SMG", "STMG", "SMMG"])
+@pytest.mark.parametrize("P", [1, 4])
+def test_mg_fem1d_matches_reference(golden, strategy, P):
+    g = golden("mg_fem1d")
+    s = _heat()
+    h = pd.build_hierarchy(s, strategy, 3, 3, partitions=P)
+    key = f"{strategy}_P{P}"
+    v1 = h.vcycle(s.rhs(), np.zeros(s.size))
+    assert rel_l2(v1, g[key + "_v1"]) < 1e-12
+    x, rep = h.solve(s.rhs(), tol_rel=1e-10, tol_abs=1e-10)
+    assert rep.converged and rep.iterations == int(g[key + "_its"])
+    assert per_node_rel(x, g[key + "_x"], (16, 3, 65)) < 1e-10
+    np.testing.assert_allclose(rep.residual_history, g[key + "_hist"], rtol=1e-6)
+
+
+@pytest.mark.parametrize("strategy", ["SMG", "STMG"])
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_c1_mg_matches_reference(golden, strategy, P):
+    g = golden("c1")
+    cfg = pd.baseline_config("C1")
+    system = pd.assemble_system(pd.make_tableau(cfg.M), pd.fd_space(cfg.spec),
+                                pd.TimeGrid(cfg.Nt, cfg.T), 0.0, cfg.u0())
+    h = pd.build_hierarchy(system, strategy, 4, 3, partitions=P)
+    x, rep = h.solve(system.rhs(), tol_rel=1e-10, tol_abs=1e-10)
+    assert rep.iterations == int(g[f"{strategy}_P{P}_its"])
+    assert per_node_rel(x, g[f"{strategy}_P{P}_x"], (16, 3, 127)) < 1e-10
+
+
+def test_c2_small_mg_matches_reference(golden):
+    g = golden("c2_small")
+    spec = pd.StencilSpec(2, 15, "dirichlet", 1.0)
+    system = pd.assemble_system(pd.make_tableau(3), pd.fd_space(spec), pd.TimeGrid(8, 8 / 64),
+                                0.0, g["u0"])
+    for strat in ("SMG", "STMG"):
+        for P in (1, 4):
+            h = pd.build_hierarchy(system, strat, 3, 3, partitions=P)
+            x, rep = h.solve(system.rhs(), tol_rel=1e-10, tol_abs=1e-10)
+            assert rep.iterations == int(g[f"{strat}_P{P}_its"]), (strat, P)
+            assert per_node_rel(x, g[f"{strat}_P{P}_x"], (8, 3, 225)) < 1e-10
+
+
+def test_dense_lu_matches_scipy():
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((300, 300)) + 30 * np.eye(300)
+    b = rng.standard_normal(300)
+    x = pd.DenseLU(sp.csr_matrix(A)).solve(b)
+    assert rel_l2(x, np.linalg.solve(A, b)) < 1e-13
+
+
+def test_spacetime_residual_matches_reference(golden):
+    g = golden("spacetime")
+    prob = pd.monodomain_problem()
+    mesh = pd.SpaceMesh(16, prob.X)
+    s = pd.assemble_system(pd.make_tableau(3), pd.assemble_space(mesh), pd.TimeGrid(4, prob.T),
+                           prob.gamma, prob.u0(mesh.vertices))
+    np.testing.assert_allclose(s.residual(g["u"]), g["res"], rtol=1e-12, atol=1e-12)
+
+
+def test_newton_mg_matches_reference(golden):
+    g = golden("newton")
+    prob = pd.monodomain_problem()
+    mesh = pd.SpaceMesh(32, prob.X)
+    s = pd.assemble_system(pd.make_tableau(2), pd.assemble_space(mesh), pd.TimeGrid(8, prob.T),
+                           prob.gamma, prob.u0(mesh.vertices))
+    h = pd.build_hierarchy(s, "SMG", 3, 3)
+    x, rep = pd.newton_solve(s, pd.mg_linear_solver(h, tol_rel=1e-9, tol_abs=1e-9), tol=1e-9)
+    assert rep.iterations == int(g["its"])
+    assert rep.inner_iterations == g["inner"].tolist()
+    assert rep.damped_steps == int(g["damped"])
+    assert per_node_rel(x, g["x"], (8, 2, 33)) < 1e-9
