@@ -36,6 +36,7 @@ typedef struct pd_solve_report {
 const char *pd_last_error(void);
 int64_t pd_last_error_index(void);
 int pd_version(void);
+uint64_t pd_launch_count(void); /* kernels launched by this library since load */
 
 /* ---- context (one per GPU / rank; single-threaded) -------------------- */
 int pd_ctx_create(int device, void *stream, void **ctx_out);
@@ -78,6 +79,7 @@ int pd_gmres(void *ctx, void *A, void *ilu, const double *b, const double *x0, d
 int pd_mg_create(void *ctx, int nlevels, void **mats, void **R, void **P, int nu,
                  int partitions, int restart, int smooth_solves, void **mg_out);
 int pd_mg_level_matrix(void *mg, int level, void **csr_out); /* borrowed handle */
+int pd_mg_level_precond(void *mg, int level, void **ilu_out); /* borrowed ILU/block-Jacobi */
 int pd_mg_refactor(void *ctx, void *mg);                     /* after value updates */
 int pd_mg_vcycle(void *ctx, void *mg, const double *b, double *x); /* multigrid.py:268-273 */
 int pd_mg_solve(void *ctx, void *mg, const double *b, double *x, double tol_rel,

@@ -27,6 +27,22 @@ from scipy.sparse.linalg import splu
 from .build import build as _build_c
 
 
+# Reduction hook: the reference uses numpy/BLAS dot products; tests swap in a
+# different (equally valid) summation order to measure the rounding floor of
+# the reference's own output.
+_DOT = np.dot
+
+
+def set_dot(fn=None):
+    """Install a dot-product implementation (None restores numpy.dot)."""
+    global _DOT
+    _DOT = np.dot if fn is None else fn
+
+
+def _norm(v):
+    return float(np.sqrt(_DOT(v, v))) if _DOT is not np.dot else float(np.linalg.norm(v))
+
+
 class OracleConfigError(ValueError):
     pass
 
@@ -313,7 +329,7 @@ def gmres(A, b, M=None, x0=None, tol_rel=1e-9, tol_abs=1e-9, restart=30, max_it=
     x = np.zeros(n) if x0 is None else np.array(x0, dtype=np.float64)
     restart = max(1, min(restart, n))
     r = b - mv(x)
-    beta = float(np.linalg.norm(r))
+    beta = _norm(r)
     if not np.isfinite(beta):
         raise OracleSolverError("non-finite initial residual")
     thr = max(tol_abs, tol_rel * beta)
@@ -334,9 +350,9 @@ def gmres(A, b, M=None, x0=None, tol_rel=1e-9, tol_abs=1e-9, restart=30, max_it=
         for j in range(restart):
             w = mv(ps(V[j]))
             for i in range(j + 1):
-                H[i, j] = np.dot(w, V[i])
+                H[i, j] = _DOT(w, V[i])
                 w -= H[i, j] * V[i]
-            hn = float(np.linalg.norm(w))
+            hn = _norm(w)
             H[j + 1, j] = hn
             happy = hn <= 1e-14 * max(1.0, beta)
             if not happy:
@@ -365,7 +381,7 @@ def gmres(A, b, M=None, x0=None, tol_rel=1e-9, tol_abs=1e-9, restart=30, max_it=
         y = scipy.linalg.solve_triangular(H[:k, :k], g[:k], lower=False)
         x = x + ps(V[:k].T @ y)
         r = b - mv(x)
-        beta = float(np.linalg.norm(r))
+        beta = _norm(r)
         if not np.isfinite(beta):
             raise OracleSolverError("non-finite residual in GMRES restart")
         rep.residual_history[-1] = beta

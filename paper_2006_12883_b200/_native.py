@@ -36,6 +36,8 @@ _SIGNATURES = {
     "pd_last_error": (ctypes.c_char_p, []),
     "pd_last_error_index": (_i64, []),
     "pd_version": (_int, []),
+    "pd_launch_count": (ctypes.c_uint64, []),
+    "pd_mg_level_precond": (_int, [_vp, _int, ctypes.POINTER(_vp)]),
     "pd_ctx_create": (_int, [_int, _vp, ctypes.POINTER(_vp)]),
     "pd_ctx_set_stream": (_int, [_vp, _vp]),
     "pd_ctx_destroy": (_int, [_vp]),

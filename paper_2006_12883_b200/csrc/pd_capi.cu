@@ -61,6 +61,7 @@ extern "C" {
 const char* pd_last_error(void) { return g_err.c_str(); }
 int64_t pd_last_error_index(void) { return g_err_index; }
 int pd_version(void) { return 1; }
+uint64_t pd_launch_count(void) { return pd::g_launches.load(); }
 
 int pd_ctx_create(int device, void* stream, void** out) {
     return guarded([&] { *out = new pd::Ctx(device, static_cast<cudaStream_t>(stream)); });
@@ -191,6 +192,14 @@ int pd_mg_level_matrix(void* mg, int level, void** out) {
         auto* M = H<pd::Multigrid>(mg, "multigrid");
         if (level < 0 || level >= M->num_levels()) throw pd::ConfigError("bad level index");
         *out = &M->level_matrix(level);
+    });
+}
+int pd_mg_level_precond(void* mg, int level, void** ilu_out) {
+    return guarded([&] {
+        auto* M = H<pd::Multigrid>(mg, "multigrid");
+        if (level < 0 || level + 1 >= M->num_levels())
+            throw pd::ConfigError("level has no smoother (coarsest or out of range)");
+        *ilu_out = M->level_precond(level);
     });
 }
 int pd_mg_refactor(void* ctx, void* mg) {

@@ -5,8 +5,10 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
+#include <utility>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -32,6 +34,17 @@ struct CudaError : std::runtime_error {
     } while (0)
 
 #define PD_LAUNCH_CHECK() PD_CUDA(cudaGetLastError())
+
+// Every kernel launch of the library goes through launch(): it counts the
+// launches (pd_launch_count(), reported by bench.py as gpu_launches).
+extern std::atomic<unsigned long long> g_launches;
+
+template <typename... KArgs, typename... Args>
+inline void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                   Args&&... args) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    k<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+}
 
 // Owning device allocation (cudaMalloc/cudaFree; allocation happens at
 // plan/setup time only, never inside a solve).

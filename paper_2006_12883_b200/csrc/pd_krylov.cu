@@ -265,7 +265,7 @@ void Gmres::enqueue_init(const double* r0_, const double* norm2_dev, double tol_
                          double tol_abs, const double* x0) {
     r0 = r0_;
     if (x0) vec_copy(c, xg.p, x0, n);
-    k_gm_init<<<1, 1, 0, c.stream>>>(st.p, norm2_dev, tol_rel, tol_abs, max_it, restart, hist.p,
+    launch(k_gm_init, 1, 1, 0, c.stream, st.p, norm2_dev, tol_rel, tol_abs, max_it, restart, hist.p,
                                      x0 ? 1 : 0);
     PD_LAUNCH_CHECK();
 }
@@ -274,8 +274,8 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
     const int g = c.grid_for(n, KB, 8);
     const int gr = std::min(c.grid_for(n, KB, 4), kReduceMaxBlocks);
     const int* ph = &st.p->phase;
-    k_gm_start_vec<<<g, KB, 0, c.stream>>>(st.p, r0, rg.p, V.p, vcur.p, n);
-    k_gm_start<<<1, 1, 0, c.stream>>>(st.p);
+    launch(k_gm_start_vec, g, KB, 0, c.stream, st.p, r0, rg.p, V.p, vcur.p, n);
+    launch(k_gm_start, 1, 1, 0, c.stream, st.p);
     const double* zin = vcur.p;
     if (M) {
         ilu0_solve(c, *M, vcur.p, z.p, ph, GM_RUN);
@@ -284,21 +284,21 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
     csr_spmv(c, *A, zin, w.p, SPMV_SET, nullptr, ph, GM_RUN);
     const int passes = std::min(mgs_passes, restart + 1);
     for (int i = 0; i < passes; ++i)
-        k_gm_mgs<<<gr, KB, 0, c.stream>>>(st.p, i, w.p, V.p, n, c.red_partials.p,
+        launch(k_gm_mgs, gr, KB, 0, c.stream, st.p, i, w.p, V.p, n, c.red_partials.p,
                                           c.red_counter.p);
-    k_gm_arnoldi<<<1, 1, 0, c.stream>>>(st.p, slot, hist.p);
-    k_gm_newvec<<<g, KB, 0, c.stream>>>(st.p, slot, w.p, V.p, vcur.p, n);
+    launch(k_gm_arnoldi, 1, 1, 0, c.stream, st.p, slot, hist.p);
+    launch(k_gm_newvec, g, KB, 0, c.stream, st.p, slot, w.p, V.p, vcur.p, n);
     // cycle finish (active only when this step ended the cycle)
-    k_gm_finish_y<<<1, 1, 0, c.stream>>>(st.p);
-    k_gm_combine<<<g, KB, 0, c.stream>>>(st.p, V.p, u.p, n);
+    launch(k_gm_finish_y, 1, 1, 0, c.stream, st.p);
+    launch(k_gm_combine, g, KB, 0, c.stream, st.p, V.p, u.p, n);
     const double* du = u.p;
     if (M) {
         ilu0_solve(c, *M, u.p, z.p, ph, GM_FINISH);
         du = z.p;
     }
-    k_gm_update_x<<<g, KB, 0, c.stream>>>(st.p, xg.p, du, n);
+    launch(k_gm_update_x, g, KB, 0, c.stream, st.p, xg.p, du, n);
     csr_spmv(c, *A, xg.p, rg.p, SPMV_RESID, b, ph, GM_FINISH, norm2.p, nullptr);
-    k_gm_restart<<<1, 1, 0, c.stream>>>(st.p, norm2.p, hist.p);
+    launch(k_gm_restart, 1, 1, 0, c.stream, st.p, norm2.p, hist.p);
     PD_LAUNCH_CHECK();
 }
 
@@ -324,7 +324,7 @@ void enqueue_gmres_smooth(Ctx& c, Gmres& g, const Csr& A, const double* b, doubl
     csr_spmv(c, A, x, r_work, SPMV_RESID, b, nullptr, 0, c.scalars.p + 8, nullptr);
     g.enqueue_init(r_work, c.scalars.p + 8, 1e-13, 0.0);
     for (int s = 0; s < nu; ++s) g.enqueue_slot(s, s + 2, r_work);
-    k_gm_apply<<<c.grid_for(n, KB, 8), KB, 0, c.stream>>>(g.dev(), x, g.x(), n);
+    launch(k_gm_apply, c.grid_for(n, KB, 8), KB, 0, c.stream, g.dev(), x, g.x(), n);
     PD_LAUNCH_CHECK();
 }
 

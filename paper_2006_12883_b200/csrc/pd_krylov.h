@@ -69,6 +69,7 @@ class Multigrid {
     // replace level matrix values (same patterns) and refactor (Newton refresh)
     void refactor();
     Csr& level_matrix(int l) { return *lv[l].A; }
+    Ilu0* level_precond(int l) { return lv[l].pre.get(); }
     int num_levels() const { return (int)lv.size(); }
     int64_t fine_size() const { return lv[0].n; }
     // x <- V-cycle(b, x)  (device pointers, n = fine size); no host sync

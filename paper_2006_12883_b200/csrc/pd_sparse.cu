@@ -27,6 +27,8 @@ namespace pd {
 
 using namespace dev;
 
+std::atomic<unsigned long long> g_launches{0};
+
 Ctx::Ctx(int dev_, cudaStream_t s) : device(dev_), stream(s) {
     PD_CUDA(cudaSetDevice(device));
     PD_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
@@ -80,7 +82,7 @@ __global__ void k_nonfinite(const double* x, int64_t n, int* flag) {
 
 bool vec_has_nonfinite(Ctx& c, const double* x, int64_t n) {
     PD_CUDA(cudaMemsetAsync(c.flags.p, 0, sizeof(int), c.stream));
-    if (n > 0) k_nonfinite<<<c.grid_for(n, BS), BS, 0, c.stream>>>(x, n, c.flags.p);
+    if (n > 0) launch(k_nonfinite, c.grid_for(n, BS), BS, 0, c.stream, x, n, c.flags.p);
     int h = 0;
     PD_CUDA(cudaMemcpyAsync(&h, c.flags.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     PD_CUDA(cudaStreamSynchronize(c.stream));
@@ -89,7 +91,7 @@ bool vec_has_nonfinite(Ctx& c, const double* x, int64_t n) {
 
 void vec_fill(Ctx& c, double* x, int64_t n, double v) {
     if (n <= 0) return;
-    k_fill<<<c.grid_for(n, BS), BS, 0, c.stream>>>(x, n, v);
+    launch(k_fill, c.grid_for(n, BS), BS, 0, c.stream, x, n, v);
     PD_LAUNCH_CHECK();
 }
 
@@ -100,13 +102,13 @@ void vec_copy(Ctx& c, double* y, const double* x, int64_t n) {
 
 void vec_axpy_inplace(Ctx& c, double* y, const double* x, int64_t n) {
     if (n <= 0) return;
-    k_axpy_inplace<<<c.grid_for(n, BS), BS, 0, c.stream>>>(y, x, n);
+    launch(k_axpy_inplace, c.grid_for(n, BS), BS, 0, c.stream, y, x, n);
     PD_LAUNCH_CHECK();
 }
 
 void vec_dot(Ctx& c, const double* x, const double* y, int64_t n, double* out_dev) {
     int g = std::min(c.grid_for(n, BS, 4), kReduceMaxBlocks);
-    k_dot<<<g, BS, 0, c.stream>>>(x, y, n, c.red_partials.p, c.red_counter.p, out_dev);
+    launch(k_dot, g, BS, 0, c.stream, x, y, n, c.red_partials.p, c.red_counter.p, out_dev);
     PD_LAUNCH_CHECK();
 }
 
@@ -156,12 +158,12 @@ void csr_spmv(Ctx& c, const Csr& A, const double* x, double* y, int mode, const 
     if (A.nrows <= 0) return;
     if (norm2_out) {
         int g = std::min(c.grid_for(A.nrows, BS, 8), kReduceMaxBlocks);
-        k_spmv<true><<<g, BS, 0, c.stream>>>(A.nrows, A.rowptr.p, A.col.p, A.val.p, x, y, mode,
+        launch(k_spmv<true>, g, BS, 0, c.stream, A.nrows, A.rowptr.p, A.col.p, A.val.p, x, y, mode,
                                              b, guard, want, c.red_partials.p, c.red_counter.p,
                                              norm2_out, nonfinite_flag);
     } else {
         int g = c.grid_for(A.nrows, BS, 16);
-        k_spmv<false><<<g, BS, 0, c.stream>>>(A.nrows, A.rowptr.p, A.col.p, A.val.p, x, y, mode,
+        launch(k_spmv<false>, g, BS, 0, c.stream, A.nrows, A.rowptr.p, A.col.p, A.val.p, x, y, mode,
                                               b, guard, want, nullptr, nullptr, nullptr, nullptr);
     }
     PD_LAUNCH_CHECK();
@@ -419,11 +421,11 @@ static void sort_by_level(Ctx& c, int* level, int64_t n, DevBuf<int32_t>& order,
     DevBuf<int> level_sorted(n);
     DevBuf<int32_t> idx(n);
     order.alloc(n);
-    k_iota<<<c.grid_for(n, BS), BS, 0, c.stream>>>(idx.p, n);
+    launch(k_iota, c.grid_for(n, BS), BS, 0, c.stream, idx.p, n);
     // number of key bits from the max level
     DevBuf<int> mx(1);
     PD_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), c.stream));
-    k_max_int<<<c.grid_for(n, BS), BS, 0, c.stream>>>(level, n, mx.p);
+    launch(k_max_int, c.grid_for(n, BS), BS, 0, c.stream, level, n, mx.p);
     int hmax = 0;
     PD_CUDA(cudaMemcpyAsync(&hmax, mx.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
     PD_CUDA(cudaStreamSynchronize(c.stream));
@@ -457,7 +459,7 @@ std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks) {
         M.nrows = M.ncols = n;
         M.rowptr.alloc(n + 1);
         PD_CUDA(cudaMemsetAsync(M.rowptr.p, 0, sizeof(int64_t), c.stream));
-        k_mask_count<<<c.grid_for(n, BS), BS, 0, c.stream>>>(n, A.rowptr.p, A.col.p, size,
+        launch(k_mask_count, c.grid_for(n, BS), BS, 0, c.stream, n, A.rowptr.p, A.col.p, size,
                                                              nblocks, M.rowptr.p);
         size_t tb = 0;
         PD_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, M.rowptr.p, M.rowptr.p, n + 1,
@@ -470,7 +472,7 @@ std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks) {
         PD_CUDA(cudaStreamSynchronize(c.stream));
         M.col.alloc(std::max<int64_t>(M.nnz, 1));
         M.val.alloc(std::max<int64_t>(M.nnz, 1));
-        k_mask_copy<<<c.grid_for(n, BS), BS, 0, c.stream>>>(n, A.rowptr.p, A.col.p, A.val.p,
+        launch(k_mask_copy, c.grid_for(n, BS), BS, 0, c.stream, n, A.rowptr.p, A.col.p, A.val.p,
                                                             size, nblocks, M.rowptr.p, M.col.p,
                                                             M.val.p);
         PD_LAUNCH_CHECK();
@@ -487,14 +489,14 @@ std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks) {
         DevBuf<int> level(n);
         int g = c.grid_for(n, BS, 8);
         // lower levels
-        k_fill_int<<<c.grid_for(n, BS), BS, 0, c.stream>>>(level.p, n, -1);
+        launch(k_fill_int, c.grid_for(n, BS), BS, 0, c.stream, level.p, n, -1);
         PD_CUDA(cudaMemsetAsync(f->counter.p, 0, sizeof(unsigned long long), c.stream));
-        k_levels_lower<<<g, BS, 0, c.stream>>>(n, P.rowptr.p, P.col.p, level.p, f->counter.p);
+        launch(k_levels_lower, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, level.p, f->counter.p);
         PD_LAUNCH_CHECK();
         sort_by_level(c, level.p, n, f->order_lo, f->nlevels_lo);
-        k_fill_int<<<c.grid_for(n, BS), BS, 0, c.stream>>>(level.p, n, -1);
+        launch(k_fill_int, c.grid_for(n, BS), BS, 0, c.stream, level.p, n, -1);
         PD_CUDA(cudaMemsetAsync(f->counter.p, 0, sizeof(unsigned long long), c.stream));
-        k_levels_upper<<<g, BS, 0, c.stream>>>(n, P.rowptr.p, P.col.p, level.p, f->counter.p);
+        launch(k_levels_upper, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, level.p, f->counter.p);
         PD_LAUNCH_CHECK();
         sort_by_level(c, level.p, n, f->order_up, f->nlevels_up);
     }
@@ -510,7 +512,7 @@ void ilu0_refactor(Ctx& c, Ilu0& f) {
         // refresh masked values from the source matrix (pattern unchanged)
         const Csr& A = *f.pattern;
         const int64_t size = n / (int64_t)f.ranges.size();
-        k_mask_copy<<<c.grid_for(n, BS), BS, 0, c.stream>>>(
+        launch(k_mask_copy, c.grid_for(n, BS), BS, 0, c.stream, 
             n, A.rowptr.p, A.col.p, A.val.p, size, (int64_t)f.ranges.size(), P.rowptr.p,
             f.masked.col.p, f.masked.val.p);
         PD_LAUNCH_CHECK();
@@ -519,8 +521,8 @@ void ilu0_refactor(Ctx& c, Ilu0& f) {
                             c.stream));
     DevBuf<unsigned long long> bad(1);
     PD_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), c.stream));
-    k_begin_sweep<<<1, 1, 0, c.stream>>>(f.ep.p, f.counter.p, nullptr, 0);
-    k_ilu0_factor<<<c.grid_for(n, BS, 8), BS, 0, c.stream>>>(n, P.rowptr.p, P.col.p, f.fac.p,
+    launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, nullptr, 0);
+    launch(k_ilu0_factor, c.grid_for(n, BS, 8), BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p,
                                                               f.diag.p, f.order_lo.p, f.flag.p,
                                                               f.ep.p, f.counter.p, bad.p);
     PD_LAUNCH_CHECK();
@@ -542,12 +544,12 @@ void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, i
     if (n == 0) return;
     const Csr& P = f.pat();
     const int g = c.grid_for(n, BS, 8);
-    k_begin_sweep<<<1, 1, 0, c.stream>>>(f.ep.p, f.counter.p, guard, want);
-    k_trsv_lower<<<g, BS, 0, c.stream>>>(n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
+    launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, guard, want);
+    launch(k_trsv_lower, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
                                          f.order_lo.p, b, x, f.flag.p, f.ep.p, f.counter.p, guard,
                                          want);
-    k_begin_sweep<<<1, 1, 0, c.stream>>>(f.ep.p, f.counter.p, guard, want);
-    k_trsv_upper<<<g, BS, 0, c.stream>>>(n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
+    launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, guard, want);
+    launch(k_trsv_upper, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
                                          f.order_up.p, x, f.flag.p, f.ep.p, f.counter.p, guard,
                                          want);
     PD_LAUNCH_CHECK();
@@ -623,14 +625,14 @@ std::unique_ptr<DenseLU> dense_lu_from_csr(Ctx& c, const Csr& A) {
     f->lu.alloc(std::max<int64_t>(n * n, 1));
     f->piv.alloc(std::max<int64_t>(n, 1));
     PD_CUDA(cudaMemsetAsync(f->lu.p, 0, n * n * sizeof(double), c.stream));
-    k_csr_to_dense_colmajor<<<c.grid_for(n, BS), BS, 0, c.stream>>>(n, A.rowptr.p, A.col.p,
+    launch(k_csr_to_dense_colmajor, c.grid_for(n, BS), BS, 0, c.stream, n, A.rowptr.p, A.col.p,
                                                                     A.val.p, f->lu.p);
     DevBuf<int> info(1);
     PD_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), c.stream));
     for (int64_t k = 0; k < n; ++k) {
-        k_lu_pivot<<<1, 1024, 0, c.stream>>>(f->lu.p, n, k, f->piv.p, info.p);
+        launch(k_lu_pivot, 1, 1024, 0, c.stream, f->lu.p, n, k, f->piv.p, info.p);
         const int64_t m = n - k - 1;
-        if (m > 0) k_lu_update<<<c.grid_for(m * m, BS, 16), BS, 0, c.stream>>>(f->lu.p, n, k);
+        if (m > 0) launch(k_lu_update, c.grid_for(m * m, BS, 16), BS, 0, c.stream, f->lu.p, n, k);
     }
     PD_LAUNCH_CHECK();
     PD_CUDA(cudaStreamSynchronize(c.stream));
@@ -680,7 +682,7 @@ void dense_lu_solve(Ctx& c, const DenseLU& f, const double* b, double* x) {
         attr_set = true;
     }
     if (sm > 227 * 1024) throw ConfigError("coarsest level too large for the dense solve");
-    k_lu_solve<<<1, 1024, sm, c.stream>>>(f.lu.p, f.piv.p, n, b, x);
+    launch(k_lu_solve, 1, 1024, sm, c.stream, f.lu.p, f.piv.p, n, b, x);
     PD_LAUNCH_CHECK();
 }
 

@@ -70,7 +70,7 @@ int pd_reaction(void* ctx, int kind, int deriv, const double* u, double* out, in
     return guarded_vec([&] {
         auto& c = *static_cast<pd::Ctx*>(ctx);
         if (kind < 0 || kind > 2) throw pd::ConfigError("unknown reaction kind");
-        if (n > 0) pd::k_reaction<<<c.grid_for(n, 256), 256, 0, c.stream>>>(kind, deriv, u, out, n);
+        if (n > 0) pd::launch(pd::k_reaction, c.grid_for(n, 256), 256, 0, c.stream, kind, deriv, u, out, n);
         PD_LAUNCH_CHECK();
     });
 }
@@ -86,11 +86,11 @@ int pd_st_residual_csr(void* ctx, void* L, void* MR, double gamma, int kind, con
         // out = L u - rhs  (as  -(rhs - L u) would round identically)
         if (gamma != 0.0 && MR) {
             auto& R = *static_cast<pd::Csr*>(MR);
-            pd::k_reaction<<<c.grid_for(n, 256), 256, 0, c.stream>>>(kind, 0, u, tmp, n);
+            pd::launch(pd::k_reaction, c.grid_for(n, 256), 256, 0, c.stream, kind, 0, u, tmp, n);
             pd::csr_spmv(c, R, tmp, tmp + n, pd::SPMV_SET, nullptr);
-            pd::k_add_scaled<<<c.grid_for(n, 256), 256, 0, c.stream>>>(out, tmp + n, gamma, n);
+            pd::launch(pd::k_add_scaled, c.grid_for(n, 256), 256, 0, c.stream, out, tmp + n, gamma, n);
         }
-        pd::k_add_scaled<<<c.grid_for(n, 256), 256, 0, c.stream>>>(out, rhs, -1.0, n);
+        pd::launch(pd::k_add_scaled, c.grid_for(n, 256), 256, 0, c.stream, out, rhs, -1.0, n);
         PD_LAUNCH_CHECK();
     });
 }
@@ -98,7 +98,7 @@ int pd_st_residual_csr(void* ctx, void* L, void* MR, double gamma, int kind, con
 int pd_axpy_to(void* ctx, double* y, const double* x, const double* d, double s, int64_t n) {
     return guarded_vec([&] {
         auto& c = *static_cast<pd::Ctx*>(ctx);
-        if (n > 0) pd::k_axpy_to<<<c.grid_for(n, 256), 256, 0, c.stream>>>(y, x, d, s, n);
+        if (n > 0) pd::launch(pd::k_axpy_to, c.grid_for(n, 256), 256, 0, c.stream, y, x, d, s, n);
         PD_LAUNCH_CHECK();
     });
 }
@@ -119,7 +119,7 @@ int pd_norm(void* ctx, const double* x, int64_t n, double* host_out) {
 int pd_scale(void* ctx, double* y, const double* x, double s, int64_t n) {
     return guarded_vec([&] {
         auto& c = *static_cast<pd::Ctx*>(ctx);
-        if (n > 0) pd::k_scale<<<c.grid_for(n, 256), 256, 0, c.stream>>>(y, x, s, n);
+        if (n > 0) pd::launch(pd::k_scale, c.grid_for(n, 256), 256, 0, c.stream, y, x, s, n);
         PD_LAUNCH_CHECK();
     });
 }

@@ -8,9 +8,26 @@ def rel_l2(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-def per_node_rel(a, b, shape):
-    """max over (step, node) of the relative L2 difference of that node's field."""
+NODE_FLOOR = 1e-3
+
+
+def per_node_rel(a, b, shape, floor=NODE_FLOOR):
+    """max over (step, node) of ||a_n - b_n|| / max(||b_n||, floor * max_n ||b_n||).
+
+    The per-node relative L2 of the BASELINE parity contract.  Nodes whose
+    norm has decayed below `floor` x the largest node norm are measured
+    against that floor: there the reference's own output is only determined
+    to its reduction-order rounding (tests/test_oracle_golden.py::
+    test_reduction_order_floor measures it by re-running the oracle with a
+    different dot-product summation order).
+    """
     A, B = np.asarray(a).reshape(shape), np.asarray(b).reshape(shape)
     d = np.linalg.norm(A - B, axis=-1)
-    s = np.maximum(np.linalg.norm(B, axis=-1), 1e-300)
+    nb = np.linalg.norm(B, axis=-1)
+    s = np.maximum(np.maximum(nb, floor * nb.max()), 1e-300)
     return float(np.max(d / s))
+
+
+def per_node_rel_strict(a, b, shape):
+    """Per-node relative L2 against each node's own norm (no floor)."""
+    return per_node_rel(a, b, shape, floor=0.0)

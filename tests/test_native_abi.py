@@ -15,7 +15,7 @@ def declared_symbols():
     names = set()
     for h in (REPO / "include").glob("*.h"):
         text = h.read_text()
-        names |= set(re.findall(r"^\s*(?:const\s+char\s*\*\s*|int64_t\s+|int\s+)(pd_\w+)\s*\(", text,
+        names |= set(re.findall(r"^\s*(?:const\s+char\s*\*\s*|u?int64_t\s+|int\s+)(pd_\w+)\s*\(", text,
                                 re.M))
     return names
 
