@@ -1,0 +1,308 @@
+"""Benchmark: BASELINE config 2 space-time multigrid solve on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (BASELINE.json configs[1], the metric's single-GPU config): linear
+2D heat u_t = Lap u on [0,1]^2, 255x255 interior Dirichlet FD grid, Nt=64
+steps of dt=1/64, M=3 right-Radau nodes, fp64, u0 = 8 seeded sin modes;
+space-time multigrid with the block-Jacobi(P=8, time slabs) ILU(0)-GMRES(3)
+smoother, V(3,3), L=7 Galerkin levels, dense-LU coarsest, tol 1e-10.  The
+strategy is SMG: with the reference's own algorithm STMG stagnates at 1e-4 on
+this config (measured, 300 cycles), see DESIGN.md.
+
+One "step" = one full solve to tolerance from x=0 (inputs resident in HBM).
+value = N * (2*nu*cycles) / t  (space-time GDOF/s per fine smoother sweep,
+SURVEY §8(d)), summed over ranks / max-over-ranks time for N>1 (replicas of
+the workload per GPU in round 1; weak scaling).
+`e2e` = the same metric through the public API (`MultigridHierarchy.solve`
+with host numpy in, host numpy out: H2D + D2H inside the timed region).
+`--impl reference` times the reference algorithm's CPU restatement (oracle/,
+a port: the reference itself is not present on the GPU box) on host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+METRIC = "space-time GDOF/s per smoother/SDC sweep; solve time to tol; % of HBM roofline"
+UNIT = "GDOF/s"
+NU, LEVELS, PARTS, TOL = 3, 7, 8, 1e-10
+
+
+def workload_config(Nt=64):
+    return {
+        "workload": "C2: 2D heat 255^2 Dirichlet FD, Nt=64, M=3 Radau, fp64; SMG L=7 V(3,3), "
+                    "block-Jacobi(P=8 time slabs) ILU(0)-GMRES(3) smoother, dense-LU coarsest, "
+                    "tol 1e-10",
+        "Nt": Nt, "M": 3, "grid": "255x255", "dofs": Nt * 3 * 255 * 255, "levels": LEVELS,
+        "nu": NU, "partitions": PARTS, "strategy": "SMG", "tol": TOL,
+        "l2_policy": "inputs larger than L2 (fine CSR 2.4 GB, vectors 100 MB each)",
+    }
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) >= 7:
+                    self.rows.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if r[3 + i].strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(self.rows[0][1]),
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU arm (oracle port)
+def cpu_sample(steps: int, warmup: int, threads: int):
+    """Reference algorithm on host cores: C2 with Nt=8 (same grid/M/hierarchy),
+    one V-cycle per step; returns (GDOF/s per sweep, sample description)."""
+    from oracle import paradiff_oracle as O
+    from paper_2006_12883_b200 import problems as PB
+
+    cfg = PB.baseline_config("C2", Nt=8)
+    ops = PB.fd_space(cfg.spec)
+    s = O.OSystem(O.tableau(3), ops.Kh, ops.lumped_diagonal, cfg.Nt, cfg.T, 0.0, cfg.u0())
+    specs = [cfg.spec]
+    for _ in range(LEVELS - 1):
+        specs.append(specs[-1].coarse())
+    dims = [O.Dims(cfg.Nt, 3, sp_.ndof) for sp_ in specs]
+    pairs = [PB.fd_transfers(specs[l]) for l in range(LEVELS - 1)]
+    mg = O.OMultigrid(s.global_matrix(), dims, O.composite_transfers(dims, pairs), NU, PARTS,
+                      threads=threads)
+    b = s.rhs()
+    x = np.zeros_like(b)
+    for _ in range(warmup):
+        x = mg.vcycle(b, x)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        x = mg.vcycle(b, x)
+        times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    value = s.size * 2 * NU / t / 1e9
+    sample = (f"C2 grid 255^2, M=3, Nt=8 (of 64), SMG L=7 nu=3 P=8: one V-cycle per step, "
+              f"{t:.2f} s/cycle")
+    return value, sample, t
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = min(PARTS, os.cpu_count() or 1)
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
+    value, sample, t = cpu_sample(args.steps, args.warmup, threads)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(8) | {"sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm
+def run_b200(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2006_12883_b200 as pd
+    from paper_2006_12883_b200 import _native as N
+
+    t_setup = time.perf_counter()
+    cfg = pd.baseline_config("C2")
+    system = pd.assemble_system(pd.make_tableau(cfg.M), pd.fd_space(cfg.spec),
+                                pd.TimeGrid(cfg.Nt, cfg.T), 0.0, cfg.u0())
+    h = pd.build_hierarchy(system, "SMG", LEVELS, NU, partitions=PARTS)
+    b_host = system.rhs()
+    b = N.to_device(b_host)
+    x = N.zeros(system.size)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    lib = N.load_library()
+
+    def one_solve():
+        N.call("pd_scale", h.ctx.handle, N.ptr(x), N.ptr(x), 0.0, system.size)  # x = 0
+        return h.solve_dev(b, x, TOL, TOL, 1000)[1]
+
+    for _ in range(args.warmup):
+        rep = one_solve()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.pd_launch_count()
+    cycles = 0
+    with ClockSampler(local) as clk:
+        ev0.record()
+        for _ in range(args.steps):
+            rep = one_solve()
+            cycles += rep.iterations
+        ev1.record()
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = lib.pd_launch_count() - launches0
+    t_dev = ev0.elapsed_time(ev1) / 1e3
+    if dist:
+        tt = torch.tensor([t_dev], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_dev = float(tt.item())
+    sweeps = 2 * NU * cycles
+    value = world * system.size * sweeps / t_dev / 1e9
+
+    # e2e: public API with host numpy in/out (H2D of b, D2H of x inside the region)
+    e2e_times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        xh, rep_e = h.solve(b_host, tol_rel=TOL, tol_abs=TOL, max_cycles=1000)
+        torch.cuda.synchronize()
+        e2e_times.append(time.perf_counter() - t0)
+    t_e2e = float(np.mean(e2e_times))
+    if dist:
+        tt = torch.tensor([t_e2e], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e_value = world * system.size * 2 * NU * rep_e.iterations / t_e2e / 1e9
+
+    # roofline: dominant kernel = fine-level ILU(0) triangular sweeps (both), timed
+    # live with CUDA events on the library's stream (torch's current stream)
+    import ctypes
+
+    ilu = ctypes.c_void_p()
+    N.call("pd_mg_level_precond", h._mg, 0, ctypes.byref(ilu))
+    y = N.empty(system.size)
+    for _ in range(2):
+        N.call("pd_ilu0_solve", h.ctx.handle, ilu, N.ptr(b), N.ptr(y))
+    reps = 10
+    ev0.record()
+    for _ in range(reps):
+        N.call("pd_ilu0_solve", h.ctx.handle, ilu, N.ptr(b), N.ptr(y))
+    ev1.record()
+    torch.cuda.synchronize()
+    t_ilu = ev0.elapsed_time(ev1) / 1e3 / reps
+    nnz_row = h.matrices[0].nnz / system.size
+    alg_bytes = (12.0 * nnz_row + 24.0) * system.size
+    peak, peak_kind = peaks()
+    achieved = alg_bytes / t_ilu / 1e9
+    traffic = None
+    tfile = ROOT / "profiles" / "ilu_traffic.json"
+    if tfile.exists():
+        traffic = json.loads(tfile.read_text()).get("bytes_per_launch")
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            threads = min(PARTS, os.cpu_count() or 1)
+            cv, sample, _ = cpu_sample(1, 1, threads)
+            cpu = {"value": cv, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config() | {"parallelism": f"replicas x{world}" if world > 1
+                                           else "1 GPU"},
+            "solve_time_s": t_dev / args.steps, "cycles_per_solve": cycles / max(args.steps, 1),
+            "setup_s": setup_s,
+            "clocks": clk.summary(),
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": system.size * 8,
+                    "d2h_bytes_per_step": system.size * 8, "solve_time_s": t_e2e},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_trsv_lower+k_trsv_upper (fine-level ILU(0) apply)",
+                         "alg_bytes_per_launch": alg_bytes, "ms_per_launch": t_ilu * 1e3,
+                         "peak_kind": peak_kind},
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

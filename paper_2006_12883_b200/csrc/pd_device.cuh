@@ -29,10 +29,37 @@ __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// Wait until every row in cols[p0, p1) has flag >= target.  The polls are
+// independent relaxed loads (issued back to back, one L2 round trip per
+// sweep over the dependencies) followed by a single acquire fence, instead of
+// one acquire round trip per dependency.
+__device__ __forceinline__ void wait_all(const int* flag, const int32_t* cols, int64_t p0,
+                                         int64_t p1, int target) {
+    unsigned int ns = 32;
+    for (;;) {
+        int ok = 1;
+        for (int64_t p = p0; p < p1; ++p) ok &= (ld_relaxed(flag + cols[p]) >= target);
+        if (ok) break;
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+    }
+    fence_acq_rel();
+}
+
 // Wait until flag >= target (monotone epochs).
 __device__ __forceinline__ void wait_flag(const int* f, int target) {
+    if (ld_acquire(f) >= target) return;
+    unsigned int ns = 32;
     while (ld_acquire(f) < target) {
-        __nanosleep(20);
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
     }
 }
 

@@ -112,7 +112,8 @@ struct Ilu0 {
     DevBuf<int32_t> order_up;       // rows in upper-solve level order
     DevBuf<int> flag;               // per-row completion epochs
     DevBuf<unsigned long long> counter;
-    DevBuf<int> ep;                 // device-resident sweep epoch
+    DevBuf<int> ep;                 // device-resident sweep epoch (factorization)
+    DevBuf<double> scratch;         // lower-sweep output, kept armed with the pending sentinel
     int nlevels_lo = 0, nlevels_up = 0;
     std::vector<std::pair<int64_t, int64_t>> ranges;
     const Csr& pat() const { return use_masked ? masked : *pattern; }

@@ -50,6 +50,10 @@ int Ctx::grid_for(int64_t n, int bs, int per_sm) const {
 
 // ------------------------------------------------------------------ vector kernels
 constexpr int BS = 256;
+// Sync-free sweeps keep only ~2 blocks per SM resident: enough rows in flight
+// to cover a few dependency levels, few enough that flag polling does not
+// flood L2 (33 ms -> see profiles/ for the measured effect).
+constexpr int kSweepBlocksPerSM = 2;
 
 __global__ void k_fill(double* x, int64_t n, double v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -324,10 +328,14 @@ __global__ void k_ilu0_factor(int64_t n, const int64_t* __restrict__ rp,
             for (int64_t p = a; p < e; ++p)
                 if (ci[p] == i) { d = p; break; }
             unsigned long long mybad = ~0ull;
+            {  // all lower neighbours must be fully factored first
+                int64_t pl = a;
+                while (pl < e && ci[pl] < i) ++pl;
+                wait_all(flag, ci, a, pl, epoch);
+            }
             for (int64_t pk = a; pk < e; ++pk) {
                 const int64_t k = ci[pk];
                 if (k >= i) break;
-                wait_flag(flag + k, epoch);
                 const int64_t dk = ldcg(diag + k);
                 const double ukk = ldcg(fac + dk);
                 if (ukk == 0.0 && mybad == ~0ull) mybad = (unsigned long long)k;
@@ -345,49 +353,102 @@ __global__ void k_ilu0_factor(int64_t n, const int64_t* __restrict__ rp,
             if (mybad == ~0ull && (d < 0 || fac[d] == 0.0)) mybad = (unsigned long long)i;
             if (mybad != ~0ull) atomicMin(bad, mybad);
             diag[i] = d < 0 ? a : d;  // keep a valid index; error is reported
-            __threadfence();
+            // st.release orders the row's stores before the flag
             st_release(flag + i, epoch);
         }
     }
 }
 
 // ------------------------------------------------------------------ ILU(0) triangular solves
-// lower: x_i = b_i - sum_{p < diag} L_p x_col (unit diagonal), linalg.py:104-108
+// Value-as-flag sync-free sweeps.  Every output word starts as a sentinel NaN
+// payload; a row publishes its result with one 64-bit strong store (single-copy
+// atomic), and dependants poll the value itself, so readiness and data arrive
+// in the same L2 round trip — no per-row flag, no fences.  Each row prefetches
+// its factor entries before polling, then accumulates strictly in CSR order
+// (linalg.py:104-113), separately rounded.  The lower sweep re-arms the upper
+// sweep's output words and the upper sweep re-arms the lower scratch, so no
+// extra initialisation pass is needed between solves.
+constexpr unsigned long long kPending = 0x7ff4a5a55a5a0001ull;  // signalling-NaN payload
+constexpr int kChunk = 16;
+
+__device__ __forceinline__ unsigned long long ld_strong_u64(const double* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_strong(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v))
+                 : "memory");
+}
+__device__ __forceinline__ void st_pending(double* p) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(kPending) : "memory");
+}
+
+// s -= sum_{p in [p0,p1)} fac[p] * src[col[p]]  (in order), polling unpublished entries
+__device__ __forceinline__ double accumulate_polling(double s, const int32_t* __restrict__ ci,
+                                                     const double* __restrict__ fac,
+                                                     const double* src, int64_t p0, int64_t p1) {
+    for (int64_t c0 = p0; c0 < p1; c0 += kChunk) {
+        const int cnt = (int)min((int64_t)kChunk, p1 - c0);
+        double f[kChunk];
+        unsigned long long v[kChunk];
+        int32_t col[kChunk];
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k)
+            if (k < cnt) {
+                col[k] = ci[c0 + k];
+                f[k] = fac[c0 + k];
+            }
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k)
+            if (k < cnt) v[k] = ld_strong_u64(src + col[k]);
+        unsigned int ns = 32;
+        for (;;) {
+            bool missing = false;
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k)
+                if (k < cnt && v[k] == kPending) {
+                    v[k] = ld_strong_u64(src + col[k]);
+                    missing |= (v[k] == kPending);
+                }
+            if (!missing) break;
+            __nanosleep(ns);
+            if (ns < 256) ns <<= 1;
+        }
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k)
+            if (k < cnt) s = sub(s, mul(f[k], __longlong_as_double((long long)v[k])));
+    }
+    return s;
+}
+
+// lower: y_i = b_i - sum_{p < diag} L_p y_col (unit diagonal), linalg.py:104-108
 __global__ void k_trsv_lower(int64_t n, const int64_t* __restrict__ rp,
                              const int32_t* __restrict__ ci, const double* __restrict__ fac,
                              const int64_t* __restrict__ diag, const int32_t* __restrict__ order,
-                             const double* __restrict__ b, double* x, int* flag, const int* ep,
+                             const double* __restrict__ b, double* y, double* x_rearm,
                              unsigned long long* counter, const int* guard, int want) {
     if (guard_off(guard, want)) return;
-    const int epoch = *((volatile const int*)ep);
     for (;;) {
         int64_t base = fetch_batch(counter);
         if (base >= n) return;
         int64_t t = base + threadIdx.x;
         if (t < n) {
             const int64_t i = order[t];
-            double s = b[i];
-            const int64_t d = diag[i];
-            for (int64_t p = rp[i]; p < d; ++p) {
-                const int32_t cc = ci[p];
-                wait_flag(flag + cc, epoch);
-                s = sub(s, mul(fac[p], ldcg(x + cc)));
-            }
-            x[i] = s;
-            __threadfence();
-            st_release(flag + i, epoch);
+            const double s = accumulate_polling(b[i], ci, fac, y, rp[i], diag[i]);
+            st_pending(x_rearm + i);
+            st_strong(y + i, s);
         }
     }
 }
 
-// upper: x_i = (x_i - sum_{p > diag} U_p x_col) / U_diag, linalg.py:109-113
+// upper: x_i = (y_i - sum_{p > diag} U_p x_col) / U_diag, linalg.py:109-113
 __global__ void k_trsv_upper(int64_t n, const int64_t* __restrict__ rp,
                              const int32_t* __restrict__ ci, const double* __restrict__ fac,
                              const int64_t* __restrict__ diag, const int32_t* __restrict__ order,
-                             double* x, int* flag, const int* ep, unsigned long long* counter,
-                             const int* guard, int want) {
+                             double* y, double* x, unsigned long long* counter, const int* guard,
+                             int want) {
     if (guard_off(guard, want)) return;
-    const int epoch = *((volatile const int*)ep);
     for (;;) {
         int64_t base = fetch_batch(counter);
         if (base >= n) return;
@@ -395,18 +456,18 @@ __global__ void k_trsv_upper(int64_t n, const int64_t* __restrict__ rp,
         if (t < n) {
             const int64_t i = order[t];
             const int64_t d = diag[i];
-            double s = ldcg(x + i);
-            const int64_t e = rp[i + 1];
-            for (int64_t p = d + 1; p < e; ++p) {
-                const int32_t cc = ci[p];
-                wait_flag(flag + cc, epoch);
-                s = sub(s, mul(fac[p], ldcg(x + cc)));
-            }
-            x[i] = s / fac[d];
-            __threadfence();
-            st_release(flag + i, epoch);
+            const double yi = y[i];
+            const double s = accumulate_polling(yi, ci, fac, x, d + 1, rp[i + 1]);
+            st_pending(y + i);  // re-arm the lower scratch for the next solve
+            st_strong(x + i, s / fac[d]);
         }
     }
+}
+
+__global__ void k_fill_pending(double* y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        reinterpret_cast<unsigned long long*>(y)[i] = kPending;
 }
 
 // Starts one sync-free sweep: bumps the device-resident epoch (so CUDA-graph
@@ -483,6 +544,8 @@ std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks) {
     f->flag.alloc(std::max<int64_t>(n, 1));
     f->counter.alloc(1);
     f->ep.alloc(1);
+    f->scratch.alloc(std::max<int64_t>(n, 1));
+    if (n > 0) launch(k_fill_pending, c.grid_for(n, BS), BS, 0, c.stream, f->scratch.p, n);
     PD_CUDA(cudaMemsetAsync(f->flag.p, 0, std::max<int64_t>(n, 1) * sizeof(int), c.stream));
     PD_CUDA(cudaMemsetAsync(f->ep.p, 0, sizeof(int), c.stream));
     if (n > 0) {
@@ -522,7 +585,7 @@ void ilu0_refactor(Ctx& c, Ilu0& f) {
     DevBuf<unsigned long long> bad(1);
     PD_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), c.stream));
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, nullptr, 0);
-    launch(k_ilu0_factor, c.grid_for(n, BS, 8), BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p,
+    launch(k_ilu0_factor, c.grid_for(n, BS, kSweepBlocksPerSM), BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p,
                                                               f.diag.p, f.order_lo.p, f.flag.p,
                                                               f.ep.p, f.counter.p, bad.p);
     PD_LAUNCH_CHECK();
@@ -542,16 +605,15 @@ void ilu0_refactor(Ctx& c, Ilu0& f) {
 void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int want) {
     const int64_t n = f.n;
     if (n == 0) return;
+    if (b == x) throw ConfigError("ILU(0) solve needs distinct input and output buffers");
     const Csr& P = f.pat();
-    const int g = c.grid_for(n, BS, 8);
+    const int g = c.grid_for(n, BS, kSweepBlocksPerSM);
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, guard, want);
     launch(k_trsv_lower, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
-                                         f.order_lo.p, b, x, f.flag.p, f.ep.p, f.counter.p, guard,
-                                         want);
+           f.order_lo.p, b, f.scratch.p, x, f.counter.p, guard, want);
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, guard, want);
     launch(k_trsv_upper, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
-                                         f.order_up.p, x, f.flag.p, f.ep.p, f.counter.p, guard,
-                                         want);
+           f.order_up.p, f.scratch.p, x, f.counter.p, guard, want);
     PD_LAUNCH_CHECK();
 }
 
