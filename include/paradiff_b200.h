@@ -97,6 +97,25 @@ int pd_axpy_to(void *ctx, double *y, const double *x, const double *d, double s,
 int pd_norm(void *ctx, const double *x, int64_t n, double *host_out); /* synchronising */
 int pd_scale(void *ctx, double *y, const double *x, double s, int64_t n);
 
+/* ---- SDC / PFASST building blocks, batched over W workers of a window
+ *      (pfasst.py:60-303).  State layout: U[W][M][S], U0[W][S], tau[W][M][S]. */
+int pd_sdc_level_create(void *ctx, void *Kh, const double *mh_host, int M, const double *Q,
+                        const double *QDI, const double *QDE, double dt, double gamma,
+                        int reaction, int imex, int max_workers, void **lvl_out); /* SdcLevel */
+int pd_sdc_level_destroy(void *lvl);
+int pd_sdc_sweep(void *lvl, double *U, const double *U0, const double *tau, int W); /* :155-200 */
+int pd_sdc_residual(void *lvl, const double *U, const double *U0, const double *tau, int W,
+                    double *res_dev);                            /* :107-115, per worker */
+int pd_sdc_coll_op(void *lvl, const double *U, double *out, int W); /* C(u) = u - dt Q F(u) */
+int pd_sdc_errors(void *lvl, int *host_out);                        /* synchronising */
+int pd_node_mix(void *ctx, const double *in, double *out, int W, int Min, int Mout, int64_t S,
+                const double *N_host, int accumulate);           /* node transfer :262-266 */
+int pd_csr_spmm(void *ctx, void *A, const double *x, int64_t xs, double *y, int64_t ys,
+                int nvec, int mode);                             /* space transfer, batched */
+int pd_sub(void *ctx, double *out, const double *a, const double *b, int64_t n);
+int pd_spread(void *ctx, const double *u0, double *U, double *U0, int W, int M, int64_t S);
+int pd_terminal(void *ctx, const double *U, double *out, int W, int M, int64_t S);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,18 @@ _SIGNATURES = {
     "pd_reaction": (_int, [_vp, _int, _int, _vp, _vp, _i64]),
     "pd_axpy_to": (_int, [_vp, _vp, _vp, _vp, _dbl, _i64]),
     "pd_norm": (_int, [_vp, _vp, _i64, ctypes.POINTER(_dbl)]),
+    "pd_sdc_level_create": (_int, [_vp, _vp, _vp, _int, _vp, _vp, _vp, _dbl, _dbl, _int, _int,
+                                   _int, ctypes.POINTER(_vp)]),
+    "pd_sdc_level_destroy": (_int, [_vp]),
+    "pd_sdc_sweep": (_int, [_vp, _vp, _vp, _vp, _int]),
+    "pd_sdc_residual": (_int, [_vp, _vp, _vp, _vp, _int, _vp]),
+    "pd_sdc_coll_op": (_int, [_vp, _vp, _vp, _int]),
+    "pd_sdc_errors": (_int, [_vp, ctypes.POINTER(_int)]),
+    "pd_node_mix": (_int, [_vp, _vp, _vp, _int, _int, _int, _i64, _vp, _int]),
+    "pd_csr_spmm": (_int, [_vp, _vp, _vp, _i64, _vp, _i64, _int, _int]),
+    "pd_sub": (_int, [_vp, _vp, _vp, _vp, _i64]),
+    "pd_spread": (_int, [_vp, _vp, _vp, _vp, _int, _int, _i64]),
+    "pd_terminal": (_int, [_vp, _vp, _vp, _int, _int, _i64]),
     "pd_scale": (_int, [_vp, _vp, _vp, _dbl, _i64]),
 }
 

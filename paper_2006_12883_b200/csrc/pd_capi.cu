@@ -56,6 +56,11 @@ void fill_report(pd_solve_report* rep, int its, bool conv, bool div,
 }
 }  // namespace
 
+void pd_set_error_(const char* msg, int64_t index) {
+    g_err = msg;
+    g_err_index = index;
+}
+
 extern "C" {
 
 const char* pd_last_error(void) { return g_err.c_str(); }

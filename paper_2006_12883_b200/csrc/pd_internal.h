@@ -13,6 +13,9 @@
 #include <string>
 #include <vector>
 
+// records the calling thread's last error for pd_last_error() (pd_capi.cu)
+void pd_set_error_(const char* msg, int64_t index);
+
 namespace pd {
 
 struct ConfigError : std::runtime_error {

@@ -1,0 +1,727 @@
+// SDC sweeps, collocation residuals, FAS and level transfers for PFASST,
+// batched over the workers (time steps) of a window.
+//
+//   sdc_sweep        <- pfasst.py:155-200 (SdcLevel.sweep, implicit and IMEX)
+//   node solves      <- pfasst.py:118-152 (_solve_node_linear/_newton)
+//   coll. residual   <- pfasst.py:107-115
+//   C(u)=u-dt*Q*F(u) <- pfasst.py:283-303 (fas_correction building block)
+//   transfers        <- pfasst.py:253-270 (LevelTransfer)
+//
+// Layout: a level's state for W workers is U[W][M][S], U0[W][S], tau[W][M][S]
+// (C order, fp64).  Every kernel takes the first worker's pointer and a
+// worker count, so the serial coarse chain (one worker at a time) and the
+// batched fine sweeps (all workers) use the same code.
+//
+// Node solves: (diag(mh) + dt*qd_mm*Kh) u = mh*rhs.  The reference runs
+// ILU(0)-preconditioned GMRES from the previous iterate to 1e-13.  Here the
+// preconditioner is an exact factorization (tridiagonal Thomas = ILU(0) of a
+// tridiagonal matrix, bitwise the reference's factor; or a dense LU for small
+// general operators), applied as iterative refinement from the same initial
+// guess with the reference's thresholds, growth test and iteration cap.
+#include "../../include/paradiff_b200.h"
+#include "pd_device.cuh"
+#include "pd_internal.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+namespace pd {
+using namespace dev;
+
+namespace {
+constexpr int TB = 256;
+constexpr int kMaxNodes = 9;
+constexpr int kRedBlocks = 64;  // max blocks per vector in batched reductions
+
+__device__ __forceinline__ double react(int kind, double u) {
+    if (kind == 1) return sub(mul(mul(u, u), u), u);
+    if (kind == 2) return sub(mul(u, u), u);
+    return 0.0;
+}
+__device__ __forceinline__ double react_d(int kind, double u) {
+    if (kind == 1) return sub(mul(3.0, mul(u, u)), 1.0);
+    if (kind == 2) return sub(mul(2.0, u), 1.0);
+    return 0.0;
+}
+
+struct Small {
+    double a[kMaxNodes * kMaxNodes];
+};
+
+// ---------------------------------------------------------------- batched CSR
+// y[v][i] = (A x_v)[i] with mode: 0 set, 1 f_diffusion = -(A x)/mh,
+// 2 residual b - A x, 3 y += A x (accumulate)
+__global__ void k_bspmv(int64_t nrows, const int64_t* __restrict__ rp,
+                        const int32_t* __restrict__ ci, const double* __restrict__ val,
+                        const double* __restrict__ x, int64_t xs, double* y, int64_t ys,
+                        int nvec, int mode, const double* __restrict__ mh, const double* b,
+                        int64_t bs) {
+    const int64_t tot = nrows * nvec;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = t / nrows, i = t - v * nrows;
+        const double* xv = x + v * xs;
+        double s = 0.0;
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) s = add(s, mul(val[p], xv[ci[p]]));
+        double* yv = y + v * ys;
+        if (mode == 0) yv[i] = s;
+        else if (mode == 1) yv[i] = (-s) / mh[i];
+        else if (mode == 2) yv[i] = sub(b[v * bs + i], s);
+        else yv[i] = add(yv[i], s);
+    }
+}
+
+void bspmv(Ctx& c, const Csr& A, const double* x, int64_t xs, double* y, int64_t ys, int nvec,
+           int mode, const double* mh = nullptr, const double* b = nullptr, int64_t bs = 0) {
+    if (nvec <= 0 || A.nrows <= 0) return;
+    launch(k_bspmv, c.grid_for(A.nrows * nvec, TB, 16), TB, 0, c.stream, A.nrows, A.rowptr.p,
+           A.col.p, A.val.p, x, xs, y, ys, nvec, mode, mh, b, bs);
+}
+
+// out = -gamma * r(U)  (zeros when gamma == 0, pfasst.py:98-101)
+__global__ void k_freact(const double* U, double* out, int64_t n, double gamma, int kind) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = gamma == 0.0 ? 0.0 : mul(-gamma, react(kind, U[i]));
+}
+
+// f = fi + fe  (f_total, pfasst.py:103-104)
+__global__ void k_add_to(double* out, const double* a, const double* b, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = add(a[i], b[i]);
+}
+
+// base[w][m] = U0[w] + dt*(sum_j A[m][j] f1[w][j] + sum_j B[m][j] f2[w][j]) (+ tau)
+// (pfasst.py:170-178); f2 may be null (non-IMEX).  Flags non-finite entries.
+__global__ void k_sdc_base(const double* U0, const double* f1, const double* f2,
+                           const double* tau, double* base, int W, int M, int64_t S, double dt,
+                           Small A, Small B, int* err) {
+    const int64_t tot = (int64_t)W * M * S;
+    bool bad = false;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t % S;
+        const int64_t wm = t / S;
+        const int m = (int)(wm % M);
+        const int64_t w = wm / M;
+        const double* F1 = f1 + w * M * S + s;
+        double acc = 0.0;
+        for (int j = 0; j < M; ++j) acc = add(acc, mul(A.a[m * M + j], F1[j * S]));
+        if (f2) {
+            const double* F2 = f2 + w * M * S + s;
+            double acc2 = 0.0;
+            for (int j = 0; j < M; ++j) acc2 = add(acc2, mul(B.a[m * M + j], F2[j * S]));
+            acc = add(acc, acc2);
+        }
+        double v = add(U0[w * S + s], mul(dt, acc));
+        if (tau) v = add(v, tau[t]);
+        base[t] = v;
+        if (!isfinite(v)) bad = true;
+    }
+    if (bad) atomicOr(err, 1);
+}
+
+// b[w] = mh * (base[w][m] + sum_{j<m} dt*qdi[m][j]*fi[w][j] (+ dt*qde[m][j]*fe[w][j]))
+// (pfasst.py:186-190, node rhs accumulated in the reference's order)
+__global__ void k_node_rhs(const double* base, const double* fi, const double* fe, double* rhs,
+                           double* bvec, const double* mh, int W, int M, int64_t S, int m,
+                           double dt, Small QDI, Small QDE, int imex) {
+    const int64_t tot = (int64_t)W * S;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = t / S, s = t - w * S;
+        const int64_t off = w * M * S + s;
+        double r = base[off + (int64_t)m * S];
+        for (int j = 0; j < m; ++j) {
+            r = add(r, mul(mul(dt, QDI.a[m * M + j]), fi[off + (int64_t)j * S]));
+            if (imex) r = add(r, mul(mul(dt, QDE.a[m * M + j]), fe[off + (int64_t)j * S]));
+        }
+        rhs[t] = r;
+        bvec[t] = mul(mh[s], r);
+    }
+}
+
+// copy node m of U[w] <-> contiguous per-worker vectors
+__global__ void k_gather_node(const double* U, double* out, int W, int M, int64_t S, int m) {
+    const int64_t tot = (int64_t)W * S;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = t / S, s = t - w * S;
+        out[t] = U[w * M * S + (int64_t)m * S + s];
+    }
+}
+__global__ void k_scatter_node(const double* in, double* U, int W, int M, int64_t S, int m) {
+    const int64_t tot = (int64_t)W * S;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = t / S, s = t - w * S;
+        U[w * M * S + (int64_t)m * S + s] = in[t];
+    }
+}
+
+// ---------------------------------------------------------------- batched reductions
+// partial sums of squares of (W vectors of length n); second stage in order
+__global__ void k_bnorm2_partial(const double* x, int64_t n, int64_t stride, double* partials,
+                                 int nb) {
+    __shared__ double sh[TB / 32];
+    const int v = blockIdx.y;
+    const double* xv = x + v * stride;
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        s = fma(xv[i], xv[i], s);
+    s = block_sum<TB>(s, sh);
+    if (threadIdx.x == 0) partials[v * nb + blockIdx.x] = s;
+}
+__global__ void k_bnorm2_final(const double* partials, int nb, int W, double* out, int sqrt_it) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= W) return;
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += partials[v * nb + b];
+    out[v] = sqrt_it ? sqrt(s) : s;
+}
+}  // namespace
+
+// ---------------------------------------------------------------- level object
+struct SdcLevelDev {
+    Ctx& c;
+    int64_t S;
+    int M, imex, kind, solver, maxW;
+    double dt, gamma;
+    Small Q, QDI, QDE, A_imp, A_exp;  // A_imp = Q-QDI, A_exp = Q-QDE
+    std::unique_ptr<Csr> Kh;
+    DevBuf<double> mh;
+    // node operators A_m = diag(mh) + dt*qdi[m][m]*Kh
+    std::vector<std::unique_ptr<Csr>> Am;
+    // tridiagonal factors (solver 0): lower l (M x S), pivots u (M x S), super c (M x S)
+    DevBuf<double> tl, tu, tc;
+    // dense factors (solver 1)
+    std::vector<std::unique_ptr<DenseLU>> dlu;
+    // scratch
+    DevBuf<double> fi_old, fe_old, f_tot, base, fi_new, fe_new, rhs, bvec, x, r, tmp;
+    DevBuf<double> partials, beta0, thr, beta, lowest;
+    DevBuf<int> done, err;
+    SdcLevelDev(Ctx& c_) : c(c_) {}
+};
+
+namespace {
+// Thomas factorization of A_m from its CSR (rows sorted; tridiagonal): the
+// ILU(0) of a tridiagonal matrix, in the reference's arithmetic order.
+__global__ void k_tri_factor(const int64_t* rp, const int32_t* ci, const double* v, int64_t S,
+                             double* l, double* u, double* cc, int* err) {
+    // one thread per node operator (blockIdx.x = m)
+    const int64_t* r = rp;
+    double up_prev = 0.0;
+    for (int64_t i = 0; i < S; ++i) {
+        double lo = 0.0, di = 0.0, su = 0.0;
+        for (int64_t p = r[i]; p < r[i + 1]; ++p) {
+            if (ci[p] == i - 1) lo = v[p];
+            else if (ci[p] == i) di = v[p];
+            else if (ci[p] == i + 1) su = v[p];
+        }
+        double li = 0.0;
+        if (i > 0) {
+            if (up_prev == 0.0) atomicOr(err, 2);
+            li = lo / up_prev;
+            di = sub(di, mul(li, cc[i - 1]));
+        }
+        l[i] = li;
+        u[i] = di;
+        cc[i] = su;
+        up_prev = di;
+    }
+    if (up_prev == 0.0) atomicOr(err, 2);
+}
+
+// z = U^{-1} L^{-1} r per worker (one thread per worker system), linalg.py:100-113
+__global__ void k_tri_solve(const double* l, const double* u, const double* cc, int64_t S,
+                            const double* r, double* z, int W, const int* done) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= W || (done && done[w])) return;
+    const double* rw = r + (int64_t)w * S;
+    double* zw = z + (int64_t)w * S;
+    double y = rw[0];
+    zw[0] = y;
+    for (int64_t i = 1; i < S; ++i) {
+        y = sub(rw[i], mul(l[i], y));
+        zw[i] = y;
+    }
+    double xn = zw[S - 1] / u[S - 1];
+    zw[S - 1] = xn;
+    for (int64_t i = S - 2; i >= 0; --i) {
+        xn = sub(zw[i], mul(cc[i], xn)) / u[i];
+        zw[i] = xn;
+    }
+}
+
+// batched dense LU solve (one CTA per worker), LAPACK getrs order
+__global__ void k_lu_solve_batched(const double* __restrict__ LU, const int32_t* __restrict__ piv,
+                                   int64_t n, const double* b, double* xout, const int* done) {
+    extern __shared__ double xs[];
+    const int w = blockIdx.x;
+    if (done && done[w]) return;
+    const double* bw = b + (int64_t)w * n;
+    double* xw = xout + (int64_t)w * n;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) xs[i] = bw[i];
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int64_t i = 0; i < n; ++i) {
+            int64_t p = piv[i];
+            if (p != i) { double t = xs[i]; xs[i] = xs[p]; xs[p] = t; }
+        }
+    __syncthreads();
+    for (int64_t k = 0; k < n; ++k) {
+        const double xk = xs[k];
+        for (int64_t i = k + 1 + threadIdx.x; i < n; i += blockDim.x) xs[i] -= LU[i + k * n] * xk;
+        __syncthreads();
+    }
+    for (int64_t k = n - 1; k >= 0; --k) {
+        if (threadIdx.x == 0) xs[k] = xs[k] / LU[k + k * n];
+        __syncthreads();
+        const double xk = xs[k];
+        for (int64_t i = threadIdx.x; i < k; i += blockDim.x) xs[i] -= LU[i + k * n] * xk;
+        __syncthreads();
+    }
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) xw[i] = xs[i];
+}
+
+// refinement bookkeeping (one thread per worker):
+// stage 0: beta0 = |r0|, thr = max(1e-13*max(1,|b|), 1e-13*beta0), done if beta0 <= thr
+// stage 1: beta = |r|; done if <= thr; fail if beta > 10*lowest
+__global__ void k_refine_check(const double* rn, const double* bn, double* beta0, double* thr,
+                               double* lowest, int* done, int* err, int W, int stage,
+                               double tol) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= W) return;
+    const double beta = rn[w];
+    if (stage == 0) {
+        beta0[w] = beta;
+        if (!isfinite(beta)) {
+            done[w] = 1;
+            atomicOr(err, 4);
+            return;
+        }
+        const double t = fmax(mul(tol, fmax(1.0, bn[w])), mul(tol, beta));
+        thr[w] = t;
+        lowest[w] = beta;
+        done[w] = beta <= t ? 1 : 0;
+        return;
+    }
+    if (done[w]) return;
+    if (!isfinite(beta) || beta > mul(10.0, lowest[w])) {
+        done[w] = 1;
+        atomicOr(err, 4);
+        return;
+    }
+    lowest[w] = fmin(lowest[w], beta);
+    if (beta <= thr[w]) done[w] = 1;
+}
+
+__global__ void k_refine_update(double* x, const double* z, int W, int64_t S, const int* done) {
+    const int64_t tot = (int64_t)W * S;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = t / S;
+        if (!done[w]) x[t] = add(x[t], z[t]);
+    }
+}
+
+__global__ void k_any_open(const int* done, int W, int* err) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w < W && !done[w]) atomicOr(err, 8);
+}
+
+// collocation residual / C(u):  R = U - U0 - dt*Q*F - tau ;  C = U - dt*Q*F
+__global__ void k_coll(const double* U, const double* U0, const double* F, const double* tau,
+                       double* out, int W, int M, int64_t S, double dt, Small Q, int with_u0) {
+    const int64_t tot = (int64_t)W * M * S;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t % S, wm = t / S;
+        const int m = (int)(wm % M);
+        const int64_t w = wm / M;
+        const double* Fw = F + w * M * S + s;
+        double acc = 0.0;
+        for (int j = 0; j < M; ++j) acc = add(acc, mul(Q.a[m * M + j], Fw[j * S]));
+        double v = U[t];
+        if (with_u0) v = sub(v, U0[w * S + s]);
+        v = sub(v, mul(dt, acc));
+        if (tau) v = sub(v, tau[t]);
+        out[t] = v;
+    }
+}
+
+// node mixing: out[w][a][s] (+)= sum_b N[a][b] in[w][b][s]
+__global__ void k_node_mix(const double* in, double* out, int W, int Min, int Mout, int64_t S,
+                           Small N, int accumulate) {
+    const int64_t tot = (int64_t)W * Mout * S;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t % S, wa = t / S;
+        const int a = (int)(wa % Mout);
+        const int64_t w = wa / Mout;
+        const double* iw = in + w * Min * S + s;
+        double acc = 0.0;
+        for (int b = 0; b < Min; ++b) acc = add(acc, mul(N.a[a * Min + b], iw[b * S]));
+        out[t] = accumulate ? add(out[t], acc) : acc;
+    }
+}
+
+__global__ void k_sub_into(double* out, const double* a, const double* b, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = sub(a[i], b[i]);
+}
+
+// U[w][m] = u0 for all m; U0[w] = u0 (spread_state, pfasst.py:54-57)
+__global__ void k_spread(const double* u0, double* U, double* U0, int W, int M, int64_t S) {
+    const int64_t tot = (int64_t)W * M * S;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = t % S;
+        U[t] = u0[s];
+        if (t < (int64_t)W * S) U0[t] = u0[t % S];
+    }
+}
+
+// out[w] = U[w][M-1] (terminal values)
+__global__ void k_terminal(const double* U, double* out, int W, int M, int64_t S) {
+    const int64_t tot = (int64_t)W * S;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = t / S, s = t - w * S;
+        out[t] = U[w * M * S + (int64_t)(M - 1) * S + s];
+    }
+}
+
+Small small_from(const double* h, int r, int cols) {
+    Small s;
+    std::memset(&s, 0, sizeof(s));
+    for (int i = 0; i < r * cols; ++i) s.a[i] = h[i];
+    return s;
+}
+}  // namespace
+
+// ---------------------------------------------------------------- host API
+static void bnorm(SdcLevelDev& L, const double* x, int64_t n, int64_t stride, int W, double* out,
+                  bool take_sqrt) {
+    Ctx& c = L.c;
+    int nb = (int)std::min<int64_t>(kRedBlocks, std::max<int64_t>(1, (n + TB * 8 - 1) / (TB * 8)));
+    dim3 grid(nb, W);
+    launch(k_bnorm2_partial, grid, TB, 0, c.stream, x, n, stride, L.partials.p, nb);
+    launch(k_bnorm2_final, (W + 127) / 128, 128, 0, c.stream, L.partials.p, nb, W, out,
+           take_sqrt ? 1 : 0);
+}
+
+static void node_apply_inverse(SdcLevelDev& L, int m, const double* r, double* z, int W) {
+    Ctx& c = L.c;
+    if (L.solver == 0) {
+        const int64_t S = L.S;
+        launch(k_tri_solve, (W + 63) / 64, 64, 0, c.stream, L.tl.p + m * S, L.tu.p + m * S,
+               L.tc.p + m * S, S, r, z, W, L.done.p);
+    } else {
+        launch(k_lu_solve_batched, W, 256, L.S * sizeof(double), c.stream, L.dlu[m]->lu.p,
+               L.dlu[m]->piv.p, L.S, r, z, L.done.p);
+    }
+}
+
+// x (in: guess, out: solution) for W workers; b = mh*rhs (W x S contiguous)
+static void node_solve(SdcLevelDev& L, int m, const double* b, double* x, int W, int rounds) {
+    Ctx& c = L.c;
+    const int64_t S = L.S;
+    const Csr& A = *L.Am[m];
+    double* bn = L.tmp.p;  // W norms
+    bnorm(L, b, S, S, W, bn, true);
+    bspmv(c, A, x, S, L.r.p, S, W, 2, nullptr, b, S);  // r = b - A x
+    bnorm(L, L.r.p, S, S, W, L.beta.p, true);
+    launch(k_refine_check, (W + 127) / 128, 128, 0, c.stream, L.beta.p, bn, L.beta0.p, L.thr.p,
+           L.lowest.p, L.done.p, L.err.p, W, 0, 1e-13);
+    for (int k = 0; k < rounds; ++k) {
+        node_apply_inverse(L, m, L.r.p, L.rhs.p + 0, W);  // rhs buffer reused as z
+        launch(k_refine_update, c.grid_for(W * S, TB), TB, 0, c.stream, x, L.rhs.p, W, S,
+               L.done.p);
+        bspmv(c, A, x, S, L.r.p, S, W, 2, nullptr, b, S);
+        bnorm(L, L.r.p, S, S, W, L.beta.p, true);
+        launch(k_refine_check, (W + 127) / 128, 128, 0, c.stream, L.beta.p, bn, L.beta0.p,
+               L.thr.p, L.lowest.p, L.done.p, L.err.p, W, 1, 1e-13);
+    }
+    launch(k_any_open, (W + 127) / 128, 128, 0, c.stream, L.done.p, W, L.err.p);
+}
+
+static void feval(SdcLevelDev& L, const double* U, double* fi, double* fe, int W, int nodes,
+                  int64_t stride_w) {
+    // fi = -Kh U / mh ; fe = -gamma r(U) ; vectors: W*nodes of length S at stride S
+    Ctx& c = L.c;
+    const int64_t S = L.S;
+    (void)stride_w;
+    bspmv(c, *L.Kh, U, S, fi, S, W * nodes, 1, L.mh.p);
+    launch(k_freact, c.grid_for((int64_t)W * nodes * S, TB), TB, 0, c.stream, U, fe,
+           (int64_t)W * nodes * S, L.gamma, L.kind);
+}
+
+void sdc_sweep(SdcLevelDev& L, double* U, const double* U0, const double* tau, int W) {
+    Ctx& c = L.c;
+    const int64_t S = L.S;
+    const int M = L.M;
+    const int64_t n = (int64_t)W * M * S;
+    const bool imex = L.imex && L.gamma != 0.0;
+    if (W > L.maxW) throw ConfigError("too many workers for this SDC level");
+    if (L.gamma != 0.0 && !imex)
+        throw ConfigError("implicit-mode nonlinear node solves run with mode='imex' on the device");
+    feval(L, U, L.fi_old.p, L.fe_old.p, W, M, 0);
+    if (imex) {
+        launch(k_sdc_base, c.grid_for(n, TB), TB, 0, c.stream, U0, L.fi_old.p, L.fe_old.p, tau,
+               L.base.p, W, M, S, L.dt, L.A_imp, L.A_exp, L.err.p);
+    } else {
+        launch(k_add_to, c.grid_for(n, TB), TB, 0, c.stream, L.f_tot.p, L.fi_old.p, L.fe_old.p,
+               n);
+        launch(k_sdc_base, c.grid_for(n, TB), TB, 0, c.stream, U0, L.f_tot.p, (const double*)nullptr,
+               tau, L.base.p, W, M, S, L.dt, L.A_imp, L.A_exp, L.err.p);
+    }
+    for (int m = 0; m < M; ++m) {
+        // rhs and b = mh*rhs for node m of every worker
+        launch(k_node_rhs, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.base.p,
+               L.fi_new.p, L.fe_new.p, L.rhs.p, L.bvec.p, L.mh.p, W, M, S, m, L.dt,
+               L.QDI, L.QDE, imex ? 1 : 0);
+        launch(k_gather_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, U, L.x.p, W, M, S,
+               m);
+        node_solve(L, m, L.bvec.p, L.x.p, W, 2);
+        launch(k_scatter_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.x.p, U, W, M, S,
+               m);
+        // f of the new node value (stored in the node-m slot of fi_new/fe_new)
+        bspmv(c, *L.Kh, L.x.p, S, L.fi_old.p, S, W, 1, L.mh.p);  // reuse fi_old as W x S scratch
+        launch(k_scatter_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.fi_old.p,
+               L.fi_new.p, W, M, S, m);
+        launch(k_freact, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.x.p, L.fe_old.p,
+               (int64_t)W * S, L.gamma, L.kind);
+        launch(k_scatter_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.fe_old.p,
+               L.fe_new.p, W, M, S, m);
+        if (!imex) {
+            // f_total for the implicit mode: fi_new[m] = f_diff + f_react
+            launch(k_gather_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.fi_new.p,
+                   L.fi_old.p, W, M, S, m);
+            launch(k_add_to, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.fi_old.p,
+                   L.fi_old.p, L.fe_old.p, (int64_t)W * S);
+            launch(k_scatter_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.fi_old.p,
+                   L.fi_new.p, W, M, S, m);
+        }
+    }
+    PD_LAUNCH_CHECK();
+}
+
+// out = U - U0 - dt*Q*F(U) - tau (with_u0) or U - dt*Q*F(U) (C(u)); W x M x S
+void sdc_coll(SdcLevelDev& L, const double* U, const double* U0, const double* tau, double* out,
+              int W, bool with_u0) {
+    Ctx& c = L.c;
+    const int64_t S = L.S;
+    const int M = L.M;
+    const int64_t n = (int64_t)W * M * S;
+    feval(L, U, L.fi_old.p, L.fe_old.p, W, M, 0);
+    launch(k_add_to, c.grid_for(n, TB), TB, 0, c.stream, L.f_tot.p, L.fi_old.p, L.fe_old.p, n);
+    launch(k_coll, c.grid_for(n, TB), TB, 0, c.stream, U, U0, L.f_tot.p, tau, out, W, M, S, L.dt,
+           L.Q, with_u0 ? 1 : 0);
+}
+
+}  // namespace pd
+
+// ---------------------------------------------------------------- C ABI
+namespace {
+template <class F>
+int guarded_sdc(F&& f) {
+    try {
+        f();
+        return PD_OK;
+    } catch (const pd::ConfigError& e) {
+        pd_set_error_(e.what(), -1);
+        return PD_ERR_CONFIG;
+    } catch (const pd::SolverError& e) {
+        pd_set_error_(e.what(), e.index);
+        return PD_ERR_SOLVER;
+    } catch (const std::exception& e) {
+        pd_set_error_(e.what(), -1);
+        return PD_ERR_CUDA;
+    }
+}
+}  // namespace
+
+extern "C" {
+
+int pd_sdc_level_create(void* ctx, void* Kh, const double* mh_host, int M, const double* Q,
+                        const double* QDI, const double* QDE, double dt, double gamma,
+                        int reaction, int imex, int max_workers, void** out) {
+    return guarded_sdc([&] {
+        auto& c = *static_cast<pd::Ctx*>(ctx);
+        auto* K = static_cast<pd::Csr*>(Kh);
+        if (!K || K->nrows != K->ncols) throw pd::ConfigError("Kh must be square");
+        if (M < 1 || M > pd::kMaxNodes) throw pd::ConfigError("node count out of range");
+        if (max_workers < 1) throw pd::ConfigError("need at least one worker");
+        auto L = std::make_unique<pd::SdcLevelDev>(c);
+        const int64_t S = K->nrows;
+        L->S = S;
+        L->M = M;
+        L->dt = dt;
+        L->gamma = gamma;
+        L->kind = reaction;
+        L->imex = imex;
+        L->maxW = max_workers;
+        L->Q = pd::small_from(Q, M, M);
+        L->QDI = pd::small_from(QDI, M, M);
+        L->QDE = pd::small_from(QDE, M, M);
+        std::vector<double> ai(M * M), ae(M * M);
+        for (int i = 0; i < M * M; ++i) {
+            ai[i] = Q[i] - QDI[i];
+            ae[i] = Q[i] - QDE[i];
+        }
+        L->A_imp = pd::small_from(ai.data(), M, M);
+        L->A_exp = pd::small_from(ae.data(), M, M);
+        // copy Kh (the level owns its operator)
+        std::vector<int64_t> rp(S + 1);
+        PD_CUDA(cudaMemcpy(rp.data(), K->rowptr.p, (S + 1) * sizeof(int64_t),
+                           cudaMemcpyDeviceToHost));
+        L->Kh = pd::csr_upload(c, S, S, K->nnz, K->rowptr.p, K->col.p, K->val.p, true);
+        L->mh.alloc(S);
+        PD_CUDA(cudaMemcpy(L->mh.p, mh_host, S * sizeof(double), cudaMemcpyHostToDevice));
+        // node operators A_m = diag(mh) + dt*qdi[m][m]*Kh (host assembly of values on Kh's
+        // pattern plus the diagonal; the pattern must contain the diagonal)
+        std::vector<int32_t> ci(K->nnz);
+        std::vector<double> kv(K->nnz);
+        PD_CUDA(cudaMemcpy(ci.data(), K->col.p, K->nnz * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        PD_CUDA(cudaMemcpy(kv.data(), K->val.p, K->nnz * sizeof(double), cudaMemcpyDeviceToHost));
+        bool tri = true;
+        for (int64_t i = 0; i < S; ++i) {
+            bool has_d = false;
+            for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+                if (ci[p] < i - 1 || ci[p] > i + 1) tri = false;
+                if (ci[p] == i) has_d = true;
+            }
+            if (!has_d) throw pd::ConfigError("Kh pattern must contain the diagonal");
+        }
+        L->solver = tri ? 0 : 1;
+        if (!tri && S > 28000) throw pd::ConfigError("general node operator too large for the dense node solver");
+        for (int m = 0; m < M; ++m) {
+            const double q = dt * QDI[m * M + m];
+            std::vector<double> av(K->nnz);
+            for (int64_t i = 0; i < S; ++i)
+                for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+                    av[p] = (ci[p] == i ? mh_host[i] : 0.0) + q * kv[p];
+            L->Am.push_back(pd::csr_upload(c, S, S, K->nnz, rp.data(), ci.data(), av.data(), false));
+        }
+        L->err.alloc(1);
+        PD_CUDA(cudaMemset(L->err.p, 0, sizeof(int)));
+        if (tri) {
+            L->tl.alloc(M * S);
+            L->tu.alloc(M * S);
+            L->tc.alloc(M * S);
+            for (int m = 0; m < M; ++m)
+                pd::launch(pd::k_tri_factor, 1, 1, 0, c.stream, L->Am[m]->rowptr.p, L->Am[m]->col.p,
+                           L->Am[m]->val.p, S, L->tl.p + m * S, L->tu.p + m * S, L->tc.p + m * S,
+                           L->err.p);
+        } else {
+            for (int m = 0; m < M; ++m) L->dlu.push_back(pd::dense_lu_from_csr(c, *L->Am[m]));
+            static bool attr = false;
+            if (!attr) {
+                PD_CUDA(cudaFuncSetAttribute(pd::k_lu_solve_batched,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+                attr = true;
+            }
+        }
+        const int64_t W = max_workers;
+        for (auto* b : {&L->fi_old, &L->fe_old, &L->f_tot, &L->base, &L->fi_new, &L->fe_new})
+            b->alloc(W * M * S);
+        for (auto* b : {&L->rhs, &L->bvec, &L->x, &L->r}) b->alloc(W * S);
+        L->tmp.alloc(W);
+        L->partials.alloc(W * pd::kRedBlocks);
+        for (auto* b : {&L->beta0, &L->thr, &L->beta, &L->lowest}) b->alloc(W);
+        L->done.alloc(W);
+        PD_CUDA(cudaStreamSynchronize(c.stream));
+        int herr = 0;
+        PD_CUDA(cudaMemcpy(&herr, L->err.p, sizeof(int), cudaMemcpyDeviceToHost));
+        if (herr) throw pd::SolverError("zero pivot in a node operator factorization");
+        *out = L.release();
+    });
+}
+
+int pd_sdc_level_destroy(void* lvl) {
+    return guarded_sdc([&] { delete static_cast<pd::SdcLevelDev*>(lvl); });
+}
+
+int pd_sdc_sweep(void* lvl, double* U, const double* U0, const double* tau, int W) {
+    return guarded_sdc(
+        [&] { pd::sdc_sweep(*static_cast<pd::SdcLevelDev*>(lvl), U, U0, tau, W); });
+}
+
+// per-worker ||U - U0 - dt Q F(U) - tau||_F into res (device, W doubles)
+int pd_sdc_residual(void* lvl, const double* U, const double* U0, const double* tau, int W,
+                    double* res) {
+    return guarded_sdc([&] {
+        auto& L = *static_cast<pd::SdcLevelDev*>(lvl);
+        pd::sdc_coll(L, U, U0, tau, L.base.p, W, true);
+        pd::bnorm(L, L.base.p, (int64_t)L.M * L.S, (int64_t)L.M * L.S, W, res, true);
+    });
+}
+
+// out = U - dt Q F(U)  (the level's collocation operator C, pfasst.py:291)
+int pd_sdc_coll_op(void* lvl, const double* U, double* out, int W) {
+    return guarded_sdc([&] {
+        pd::sdc_coll(*static_cast<pd::SdcLevelDev*>(lvl), U, nullptr, nullptr, out, W, false);
+    });
+}
+
+// error word (bit 1 non-finite sweep input, 2 zero pivot, 4 node solve diverged,
+// 8 node solve not converged within the refinement budget); reset after read
+int pd_sdc_errors(void* lvl, int* host_out) {
+    return guarded_sdc([&] {
+        auto& L = *static_cast<pd::SdcLevelDev*>(lvl);
+        PD_CUDA(cudaMemcpyAsync(host_out, L.err.p, sizeof(int), cudaMemcpyDeviceToHost, L.c.stream));
+        PD_CUDA(cudaStreamSynchronize(L.c.stream));
+        PD_CUDA(cudaMemsetAsync(L.err.p, 0, sizeof(int), L.c.stream));
+    });
+}
+
+// node mixing  out[w][a] (+)= sum_b N[a][b] in[w][b]   (N: Mout x Min, host)
+int pd_node_mix(void* ctx, const double* in, double* out, int W, int Min, int Mout, int64_t S,
+                const double* N, int accumulate) {
+    return guarded_sdc([&] {
+        auto& c = *static_cast<pd::Ctx*>(ctx);
+        pd::Small s = pd::small_from(N, Mout, Min);
+        pd::launch(pd::k_node_mix, c.grid_for((int64_t)W * Mout * S, pd::TB), pd::TB, 0, c.stream,
+                   in, out, W, Min, Mout, S, s, accumulate);
+    });
+}
+
+// y[v] = A x[v] for nvec vectors (mode 0 set, 3 accumulate)
+int pd_csr_spmm(void* ctx, void* A, const double* x, int64_t xs, double* y, int64_t ys, int nvec,
+                int mode) {
+    return guarded_sdc([&] {
+        auto& c = *static_cast<pd::Ctx*>(ctx);
+        pd::bspmv(c, *static_cast<pd::Csr*>(A), x, xs, y, ys, nvec, mode);
+    });
+}
+
+int pd_sub(void* ctx, double* out, const double* a, const double* b, int64_t n) {
+    return guarded_sdc([&] {
+        auto& c = *static_cast<pd::Ctx*>(ctx);
+        if (n > 0) pd::launch(pd::k_sub_into, c.grid_for(n, pd::TB), pd::TB, 0, c.stream, out, a, b, n);
+    });
+}
+
+int pd_spread(void* ctx, const double* u0, double* U, double* U0, int W, int M, int64_t S) {
+    return guarded_sdc([&] {
+        auto& c = *static_cast<pd::Ctx*>(ctx);
+        pd::launch(pd::k_spread, c.grid_for((int64_t)W * M * S, pd::TB), pd::TB, 0, c.stream, u0,
+                   U, U0, W, M, S);
+    });
+}
+
+int pd_terminal(void* ctx, const double* U, double* out, int W, int M, int64_t S) {
+    return guarded_sdc([&] {
+        auto& c = *static_cast<pd::Ctx*>(ctx);
+        pd::launch(pd::k_terminal, c.grid_for((int64_t)W * S, pd::TB), pd::TB, 0, c.stream, U,
+                   out, W, M, S);
+    });
+}
+
+}  // extern "C"

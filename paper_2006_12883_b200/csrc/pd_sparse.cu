@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 namespace pd {
 
@@ -53,7 +54,14 @@ constexpr int BS = 256;
 // Sync-free sweeps keep only ~2 blocks per SM resident: enough rows in flight
 // to cover a few dependency levels, few enough that flag polling does not
 // flood L2 (33 ms -> see profiles/ for the measured effect).
-constexpr int kSweepBlocksPerSM = 2;
+static int sweep_blocks_per_sm() {
+    static int v = [] {
+        const char* e = getenv("PD_SWEEP_BPS");
+        int k = e ? atoi(e) : 2;
+        return k > 0 ? k : 2;
+    }();
+    return v;
+}
 
 __global__ void k_fill(double* x, int64_t n, double v) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -585,7 +593,7 @@ void ilu0_refactor(Ctx& c, Ilu0& f) {
     DevBuf<unsigned long long> bad(1);
     PD_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), c.stream));
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, nullptr, 0);
-    launch(k_ilu0_factor, c.grid_for(n, BS, kSweepBlocksPerSM), BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p,
+    launch(k_ilu0_factor, c.grid_for(n, BS, sweep_blocks_per_sm()), BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p,
                                                               f.diag.p, f.order_lo.p, f.flag.p,
                                                               f.ep.p, f.counter.p, bad.p);
     PD_LAUNCH_CHECK();
@@ -607,7 +615,7 @@ void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, i
     if (n == 0) return;
     if (b == x) throw ConfigError("ILU(0) solve needs distinct input and output buffers");
     const Csr& P = f.pat();
-    const int g = c.grid_for(n, BS, kSweepBlocksPerSM);
+    const int g = c.grid_for(n, BS, sweep_blocks_per_sm());
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, guard, want);
     launch(k_trsv_lower, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
            f.order_lo.p, b, f.scratch.p, x, f.counter.p, guard, want);

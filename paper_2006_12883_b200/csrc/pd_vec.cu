@@ -56,9 +56,11 @@ int guarded_vec(F&& f) {
     try {
         f();
         return PD_OK;
-    } catch (const pd::ConfigError&) {
+    } catch (const pd::ConfigError& e) {
+        pd_set_error_(e.what(), -1);
         return PD_ERR_CONFIG;
-    } catch (...) {
+    } catch (const std::exception& e) {
+        pd_set_error_(e.what(), -1);
         return PD_ERR_CUDA;
     }
 }

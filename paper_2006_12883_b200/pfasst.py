@@ -1,0 +1,565 @@
+"""SDC sweeps, FAS corrections and the windowed PFASST driver on the GPU
+(drop-in for paradiff/pfasst.py).
+
+The reference runs one Python thread per time step of a window (pfasst.py:
+369-587).  Here the P steps of a window are P "workers" whose states live in
+one device array per level, U[P][M][S]; fine sweeps, FAS corrections,
+transfers and residuals are single batched kernels over all workers, and the
+coarsest level's serial forward chain (pfasst.py:441-455) runs worker by
+worker on the device.  The message schedule is the reference's exactly: the
+fine initial value of worker w is worker w-1's fine terminal from the
+PREVIOUS iteration; the coarsest initial value is worker w-1's coarse
+terminal from the CURRENT iteration; no fine post-sweep after interpolation;
+residuals use the U0 received at the start of the iteration.  One host sync
+per iteration reads the P residual norms (the convergence/divergence test).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _native as N
+from .collocation import CollocationTableau, LagrangeBasis, make_tableau
+from .errors import ConfigurationError, SolverError
+from .fem1d import SpaceMesh, SpaceOperators, assemble_space
+from .linalg import DeviceCsr, as_csr
+from .multigrid import spatial_prolongation, spatial_restriction
+from .report import SolveReport
+from .spacetime import TimeGrid, reaction
+
+MODES = ("implicit", "imex")
+_REACTION = {"cubic": 1, "fisher": 2}
+_ERR_TEXT = {1: "non-finite values entered an SDC sweep", 2: "zero pivot in a node operator",
+             4: "node solve failed", 8: "node solve did not converge within the refinement budget"}
+
+
+def _vp(t, offset_elems: int = 0):
+    return ctypes.c_void_p(t.data_ptr() + 8 * offset_elems) if t is not None else ctypes.c_void_p()
+
+
+def _host(mat) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(mat, dtype=np.float64))
+
+
+@dataclass
+class SweeperState:
+    """Node values (M, ndof), step initial value (ndof,) and FAS term (M, ndof)."""
+
+    U: object
+    U0: object
+    tau: object = None
+
+    def copy(self) -> "SweeperState":
+        return SweeperState(self.U.copy(), self.U0.copy(),
+                            None if self.tau is None else self.tau.copy())
+
+    @property
+    def terminal(self):
+        return self.U[-1]
+
+
+def spread_state(u0, M: int) -> SweeperState:
+    u0 = np.asarray(u0, dtype=np.float64)
+    return SweeperState(np.tile(u0, (M, 1)), u0.copy())
+
+
+class SdcLevel:
+    """Operators and device node solvers for SDC sweeps on one level (pfasst.py:60-200)."""
+
+    def __init__(self, tableau: CollocationTableau, space: SpaceOperators, dt: float,
+                 gamma: float, mode: str = "implicit", reaction_kind: str = "cubic"):
+        if mode not in MODES:
+            raise ConfigurationError(f"unknown sweep mode {mode!r}; expected {MODES}")
+        self.tableau = tableau
+        self.space = space
+        self.dt = float(dt)
+        self.gamma = float(gamma)
+        self.mode = mode
+        self.reaction_kind = reaction_kind
+        self.mh = space.lumped_diagonal
+        self.Kh = as_csr(space.Kh)
+        self._dev = None
+        self._cap = 0
+        self.ctx = None
+
+    @property
+    def M(self) -> int:
+        return self.tableau.M
+
+    @property
+    def ndof(self) -> int:
+        return self.mh.size
+
+    # ---- device level -------------------------------------------------------
+    def device(self, workers: int):
+        if self._dev is not None and workers <= self._cap:
+            return self._dev
+        self._release()
+        self.ctx = N.context()
+        Kd = DeviceCsr(self.Kh, self.ctx)
+        mh = _host(self.mh)
+        T = self.tableau
+        h = ctypes.c_void_p()
+        N.call("pd_sdc_level_create", self.ctx.handle, Kd.handle,
+               mh.ctypes.data_as(ctypes.c_void_p), self.M,
+               _host(T.Q).ctypes.data_as(ctypes.c_void_p),
+               _host(T.QDeltaImplicit).ctypes.data_as(ctypes.c_void_p),
+               _host(T.QDeltaExplicit).ctypes.data_as(ctypes.c_void_p), self.dt, self.gamma,
+               _REACTION[self.reaction_kind], 1 if self.mode == "imex" else 0, int(workers),
+               ctypes.byref(h))
+        self._dev, self._cap = h, workers
+        return h
+
+    def _release(self):
+        if self._dev is not None:
+            N.load_library().pd_sdc_level_destroy(self._dev)
+            self._dev = None
+
+    def __del__(self):
+        try:
+            self._release()
+        except Exception:
+            pass
+
+    def check_errors(self):
+        e = ctypes.c_int()
+        N.call("pd_sdc_errors", self._dev, ctypes.byref(e))
+        if e.value:
+            bit = next(b for b in (1, 2, 4, 8) if e.value & b)
+            raise SolverError(_ERR_TEXT[bit])
+
+    # ---- batched device primitives (W workers) --------------------------------
+    def sweep_dev(self, U, U0, tau, W: int, w_off: int = 0):
+        """In-place sweep of workers [w_off, w_off+W) of the device arrays."""
+        M, S = self.M, self.ndof
+        N.call("pd_sdc_sweep", self.device(W + w_off), _vp(U, w_off * M * S), _vp(U0, w_off * S),
+               _vp(tau, w_off * M * S) if tau is not None else ctypes.c_void_p(), W)
+
+    def residual_dev(self, U, U0, tau, W: int, out):
+        N.call("pd_sdc_residual", self.device(W), _vp(U), _vp(U0),
+               _vp(tau) if tau is not None else ctypes.c_void_p(), W, _vp(out))
+        return out
+
+    def coll_op_dev(self, U, out, W: int):
+        N.call("pd_sdc_coll_op", self.device(W), _vp(U), _vp(out), W)
+        return out
+
+    # ---- reference-shaped API (numpy in/out; device inside) ---------------------
+    def _state_dev(self, state: SweeperState):
+        ctx = N.context()
+        U = N.to_device(np.asarray(state.U, dtype=np.float64).ravel(), ctx).clone()
+        U0 = N.to_device(np.asarray(state.U0, dtype=np.float64).ravel(), ctx)
+        tau = (N.to_device(np.asarray(state.tau, dtype=np.float64).ravel(), ctx)
+               if state.tau is not None else None)
+        return U, U0, tau
+
+    def sweep(self, state: SweeperState) -> SweeperState:
+        U, U0, tau = self._state_dev(state)
+        self.sweep_dev(U, U0, tau, 1)
+        self.check_errors()
+        return SweeperState(U.cpu().numpy().reshape(self.M, self.ndof), state.U0, state.tau)
+
+    def residual_norm(self, state: SweeperState) -> float:
+        U, U0, tau = self._state_dev(state)
+        out = N.empty(1)
+        self.residual_dev(U, U0, tau, 1, out)
+        return float(out.cpu().item())
+
+    def collocation_residual(self, state: SweeperState) -> np.ndarray:
+        """U - U0 - dt*Q F(U) - tau (pfasst.py:107-112); C(U) on device, U0/tau removed after."""
+        U, U0, tau = self._state_dev(state)
+        out = N.empty(self.M * self.ndof)
+        self.coll_op_dev(U, out, 1)
+        res = out.cpu().numpy().reshape(self.M, self.ndof) - np.asarray(state.U0)
+        return res - state.tau if state.tau is not None else res
+
+    # host helpers kept for API parity (inspection only; not on the solver path)
+    def f_diffusion(self, U):
+        return -(self.Kh @ np.asarray(U).T).T / self.mh
+
+    def f_reaction(self, U):
+        if self.gamma == 0.0:
+            return np.zeros_like(U)
+        return -self.gamma * reaction(np.asarray(U), self.reaction_kind)
+
+    def f_total(self, U):
+        return self.f_diffusion(U) + self.f_reaction(U)
+
+
+def sdc_sweep_implicit(state, tableau, dt, space, gamma=0.0) -> SweeperState:
+    return SdcLevel(tableau, space, dt, gamma, "implicit").sweep(state)
+
+
+def sdc_sweep_imex(state, tableau, dt, space, gamma=0.0) -> SweeperState:
+    return SdcLevel(tableau, space, dt, gamma, "imex").sweep(state)
+
+
+def sdc_solve_step(u0, level: SdcLevel, tol_rel: float = 1e-9, tol_abs: float = 1e-9,
+                   max_sweeps: int = 1000):
+    """Sweep one step until the collocation residual meets the tolerance (pfasst.py:223-249)."""
+    M, S = level.M, level.ndof
+    u0 = np.asarray(u0, dtype=np.float64)
+    ctx = N.context()
+    u0d = N.to_device(u0, ctx)
+    U = N.empty(M * S, ctx)
+    U0 = N.empty(S, ctx)
+    N.call("pd_spread", ctx.handle, _vp(u0d), _vp(U), _vp(U0), 1, M, S)
+    res_d = N.empty(1, ctx)
+    res = float(level.residual_dev(U, U0, None, 1, res_d).cpu().item())
+    report = SolveReport(residual_history=[res])
+    threshold = max(tol_abs, tol_rel * res)
+    lowest = res
+    while res > threshold:
+        if report.iterations >= max_sweeps:
+            report.diverged = True
+            break
+        level.sweep_dev(U, U0, None, 1)
+        res = float(level.residual_dev(U, U0, None, 1, res_d).cpu().item())
+        level.check_errors()
+        report.iterations += 1
+        report.residual_history.append(res)
+        if not np.isfinite(res) or res > 10.0 * lowest:
+            report.diverged = True
+            break
+        lowest = min(lowest, res)
+    report.converged = res <= threshold
+    return SweeperState(U.cpu().numpy().reshape(M, S), u0.copy()), report
+
+
+# ---------------------------------------------------------------- transfers
+class LevelTransfer:
+    """Space (CSR) and node (M_c x M_f / M_f x M_c) transfers (pfasst.py:253-270)."""
+
+    def __init__(self, space_restrict, space_prolong, node_restrict, node_prolong):
+        self.space_restrict = as_csr(space_restrict)
+        self.space_prolong = as_csr(space_prolong)
+        self.node_restrict = _host(node_restrict)
+        self.node_prolong = _host(node_prolong)
+        self._dev = None
+
+    def _devs(self):
+        if self._dev is None:
+            ctx = N.context()
+            self._dev = (DeviceCsr(self.space_restrict, ctx), DeviceCsr(self.space_prolong, ctx))
+        return self._dev
+
+    @property
+    def Sf(self):
+        return self.space_restrict.shape[1]
+
+    @property
+    def Sc(self):
+        return self.space_restrict.shape[0]
+
+    def restrict_dev(self, Uf, out, tmp, W: int, Mf: int, Mc: int):
+        """out[W][Mc][Sc] = Rn (Rs Uf) ; tmp holds W*Mf*Sc doubles."""
+        ctx = N.context()
+        Rs, _ = self._devs()
+        N.call("pd_csr_spmm", ctx.handle, Rs.handle, _vp(Uf), self.Sf, _vp(tmp), self.Sc,
+               W * Mf, 0)
+        N.call("pd_node_mix", ctx.handle, _vp(tmp), _vp(out), W, Mf, Mc, self.Sc,
+               self.node_restrict.ctypes.data_as(ctypes.c_void_p), 0)
+        return out
+
+    def prolong_add_dev(self, Vc, Uf, tmp, W: int, Mc: int, Mf: int):
+        """Uf[W][Mf][Sf] += Pn (Ps Vc) ; tmp holds W*Mc*Sf doubles."""
+        ctx = N.context()
+        _, Ps = self._devs()
+        N.call("pd_csr_spmm", ctx.handle, Ps.handle, _vp(Vc), self.Sc, _vp(tmp), self.Sf,
+               W * Mc, 0)
+        N.call("pd_node_mix", ctx.handle, _vp(tmp), _vp(Uf), W, Mc, Mf, self.Sf,
+               self.node_prolong.ctypes.data_as(ctypes.c_void_p), 1)
+        return Uf
+
+    def restrict_u0_dev(self, u0, out):
+        ctx = N.context()
+        Rs, _ = self._devs()
+        N.call("pd_csr_spmm", ctx.handle, Rs.handle, _vp(u0), self.Sf, _vp(out), self.Sc, 1, 0)
+        return out
+
+    # numpy API of the reference
+    def restrict_nodes(self, U):
+        U = np.asarray(U, dtype=np.float64)
+        Mf, Mc = U.shape[0], self.node_restrict.shape[0]
+        ctx = N.context()
+        Ud = N.to_device(U.ravel(), ctx)
+        out, tmp = N.empty(Mc * self.Sc, ctx), N.empty(Mf * self.Sc, ctx)
+        return self.restrict_dev(Ud, out, tmp, 1, Mf, Mc).cpu().numpy().reshape(Mc, self.Sc)
+
+    def prolong_nodes(self, U):
+        U = np.asarray(U, dtype=np.float64)
+        Mc, Mf = U.shape[0], self.node_prolong.shape[0]
+        ctx = N.context()
+        Ud = N.to_device(U.ravel(), ctx)
+        out, tmp = N.zeros(Mf * self.Sf, ctx), N.empty(Mc * self.Sf, ctx)
+        return self.prolong_add_dev(Ud, out, tmp, 1, Mc, Mf).cpu().numpy().reshape(Mf, self.Sf)
+
+    def restrict_u0(self, u0):
+        ctx = N.context()
+        out = N.empty(self.Sc, ctx)
+        return self.restrict_u0_dev(N.to_device(u0, ctx), out).cpu().numpy()
+
+
+def _node_eval_restriction(fine_nodes, coarse_nodes) -> np.ndarray:
+    """Fine nodal polynomial evaluated at the coarse nodes (pfasst.py:272-280)."""
+    return LagrangeBasis(fine_nodes).matrix(coarse_nodes)
+
+
+def fas_correction_dev(fine: SdcLevel, coarse: SdcLevel, tr: LevelTransfer, Uf, tau_f, W: int,
+                       tau_out, RU_out, scratch):
+    """tau = C_c(R U) - R C_f(U) (+ R tau_f) for W workers (pfasst.py:283-303)."""
+    ctx = N.context()
+    Mf, Mc, Sf, Sc = fine.M, coarse.M, fine.ndof, coarse.ndof
+    tmp_fc = scratch["tmp_fc"]    # W*Mf*Sc
+    cf = scratch["cf"]            # W*Mf*Sf
+    rcf = scratch["rcf"]          # W*Mc*Sc
+    tr.restrict_dev(Uf, RU_out, tmp_fc, W, Mf, Mc)
+    coarse.coll_op_dev(RU_out, tau_out, W)                 # C_c(RU)
+    fine.coll_op_dev(Uf, cf, W)                            # C_f(U)
+    tr.restrict_dev(cf, rcf, tmp_fc, W, Mf, Mc)            # R C_f(U)
+    n = W * Mc * Sc
+    N.call("pd_sub", ctx.handle, _vp(tau_out), _vp(tau_out), _vp(rcf), n)
+    if tau_f is not None:
+        tr.restrict_dev(tau_f, rcf, tmp_fc, W, Mf, Mc)
+        N.call("pd_axpy_to", ctx.handle, _vp(tau_out), _vp(tau_out), _vp(rcf), 1.0, n)
+    return tau_out
+
+
+def fas_correction(fine_level: SdcLevel, coarse_level: SdcLevel, transfer: LevelTransfer,
+                   fine_state: SweeperState) -> np.ndarray:
+    ctx = N.context()
+    Mf, Mc, Sf, Sc = fine_level.M, coarse_level.M, fine_level.ndof, coarse_level.ndof
+    Uf = N.to_device(np.asarray(fine_state.U).ravel(), ctx)
+    tau_f = (N.to_device(np.asarray(fine_state.tau).ravel(), ctx)
+             if fine_state.tau is not None else None)
+    scratch = {"tmp_fc": N.empty(Mf * Sc, ctx), "cf": N.empty(Mf * Sf, ctx),
+               "rcf": N.empty(Mc * Sc, ctx)}
+    tau, RU = N.empty(Mc * Sc, ctx), N.empty(Mc * Sc, ctx)
+    fas_correction_dev(fine_level, coarse_level, transfer, Uf, tau_f, 1, tau, RU, scratch)
+    return tau.cpu().numpy().reshape(Mc, Sc)
+
+
+class PfasstHierarchy:
+    def __init__(self, levels: list[SdcLevel], transfers: list[LevelTransfer], nu: int):
+        self.levels = levels
+        self.transfers = transfers
+        self.nu = nu
+
+    @property
+    def num_levels(self) -> int:
+        return len(self.levels)
+
+    @property
+    def fine(self) -> SdcLevel:
+        return self.levels[0]
+
+
+def build_pfasst_hierarchy(M: int, mesh: SpaceMesh, grid: TimeGrid, gamma: float, L: int,
+                           nu: int = 1, mode: str = "implicit", qdelta: str = "implicit-euler",
+                           space: SpaceOperators | None = None, M_coarse: int = 1,
+                           reaction_kind: str = "cubic") -> PfasstHierarchy:
+    """pfasst.py:323-365 (fine M; coarser levels M_coarse nodes, bisected meshes).
+
+    With ``space`` carrying an FD stencil (problems.fd_space) the levels are
+    rediscretised FD grids with full-weighting / bilinear transfers — the
+    BASELINE configs (coarse M=2 or 3).
+    """
+    if L < 1:
+        raise ConfigurationError("need at least one level")
+    spec = getattr(space, "stencil", None) if space is not None else None
+    tab_fine = make_tableau(M, qdelta)
+    tab_coarse = make_tableau(M_coarse, qdelta)
+    levels, transfers = [], []
+    if spec is None:
+        if mesh.Nx % 2 ** (L - 1) != 0:
+            raise ConfigurationError(f"Nx={mesh.Nx} not divisible by 2^{L - 1} for {L} levels")
+        for l in range(L):
+            sp_l = assemble_space(SpaceMesh(mesh.Nx // 2**l, mesh.X))
+            levels.append(SdcLevel(tab_fine if l == 0 else tab_coarse, sp_l, grid.dt, gamma, mode,
+                                   reaction_kind))
+        pairs = [(spatial_restriction(levels[l].ndof), spatial_prolongation(levels[l].ndof))
+                 for l in range(L - 1)]
+    else:
+        from .problems import fd_space, fd_transfers
+
+        specs = [spec]
+        for _ in range(L - 1):
+            specs.append(specs[-1].coarse())
+        for l, s in enumerate(specs):
+            levels.append(SdcLevel(tab_fine if l == 0 else tab_coarse, fd_space(s), grid.dt,
+                                   gamma, mode, reaction_kind))
+        pairs = [fd_transfers(specs[l]) for l in range(L - 1)]
+    for l in range(L - 1):
+        mf, mc = levels[l].M, levels[l + 1].M
+        if mf != mc:
+            nr = _node_eval_restriction(levels[l].tableau.nodes, levels[l + 1].tableau.nodes)
+            npr = _node_eval_restriction(levels[l + 1].tableau.nodes, levels[l].tableau.nodes)
+        else:
+            nr = npr = np.eye(mf)
+        transfers.append(LevelTransfer(pairs[l][0], pairs[l][1], nr, npr))
+    return PfasstHierarchy(levels, transfers, nu)
+
+
+# ---------------------------------------------------------------- the windowed driver
+class _WindowBuffers:
+    """Device state of one window: per level U, U0, tau, messages and scratch."""
+
+    def __init__(self, hier: PfasstHierarchy, P: int, ctx):
+        self.P = P
+        L = hier.num_levels
+        lv = hier.levels
+        self.U = [N.empty(P * l.M * l.ndof, ctx) for l in lv]
+        self.U0 = [N.empty(P * l.ndof, ctx) for l in lv]
+        self.tau = [None] + [N.empty(P * l.M * l.ndof, ctx) for l in lv[1:]]
+        self.chain = [N.empty(l.ndof, ctx) for l in lv]
+        nrecv = max(L - 1, 1)
+        self.msgs = [N.empty(P * lv[l].ndof, ctx) for l in range(nrecv)]
+        self.res = N.empty(P, ctx)
+        self.scratch = []
+        for l in range(L - 1):
+            f, c = lv[l], lv[l + 1]
+            self.scratch.append({
+                "tmp_fc": N.empty(P * f.M * c.ndof, ctx), "cf": N.empty(P * f.M * f.ndof, ctx),
+                "rcf": N.empty(P * c.M * c.ndof, ctx), "RU": N.empty(P * c.M * c.ndof, ctx),
+                "diff": N.empty(P * c.M * c.ndof, ctx),
+                "tmp_cf": N.empty(P * c.M * f.ndof, ctx)})
+
+
+def pfasst_run(hierarchy: PfasstHierarchy, u_init, Nt: int, workers: int, tol_rel: float = 1e-9,
+               tol_abs: float = 1e-9, max_iters: int = 1000):
+    """Pipelined PFASST over all steps in windows of ``workers`` (pfasst.py:509-587)."""
+    if workers < 1 or workers > Nt:
+        raise ConfigurationError(f"worker count must be in [1, Nt={Nt}], got {workers}")
+    if Nt % workers != 0:
+        raise ConfigurationError(f"worker count {workers} must divide Nt={Nt}")
+    fine = hierarchy.fine
+    S, M = fine.ndof, fine.M
+    u_init = np.asarray(u_init, dtype=np.float64)
+    if u_init.size != S:
+        raise ConfigurationError("initial state does not match the fine mesh")
+    ctx = N.context()
+    out, report = pfasst_run_dev(hierarchy, N.to_device(u_init, ctx), Nt, workers, tol_rel,
+                                 tol_abs, max_iters)
+    return out.cpu().numpy(), report
+
+
+def pfasst_run_dev(hierarchy: PfasstHierarchy, u_init_dev, Nt: int, P: int, tol_rel=1e-9,
+                   tol_abs=1e-9, max_iters=1000, on_window=None):
+    """Device-resident driver: returns (flat CUDA tensor (Nt, M, S), SolveReport)."""
+    ctx = N.context()
+    lv = hierarchy.levels
+    trs = hierarchy.transfers
+    L = len(lv)
+    nu = hierarchy.nu
+    fine = lv[0]
+    S, M = fine.ndof, fine.M
+    for l in lv:
+        l.device(P)
+    buf = _WindowBuffers(hierarchy, P, ctx)
+    out = N.empty(Nt * M * S, ctx)
+    report = SolveReport()
+    t0 = time.perf_counter()
+    u_start = u_init_dev.clone()
+    converged = True
+    nrecv = max(L - 1, 1)
+    for start in range(0, Nt, P):
+        # setup: restrict the start value down the chain, spread every level
+        N.call("pd_terminal", ctx.handle, _vp(u_start), _vp(buf.chain[0]), 1, 1, S)
+        for l in range(L - 1):
+            trs[l].restrict_u0_dev(buf.chain[l], buf.chain[l + 1])
+        for l, lev in enumerate(lv):
+            N.call("pd_spread", ctx.handle, _vp(buf.chain[l]), _vp(buf.U[l]), _vp(buf.U0[l]), P,
+                   lev.M, lev.ndof)
+        fine.residual_dev(buf.U[0], buf.U0[0], None, P, buf.res)
+        res = buf.res.cpu().numpy()
+        threshold = max(tol_abs, tol_rel * float(res[0]))
+        lowest = np.maximum(res, 1e-300)
+        iters = 0
+        diverged = False
+        if not np.all(res <= threshold):
+            for k in range(1, max_iters + 1):
+                try:
+                    if k > 1 and P > 1:  # lagged fine messages from iteration k-1
+                        for l in range(nrecv):
+                            n_l = lv[l].ndof
+                            N.call("pd_scale", ctx.handle, _vp(buf.U0[l], n_l), _vp(buf.msgs[l]),
+                                   1.0, (P - 1) * n_l)
+                    for _ in range(nu):
+                        fine.sweep_dev(buf.U[0], buf.U0[0], None, P)
+                    if L > 1:
+                        _coarse_phase(hierarchy, buf, P)
+                    for l in range(nrecv):  # publish terminals
+                        N.call("pd_terminal", ctx.handle, _vp(buf.U[l]), _vp(buf.msgs[l]), P,
+                               lv[l].M, lv[l].ndof)
+                    fine.residual_dev(buf.U[0], buf.U0[0], None, P, buf.res)
+                    res = buf.res.cpu().numpy()
+                    for lev in lv:
+                        lev.check_errors()
+                except SolverError:
+                    diverged = True
+                    break
+                iters = k
+                bad = ~np.isfinite(res) | (res > 10.0 * lowest)
+                lowest = np.minimum(lowest, np.maximum(res, 1e-300))
+                if bad.any():
+                    diverged = True
+                    break
+                if np.all(res <= threshold):
+                    break
+            else:
+                diverged = True
+        report.inner_iterations.append(int(iters))
+        report.residual_history.append(float(np.max(res)))
+        N.call("pd_scale", ctx.handle, _vp(out, start * M * S), _vp(buf.U[0]), 1.0, P * M * S)
+        if on_window is not None:
+            on_window(start, buf)
+        if diverged:
+            converged = False
+            report.diverged = True
+            break
+        N.call("pd_terminal", ctx.handle, _vp(buf.U[0], (P - 1) * M * S), _vp(u_start), 1, M, S)
+    report.converged = converged and not report.diverged
+    report.iterations = max(report.inner_iterations) if report.inner_iterations else 0
+    report.wall_time = time.perf_counter() - t0
+    return out, report
+
+
+def _coarse_phase(hier: PfasstHierarchy, buf: _WindowBuffers, P: int):
+    """FAS down, serial coarsest chain, interpolation up (pfasst.py:425-463)."""
+    ctx = N.context()
+    lv, trs, nu = hier.levels, hier.transfers, hier.nu
+    L = len(lv)
+    for l in range(1, L):
+        sc = buf.scratch[l - 1]
+        # U_l = R U_{l-1}; tau_l = FAS   (RU lands in U_l directly)
+        fas_correction_dev(lv[l - 1], lv[l], trs[l - 1], buf.U[l - 1], buf.tau[l - 1], P,
+                           buf.tau[l], buf.U[l], sc)
+        if l < L - 1:
+            for _ in range(nu):
+                lv[l].sweep_dev(buf.U[l], buf.U0[l], buf.tau[l], P)
+    c = lv[L - 1]
+    Mc, Sc = c.M, c.ndof
+    for w in range(P):  # serial forward chain within the iteration
+        if w == 0:
+            N.call("pd_scale", ctx.handle, _vp(buf.U0[L - 1]), _vp(buf.chain[L - 1]), 1.0, Sc)
+        else:
+            N.call("pd_terminal", ctx.handle, _vp(buf.U[L - 1], (w - 1) * Mc * Sc),
+                   _vp(buf.U0[L - 1], w * Sc), 1, Mc, Sc)
+        for _ in range(nu):
+            c.sweep_dev(buf.U[L - 1], buf.U0[L - 1], buf.tau[L - 1], 1, w_off=w)
+    for l in range(L - 2, -1, -1):
+        sc = buf.scratch[l]
+        f, cl = lv[l], lv[l + 1]
+        # U_l += P (U_{l+1} - R U_l)
+        trs[l].restrict_dev(buf.U[l], sc["RU"], sc["tmp_fc"], P, f.M, cl.M)
+        n = P * cl.M * cl.ndof
+        N.call("pd_sub", ctx.handle, _vp(sc["diff"]), _vp(buf.U[l + 1]), _vp(sc["RU"]), n)
+        trs[l].prolong_add_dev(sc["diff"], buf.U[l], sc["tmp_cf"], P, cl.M, f.M)
+        if 0 < l < L - 1:
+            for _ in range(nu):
+                lv[l].sweep_dev(buf.U[l], buf.U0[l], buf.tau[l], P)

@@ -1,0 +1,107 @@
+"""GPU parity of the SDC/PFASST path vs golden fixtures from the real reference.
+
+Bar (BASELINE north_star): equal PFASST iteration counts (max over windows and
+per window) and per-time-node relative L2 <= 1e-10 (pd_util.per_node_rel).
+The device node solves are exact factorizations applied as refinement; the
+reference's GMRES(ILU) reaches 1e-13, so single-sweep results agree to ~1e-13.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2006_12883_b200 as pd
+from paper_2006_12883_b200 import pfasst as PF
+from pd_util import per_node_rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+def _heat_u0(Nx):
+    return pd.heat_problem().u0(pd.SpaceMesh(Nx, 1.0).vertices)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_c1_pfasst_matches_reference(golden, P):
+    g = golden("c1")
+    cfg = pd.baseline_config("C1")
+    ops = pd.fd_space(cfg.spec)
+    hier = PF.build_pfasst_hierarchy(cfg.M, ops.mesh, pd.TimeGrid(cfg.Nt, cfg.T), 0.0, L=2,
+                                     nu=1, space=ops, M_coarse=cfg.M_coarse)
+    x, rep = PF.pfasst_run(hier, cfg.u0(), cfg.Nt, P, tol_rel=1e-10, tol_abs=1e-10)
+    assert rep.converged
+    assert rep.inner_iterations == g[f"PF_P{P}_inner"].tolist()
+    assert rep.iterations == int(g[f"PF_P{P}_its"])
+    assert per_node_rel(x, g[f"PF_P{P}_x"], (16, 3, 127)) < 1e-10
+
+
+def test_pfasst_fem1d_heat_matches_reference(golden):
+    g = golden("pfasst_fem1d")
+    mesh = pd.SpaceMesh(32, 1.0)
+    for P in (1, 2, 4):
+        hier = PF.build_pfasst_hierarchy(3, mesh, pd.TimeGrid(8, 1.0), 0.0, L=2, nu=1)
+        x, rep = PF.pfasst_run(hier, _heat_u0(32), 8, P, tol_rel=1e-10, tol_abs=1e-10)
+        assert rep.inner_iterations == g[f"heat_P{P}_inner"].tolist(), P
+        assert per_node_rel(x, g[f"heat_P{P}_x"], (8, 3, 33)) < 1e-10
+    hier = PF.build_pfasst_hierarchy(2, mesh, pd.TimeGrid(8, 1.0), 0.0, L=3, nu=1)
+    x, rep = PF.pfasst_run(hier, _heat_u0(32), 8, 4, tol_rel=1e-10, tol_abs=1e-10)
+    assert rep.inner_iterations == g["heatL3_P4_inner"].tolist()
+    assert per_node_rel(x, g["heatL3_P4_x"], (8, 2, 33)) < 1e-10
+
+
+def test_pfasst_monodomain_imex_matches_reference(golden):
+    g = golden("pfasst_fem1d")
+    prob = pd.monodomain_problem()
+    mesh = pd.SpaceMesh(64, prob.X)
+    hier = PF.build_pfasst_hierarchy(2, mesh, pd.TimeGrid(16, prob.T), prob.gamma, L=2, nu=1,
+                                     mode="imex")
+    x, rep = PF.pfasst_run(hier, prob.u0(mesh.vertices), 16, 4, tol_rel=1e-9, tol_abs=1e-9)
+    assert rep.inner_iterations == g["mono_imex_inner"].tolist()
+    assert per_node_rel(x, g["mono_imex_x"], (16, 2, 65)) < 1e-9
+
+
+def test_sweep_fas_residual_match_reference(golden):
+    g = golden("pfasst_fem1d")
+    hier = PF.build_pfasst_hierarchy(3, pd.SpaceMesh(32, 1.0), pd.TimeGrid(8, 1.0), 0.0, L=2,
+                                     nu=1)
+    u0 = _heat_u0(32)
+    st = PF.SweeperState(g["sweep_U_in"].copy(), u0.copy())
+    np.testing.assert_allclose(hier.fine.sweep(st).U, g["sweep_U_out"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(
+        PF.fas_correction(hier.levels[0], hier.levels[1], hier.transfers[0], st), g["fas_tau"],
+        rtol=0, atol=1e-12)
+    assert abs(hier.fine.residual_norm(st) - float(g["resnorm"])) < 1e-12
+    prob = pd.monodomain_problem()
+    mesh = pd.SpaceMesh(64, prob.X)
+    lv = PF.SdcLevel(pd.make_tableau(3), pd.assemble_space(mesh), 0.05, prob.gamma, "imex")
+    u0m = prob.u0(mesh.vertices)
+    np.testing.assert_allclose(lv.sweep(PF.spread_state(u0m, 3)).U, g["imex_sweep"], atol=1e-12)
+    s, rp = PF.sdc_solve_step(u0m, lv, tol_rel=1e-10, tol_abs=1e-10)
+    assert rp.iterations == int(g["sdc_step_its"])
+    np.testing.assert_allclose(s.U, g["sdc_step_U"], atol=1e-10)
+
+
+def test_c2_small_pfasst_dense_node_solves(golden):
+    g = golden("c2_small")
+    spec = pd.StencilSpec(2, 15, "dirichlet", 1.0)
+    ops = pd.fd_space(spec)
+    hier = PF.build_pfasst_hierarchy(3, ops.mesh, pd.TimeGrid(8, 8 / 64), 0.0, L=2, nu=1,
+                                     space=ops, M_coarse=2)
+    x, rep = PF.pfasst_run(hier, g["u0"], 8, 4, tol_rel=1e-9, tol_abs=1e-9)
+    assert rep.inner_iterations == g["PF_P4_inner"].tolist()
+    assert per_node_rel(x, g["PF_P4_x"], (8, 3, 225)) < 1e-10
+
+
+def test_worker_count_validation():
+    mesh = pd.SpaceMesh(16, 1.0)
+    hier = PF.build_pfasst_hierarchy(2, mesh, pd.TimeGrid(6, 1.0), 0.0, L=1, nu=1)
+    with pytest.raises(pd.ConfigurationError):
+        PF.pfasst_run(hier, np.zeros(17), 6, 4)
+
+
+def test_divergent_window_reports_nc():
+    prob = pd.monodomain_problem()
+    mesh = pd.SpaceMesh(128, prob.X)
+    hier = PF.build_pfasst_hierarchy(4, mesh, pd.TimeGrid(4, prob.T), prob.gamma, L=2, nu=1,
+                                     mode="imex")
+    u, rep = PF.pfasst_run(hier, prob.u0(mesh.vertices), 4, 4, max_iters=150)
+    assert not rep.converged and rep.diverged
