@@ -137,7 +137,8 @@ class SdcLevel:
     def sweep_dev(self, U, U0, tau, W: int, w_off: int = 0):
         """In-place sweep of workers [w_off, w_off+W) of the device arrays."""
         M, S = self.M, self.ndof
-        N.call("pd_sdc_sweep", self.device(W + w_off), _vp(U, w_off * M * S), _vp(U0, w_off * S),
+        dev = self._dev if (self._dev is not None and self._cap >= W) else self.device(W)
+        N.call("pd_sdc_sweep", dev, _vp(U, w_off * M * S), _vp(U0, w_off * S),
                _vp(tau, w_off * M * S) if tau is not None else ctypes.c_void_p(), W)
 
     def residual_dev(self, U, U0, tau, W: int, out):
@@ -406,28 +407,208 @@ def build_pfasst_hierarchy(M: int, mesh: SpaceMesh, grid: TimeGrid, gamma: float
 
 
 # ---------------------------------------------------------------- the windowed driver
-class _WindowBuffers:
-    """Device state of one window: per level U, U0, tau, messages and scratch."""
+class GpuPfasstEngine:
+    """Device state of this rank's workers of a window + the PFASST steps on them.
 
-    def __init__(self, hier: PfasstHierarchy, P: int, ctx):
+    Implements the engine interface of timeslab.run_windows; all arithmetic is
+    native (csrc/pd_sdc.cu), the host only sequences launches.
+    """
+
+    def __init__(self, hier: PfasstHierarchy, u_init_dev, Nt: int, P: int, rank: int = 0,
+                 size: int = 1, out=None):
+        from .timeslab import worker_range
+
+        self.ctx = ctx = N.context()
+        self.h = hier
         self.P = P
-        L = hier.num_levels
+        self.w0, self.w1 = worker_range(P, rank, size)
+        self.W = W = self.w1 - self.w0
+        self.rank, self.size = rank, size
         lv = hier.levels
-        self.U = [N.empty(P * l.M * l.ndof, ctx) for l in lv]
-        self.U0 = [N.empty(P * l.ndof, ctx) for l in lv]
-        self.tau = [None] + [N.empty(P * l.M * l.ndof, ctx) for l in lv[1:]]
+        self.L = L = len(lv)
+        for l in lv:
+            l.device(W)
+        self.U = [N.empty(W * l.M * l.ndof, ctx) for l in lv]
+        self.U0 = [N.empty(W * l.ndof, ctx) for l in lv]
+        self.tau = [None] + [N.empty(W * l.M * l.ndof, ctx) for l in lv[1:]]
         self.chain = [N.empty(l.ndof, ctx) for l in lv]
-        nrecv = max(L - 1, 1)
-        self.msgs = [N.empty(P * lv[l].ndof, ctx) for l in range(nrecv)]
-        self.res = N.empty(P, ctx)
+        self.nrecv = max(L - 1, 1)
+        self.msgs = [N.empty(W * lv[l].ndof, ctx) for l in range(self.nrecv)]
+        self.halo_in = [N.empty(lv[l].ndof, ctx) for l in range(self.nrecv)]
+        self.halo_out = [N.empty(lv[l].ndof, ctx) for l in range(self.nrecv)]
+        self.c_in = N.empty(lv[-1].ndof, ctx)
+        self.c_out = N.empty(lv[-1].ndof, ctx)
+        self.res = N.empty(W, ctx)
+        self.u_start = u_init_dev.clone()
+        self.fine_term = N.empty(lv[0].ndof, ctx)
         self.scratch = []
         for l in range(L - 1):
             f, c = lv[l], lv[l + 1]
             self.scratch.append({
-                "tmp_fc": N.empty(P * f.M * c.ndof, ctx), "cf": N.empty(P * f.M * f.ndof, ctx),
-                "rcf": N.empty(P * c.M * c.ndof, ctx), "RU": N.empty(P * c.M * c.ndof, ctx),
-                "diff": N.empty(P * c.M * c.ndof, ctx),
-                "tmp_cf": N.empty(P * c.M * f.ndof, ctx)})
+                "tmp_fc": N.empty(W * f.M * c.ndof, ctx), "cf": N.empty(W * f.M * f.ndof, ctx),
+                "rcf": N.empty(W * c.M * c.ndof, ctx), "RU": N.empty(W * c.M * c.ndof, ctx),
+                "diff": N.empty(W * c.M * c.ndof, ctx),
+                "tmp_cf": N.empty(W * c.M * f.ndof, ctx)})
+        S, M = lv[0].ndof, lv[0].M
+        self.out = out if out is not None else N.empty(Nt * M * S, ctx)
+        self._r0 = 0.0
+
+    num_levels = property(lambda self: self.L)
+    local_workers = property(lambda self: self.W)
+
+    def _c(self, name, *args):
+        N.call(name, self.ctx.handle, *args)
+
+    def setup_window(self, start):
+        lv, trs = self.h.levels, self.h.transfers
+        self._c("pd_scale", _vp(self.chain[0]), _vp(self.u_start), 1.0, lv[0].ndof)
+        for l in range(self.L - 1):
+            trs[l].restrict_u0_dev(self.chain[l], self.chain[l + 1])
+        for l, lev in enumerate(lv):
+            self._c("pd_spread", _vp(self.chain[l]), _vp(self.U[l]), _vp(self.U0[l]), self.W,
+                    lev.M, lev.ndof)
+        lv[0].residual_dev(self.U[0], self.U0[0], None, self.W, self.res)
+        r = self.res.cpu().numpy()
+        self._r0 = float(r[0])  # every worker starts from the same spread state
+        return r
+
+    def window_r0(self):
+        return self._r0
+
+    def halo_buffers(self):
+        return self.halo_in
+
+    def halo_out_buffers(self):
+        return self.halo_out
+
+    def receive(self, halo):
+        """U0 of levels < L-1 from the predecessor's previous-iteration terminal."""
+        lv = self.h.levels
+        for l in range(self.nrecv):
+            n = lv[l].ndof
+            if self.W > 1:
+                self._c("pd_scale", _vp(self.U0[l], n), _vp(self.msgs[l]), 1.0, (self.W - 1) * n)
+            if halo is not None:
+                self._c("pd_scale", _vp(self.U0[l]), _vp(halo[l]), 1.0, n)
+
+    def fine_sweeps(self):
+        for _ in range(self.h.nu):
+            self.h.fine.sweep_dev(self.U[0], self.U0[0], None, self.W)
+
+    def coarse_down(self):
+        lv, trs, nu = self.h.levels, self.h.transfers, self.h.nu
+        for l in range(1, self.L):
+            fas_correction_dev(lv[l - 1], lv[l], trs[l - 1], self.U[l - 1], self.tau[l - 1],
+                               self.W, self.tau[l], self.U[l], self.scratch[l - 1])
+            if l < self.L - 1:
+                for _ in range(nu):
+                    lv[l].sweep_dev(self.U[l], self.U0[l], self.tau[l], self.W)
+
+    def coarse_start_buffer(self):
+        return self.c_in
+
+    def load_coarse_start(self, buf):
+        self._c("pd_scale", _vp(buf), _vp(self.chain[-1]), 1.0, self.h.levels[-1].ndof)
+
+    def coarse_chain(self, u0c):
+        c = self.h.levels[-1]
+        Mc, Sc = c.M, c.ndof
+        U, U0, tau = self.U[-1], self.U0[-1], self.tau[-1]
+        for w in range(self.W):
+            if w == 0:
+                self._c("pd_scale", _vp(U0), _vp(u0c), 1.0, Sc)
+            else:
+                self._c("pd_terminal", _vp(U, (w - 1) * Mc * Sc), _vp(U0, w * Sc), 1, Mc, Sc)
+            for _ in range(self.h.nu):
+                c.sweep_dev(U, U0, tau, 1, w_off=w)
+        self._c("pd_terminal", _vp(U, (self.W - 1) * Mc * Sc), _vp(self.c_out), 1, Mc, Sc)
+        return self.c_out
+
+    def coarse_last_buffer(self):
+        return self.c_out
+
+    def coarse_up(self):
+        lv, trs, nu = self.h.levels, self.h.transfers, self.h.nu
+        for l in range(self.L - 2, -1, -1):
+            sc = self.scratch[l]
+            f, cl = lv[l], lv[l + 1]
+            trs[l].restrict_dev(self.U[l], sc["RU"], sc["tmp_fc"], self.W, f.M, cl.M)
+            self._c("pd_sub", _vp(sc["diff"]), _vp(self.U[l + 1]), _vp(sc["RU"]),
+                    self.W * cl.M * cl.ndof)
+            trs[l].prolong_add_dev(sc["diff"], self.U[l], sc["tmp_cf"], self.W, cl.M, f.M)
+            if 0 < l < self.L - 1:
+                for _ in range(nu):
+                    lv[l].sweep_dev(self.U[l], self.U0[l], self.tau[l], self.W)
+
+    def publish(self):
+        lv = self.h.levels
+        for l in range(self.nrecv):
+            M, S = lv[l].M, lv[l].ndof
+            self._c("pd_terminal", _vp(self.U[l]), _vp(self.msgs[l]), self.W, M, S)
+            self._c("pd_scale", _vp(self.halo_out[l]), _vp(self.msgs[l], (self.W - 1) * S), 1.0, S)
+        lv[0].residual_dev(self.U[0], self.U0[0], None, self.W, self.res)
+        r = self.res.cpu().numpy()
+        for lev in lv:
+            lev.check_errors()
+        return r
+
+    def store_window(self, start):
+        M, S = self.h.fine.M, self.h.fine.ndof
+        self._c("pd_scale", _vp(self.out, (start + self.w0) * M * S), _vp(self.U[0]), 1.0,
+                self.W * M * S)
+
+    def last_fine_terminal(self):
+        M, S = self.h.fine.M, self.h.fine.ndof
+        self._c("pd_terminal", _vp(self.U[0], (self.W - 1) * M * S), _vp(self.fine_term), 1, M, S)
+        return self.fine_term
+
+    def set_window_start(self, t):
+        self._c("pd_scale", _vp(self.u_start), _vp(t), 1.0, self.h.fine.ndof)
+
+
+def pfasst_run_dev(hierarchy: PfasstHierarchy, u_init_dev, Nt: int, P: int, tol_rel=1e-9,
+                   tol_abs=1e-9, max_iters=1000, comm=None):
+    """Device-resident driver: returns (flat CUDA tensor (Nt, M, S), SolveReport).
+
+    With ``comm`` (timeslab.TorchComm over NCCL) the window's workers are
+    sharded over the ranks; each rank's tensor then holds its own steps only.
+    """
+    from .timeslab import LocalComm, run_windows
+
+    comm = comm or LocalComm()
+    eng = GpuPfasstEngine(hierarchy, u_init_dev, Nt, P, comm.rank, comm.size)
+    report = run_windows(eng, comm, Nt, P, tol_rel, tol_abs, max_iters)
+    return eng.out, report
+
+
+def pfasst_run_distributed(hierarchy: PfasstHierarchy, u_init, Nt: int, workers: int,
+                           tol_rel: float = 1e-9, tol_abs: float = 1e-9, max_iters: int = 1000,
+                           group=None, gather: bool = True):
+    """pfasst_run with each window's workers sharded over the ranks of ``group``.
+
+    One process per GPU (torch.distributed, NCCL).  Returns the full flat
+    solution on every rank when ``gather`` (an all_gather of the slabs).
+    """
+    import torch
+    import torch.distributed as dist
+
+    from .timeslab import TorchComm
+
+    comm = TorchComm(group)
+    ctx = N.context()
+    out, report = pfasst_run_dev(hierarchy, N.to_device(u_init, ctx), Nt, workers, tol_rel,
+                                 tol_abs, max_iters, comm)
+    if not gather:
+        return out, report
+    M, S = hierarchy.fine.M, hierarchy.fine.ndof
+    W = workers // comm.size
+    parts = [torch.empty_like(out) for _ in range(comm.size)]
+    dist.all_gather(parts, out, group=group)
+    full = out.clone().view(Nt // workers, workers, M * S)
+    for r, part in enumerate(parts):
+        pv = part.view(Nt // workers, workers, M * S)
+        full[:, r * W:(r + 1) * W] = pv[:, r * W:(r + 1) * W]
+    return full.reshape(-1).cpu().numpy(), report
 
 
 def pfasst_run(hierarchy: PfasstHierarchy, u_init, Nt: int, workers: int, tol_rel: float = 1e-9,
@@ -437,8 +618,7 @@ def pfasst_run(hierarchy: PfasstHierarchy, u_init, Nt: int, workers: int, tol_re
         raise ConfigurationError(f"worker count must be in [1, Nt={Nt}], got {workers}")
     if Nt % workers != 0:
         raise ConfigurationError(f"worker count {workers} must divide Nt={Nt}")
-    fine = hierarchy.fine
-    S, M = fine.ndof, fine.M
+    S = hierarchy.fine.ndof
     u_init = np.asarray(u_init, dtype=np.float64)
     if u_init.size != S:
         raise ConfigurationError("initial state does not match the fine mesh")
@@ -446,120 +626,3 @@ def pfasst_run(hierarchy: PfasstHierarchy, u_init, Nt: int, workers: int, tol_re
     out, report = pfasst_run_dev(hierarchy, N.to_device(u_init, ctx), Nt, workers, tol_rel,
                                  tol_abs, max_iters)
     return out.cpu().numpy(), report
-
-
-def pfasst_run_dev(hierarchy: PfasstHierarchy, u_init_dev, Nt: int, P: int, tol_rel=1e-9,
-                   tol_abs=1e-9, max_iters=1000, on_window=None):
-    """Device-resident driver: returns (flat CUDA tensor (Nt, M, S), SolveReport)."""
-    ctx = N.context()
-    lv = hierarchy.levels
-    trs = hierarchy.transfers
-    L = len(lv)
-    nu = hierarchy.nu
-    fine = lv[0]
-    S, M = fine.ndof, fine.M
-    for l in lv:
-        l.device(P)
-    buf = _WindowBuffers(hierarchy, P, ctx)
-    out = N.empty(Nt * M * S, ctx)
-    report = SolveReport()
-    t0 = time.perf_counter()
-    u_start = u_init_dev.clone()
-    converged = True
-    nrecv = max(L - 1, 1)
-    for start in range(0, Nt, P):
-        # setup: restrict the start value down the chain, spread every level
-        N.call("pd_terminal", ctx.handle, _vp(u_start), _vp(buf.chain[0]), 1, 1, S)
-        for l in range(L - 1):
-            trs[l].restrict_u0_dev(buf.chain[l], buf.chain[l + 1])
-        for l, lev in enumerate(lv):
-            N.call("pd_spread", ctx.handle, _vp(buf.chain[l]), _vp(buf.U[l]), _vp(buf.U0[l]), P,
-                   lev.M, lev.ndof)
-        fine.residual_dev(buf.U[0], buf.U0[0], None, P, buf.res)
-        res = buf.res.cpu().numpy()
-        threshold = max(tol_abs, tol_rel * float(res[0]))
-        lowest = np.maximum(res, 1e-300)
-        iters = 0
-        diverged = False
-        if not np.all(res <= threshold):
-            for k in range(1, max_iters + 1):
-                try:
-                    if k > 1 and P > 1:  # lagged fine messages from iteration k-1
-                        for l in range(nrecv):
-                            n_l = lv[l].ndof
-                            N.call("pd_scale", ctx.handle, _vp(buf.U0[l], n_l), _vp(buf.msgs[l]),
-                                   1.0, (P - 1) * n_l)
-                    for _ in range(nu):
-                        fine.sweep_dev(buf.U[0], buf.U0[0], None, P)
-                    if L > 1:
-                        _coarse_phase(hierarchy, buf, P)
-                    for l in range(nrecv):  # publish terminals
-                        N.call("pd_terminal", ctx.handle, _vp(buf.U[l]), _vp(buf.msgs[l]), P,
-                               lv[l].M, lv[l].ndof)
-                    fine.residual_dev(buf.U[0], buf.U0[0], None, P, buf.res)
-                    res = buf.res.cpu().numpy()
-                    for lev in lv:
-                        lev.check_errors()
-                except SolverError:
-                    diverged = True
-                    break
-                iters = k
-                bad = ~np.isfinite(res) | (res > 10.0 * lowest)
-                lowest = np.minimum(lowest, np.maximum(res, 1e-300))
-                if bad.any():
-                    diverged = True
-                    break
-                if np.all(res <= threshold):
-                    break
-            else:
-                diverged = True
-        report.inner_iterations.append(int(iters))
-        report.residual_history.append(float(np.max(res)))
-        N.call("pd_scale", ctx.handle, _vp(out, start * M * S), _vp(buf.U[0]), 1.0, P * M * S)
-        if on_window is not None:
-            on_window(start, buf)
-        if diverged:
-            converged = False
-            report.diverged = True
-            break
-        N.call("pd_terminal", ctx.handle, _vp(buf.U[0], (P - 1) * M * S), _vp(u_start), 1, M, S)
-    report.converged = converged and not report.diverged
-    report.iterations = max(report.inner_iterations) if report.inner_iterations else 0
-    report.wall_time = time.perf_counter() - t0
-    return out, report
-
-
-def _coarse_phase(hier: PfasstHierarchy, buf: _WindowBuffers, P: int):
-    """FAS down, serial coarsest chain, interpolation up (pfasst.py:425-463)."""
-    ctx = N.context()
-    lv, trs, nu = hier.levels, hier.transfers, hier.nu
-    L = len(lv)
-    for l in range(1, L):
-        sc = buf.scratch[l - 1]
-        # U_l = R U_{l-1}; tau_l = FAS   (RU lands in U_l directly)
-        fas_correction_dev(lv[l - 1], lv[l], trs[l - 1], buf.U[l - 1], buf.tau[l - 1], P,
-                           buf.tau[l], buf.U[l], sc)
-        if l < L - 1:
-            for _ in range(nu):
-                lv[l].sweep_dev(buf.U[l], buf.U0[l], buf.tau[l], P)
-    c = lv[L - 1]
-    Mc, Sc = c.M, c.ndof
-    for w in range(P):  # serial forward chain within the iteration
-        if w == 0:
-            N.call("pd_scale", ctx.handle, _vp(buf.U0[L - 1]), _vp(buf.chain[L - 1]), 1.0, Sc)
-        else:
-            N.call("pd_terminal", ctx.handle, _vp(buf.U[L - 1], (w - 1) * Mc * Sc),
-                   _vp(buf.U0[L - 1], w * Sc), 1, Mc, Sc)
-        for _ in range(nu):
-            c.sweep_dev(buf.U[L - 1], buf.U0[L - 1], buf.tau[L - 1], 1, w_off=w)
-    for l in range(L - 2, -1, -1):
-        sc = buf.scratch[l]
-        f, cl = lv[l], lv[l + 1]
-        # U_l += P (U_{l+1} - R U_l)
-        trs[l].restrict_dev(buf.U[l], sc["RU"], sc["tmp_fc"], P, f.M, cl.M)
-        n = P * cl.M * cl.ndof
-        N.call("pd_sub", ctx.handle, _vp(sc["diff"]), _vp(buf.U[l + 1]), _vp(sc["RU"]), n)
-        trs[l].prolong_add_dev(sc["diff"], buf.U[l], sc["tmp_cf"], P, cl.M, f.M)
-        if 0 < l < L - 1:
-            for _ in range(nu):
-                lv[l].sweep_dev(buf.U[l], buf.U0[l], buf.tau[l], P)
