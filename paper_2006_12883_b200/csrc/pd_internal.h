@@ -157,5 +157,7 @@ void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard = 
 // dense LU
 std::unique_ptr<DenseLU> dense_lu_from_csr(Ctx& c, const Csr& A);
 void dense_lu_solve(Ctx& c, const DenseLU& f, const double* b, double* x);
+DevBuf<double> dense_inverse(Ctx& c, const DenseLU& f);  // row-major inverse (synchronising)
+void dense_inverse_apply(Ctx& c, const double* inv, int64_t n, const double* b, double* x);
 
 }  // namespace pd

@@ -22,6 +22,7 @@ namespace pd {
 using namespace dev;
 
 constexpr int KB = 256;
+constexpr int64_t kCoarseInverseMax = 8192;  // 512 MB of inverse at most
 
 __device__ __forceinline__ int vphase(const GmDev* s) { return *((volatile const int*)&s->phase); }
 
@@ -378,6 +379,8 @@ void Multigrid::refactor() {
         }
     }
     coarse = dense_lu_from_csr(c, *lv[L - 1].A);
+    coarse_inv.release();
+    if (lv[L - 1].n <= kCoarseInverseMax) coarse_inv = dense_inverse(c, *coarse);
 }
 
 void Multigrid::cycle(int l) {
@@ -386,7 +389,8 @@ void Multigrid::cycle(int l) {
     double* b = m.b.p;
     double* x = m.x.p;
     if (l == L - 1) {
-        dense_lu_solve(c, *coarse, b, x);
+        if (coarse_inv.p) dense_inverse_apply(c, coarse_inv.p, m.n, b, x);
+        else dense_lu_solve(c, *coarse, b, x);
         return;
     }
     for (int s = 0; s < smooth_solves; ++s) enqueue_gmres_smooth(c, *m.gm, *m.A, b, x, m.r.p, nu);

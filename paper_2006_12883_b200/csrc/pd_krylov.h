@@ -88,6 +88,7 @@ class Multigrid {
     Ctx& c;
     std::vector<MgLevel> lv;
     std::unique_ptr<DenseLU> coarse;
+    DevBuf<double> coarse_inv;  // A_c^{-1} (row-major) when n_c <= kCoarseInverseMax
     int nu, partitions, restart, smooth_solves;
     DevBuf<double> res2;
     DevBuf<int> nonfinite;

@@ -22,6 +22,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 namespace pd {
@@ -133,30 +134,63 @@ double vec_norm_host(Ctx& c, const double* x, int64_t n) {
 }
 
 // ------------------------------------------------------------------ CSR SpMV
-// One thread per row, CSR order, sum starting at 0.0 like scipy's csr_matvec.
+// One thread per row, CSR order, sum starting at 0.0 like scipy's csr_matvec
+// (so results are bitwise scipy's).  Each CTA owns a tile of BS consecutive
+// rows; the tile's contiguous (values, columns) range is streamed through
+// shared memory with coalesced loads (padded by one slot per 16 entries to
+// spread banks), then every thread walks its own row in order.
 // mode: 0 y = Ax, 1 y = b - Ax, 2 y = b + Ax.  Optional fused sum of y^2 and a
 // non-finite flag on x (the V-cycle's isfinite check, multigrid.py:271).
+constexpr int kSpmvCap = 2048;  // staged entries per chunk (24 KB + padding)
+__device__ __forceinline__ int spad(int k) { return k + (k >> 4); }
+
 template <bool REDUCE>
-__global__ void k_spmv(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                       const double* __restrict__ v, const double* __restrict__ x,
-                       double* y, int mode, const double* b,  // y may alias b (x += P xc)
-                       const int* guard, int want, double* partials, unsigned int* counter,
-                       double* norm2, int* nonfinite) {
+__global__ void __launch_bounds__(BS) k_spmv(int64_t n, const int64_t* __restrict__ rp,
+                                             const int32_t* __restrict__ ci,
+                                             const double* __restrict__ v,
+                                             const double* __restrict__ x, double* y, int mode,
+                                             const double* b,  // y may alias b (x += P xc)
+                                             const int* guard, int want, double* partials,
+                                             unsigned int* counter, double* norm2,
+                                             int* nonfinite) {
     if (guard_off(guard, want)) return;
+    __shared__ double sv[kSpmvCap + kSpmvCap / 16];
+    __shared__ int32_t sc[kSpmvCap + kSpmvCap / 16];
     double acc2 = 0.0;
     bool bad = false;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t r0 = (int64_t)blockIdx.x * BS; r0 < n; r0 += (int64_t)gridDim.x * BS) {
+        const int64_t i = r0 + threadIdx.x;
+        const int64_t rend = min(r0 + (int64_t)BS, n);
+        const int64_t e0 = rp[r0], e1 = rp[rend];
+        int64_t a = 0, bnd = 0;
+        if (i < n) {
+            a = rp[i];
+            bnd = rp[i + 1];
+        }
         double s = 0.0;
-        const int64_t e = rp[i + 1];
-        for (int64_t p = rp[i]; p < e; ++p) s = add(s, mul(v[p], x[ci[p]]));
-        double out = s;
-        if (mode == 1) out = sub(b[i], s);
-        else if (mode == 2) out = add(b[i], s);
-        y[i] = out;
-        if (REDUCE) {
-            acc2 = fma(out, out, acc2);
-            if (nonfinite && !isfinite(x[i])) bad = true;
+        for (int64_t c0 = e0; c0 < e1; c0 += kSpmvCap) {
+            const int cnt = (int)min((int64_t)kSpmvCap, e1 - c0);
+            __syncthreads();
+            for (int k = threadIdx.x; k < cnt; k += BS) {
+                sv[spad(k)] = __ldcs(v + c0 + k);
+                sc[spad(k)] = __ldcs(ci + c0 + k);
+            }
+            __syncthreads();
+            const int64_t lo = max(a, c0), hi = min(bnd, c0 + cnt);
+            for (int64_t p = lo; p < hi; ++p) {
+                const int k = spad((int)(p - c0));
+                s = add(s, mul(sv[k], __ldg(x + sc[k])));
+            }
+        }
+        if (i < n) {
+            double out = s;
+            if (mode == 1) out = sub(b[i], s);
+            else if (mode == 2) out = add(b[i], s);
+            y[i] = out;
+            if (REDUCE) {
+                acc2 = fma(out, out, acc2);
+                if (nonfinite && !isfinite(x[i])) bad = true;
+            }
         }
     }
     if (REDUCE) {
@@ -170,13 +204,14 @@ void csr_spmv(Ctx& c, const Csr& A, const double* x, double* y, int mode, const 
     if (A.nrows <= 0) return;
     if (norm2_out) {
         int g = std::min(c.grid_for(A.nrows, BS, 8), kReduceMaxBlocks);
-        launch(k_spmv<true>, g, BS, 0, c.stream, A.nrows, A.rowptr.p, A.col.p, A.val.p, x, y, mode,
-                                             b, guard, want, c.red_partials.p, c.red_counter.p,
-                                             norm2_out, nonfinite_flag);
+        launch(k_spmv<true>, g, BS, 0, c.stream, A.nrows, A.rowptr.p, A.col.p, A.val.p, x, y,
+               mode, b, guard, want, c.red_partials.p, c.red_counter.p, norm2_out,
+               nonfinite_flag);
     } else {
-        int g = c.grid_for(A.nrows, BS, 16);
-        launch(k_spmv<false>, g, BS, 0, c.stream, A.nrows, A.rowptr.p, A.col.p, A.val.p, x, y, mode,
-                                              b, guard, want, nullptr, nullptr, nullptr, nullptr);
+        int g = c.grid_for(A.nrows, BS, 8);
+        launch(k_spmv<false>, g, BS, 0, c.stream, A.nrows, A.rowptr.p, A.col.p, A.val.p, x, y,
+               mode, b, guard, want, (double*)nullptr, (unsigned int*)nullptr, (double*)nullptr,
+               (int*)nullptr);
     }
     PD_LAUNCH_CHECK();
 }
@@ -377,7 +412,7 @@ __global__ void k_ilu0_factor(int64_t n, const int64_t* __restrict__ rp,
 // sweep's output words and the upper sweep re-arms the lower scratch, so no
 // extra initialisation pass is needed between solves.
 constexpr unsigned long long kPending = 0x7ff4a5a55a5a0001ull;  // signalling-NaN payload
-constexpr int kChunk = 16;
+__constant__ unsigned int poll_ns_max = 256;  // poll backoff cap (PD_POLL_NS_MAX)
 
 __device__ __forceinline__ unsigned long long ld_strong_u64(const double* p) {
     unsigned long long v;
@@ -393,6 +428,7 @@ __device__ __forceinline__ void st_pending(double* p) {
 }
 
 // s -= sum_{p in [p0,p1)} fac[p] * src[col[p]]  (in order), polling unpublished entries
+template <int kChunk = 16>
 __device__ __forceinline__ double accumulate_polling(double s, const int32_t* __restrict__ ci,
                                                      const double* __restrict__ fac,
                                                      const double* src, int64_t p0, int64_t p1) {
@@ -411,6 +447,7 @@ __device__ __forceinline__ double accumulate_polling(double s, const int32_t* __
         for (int k = 0; k < kChunk; ++k)
             if (k < cnt) v[k] = ld_strong_u64(src + col[k]);
         unsigned int ns = 32;
+        const unsigned int ns_max = poll_ns_max;
         for (;;) {
             bool missing = false;
 #pragma unroll
@@ -421,7 +458,7 @@ __device__ __forceinline__ double accumulate_polling(double s, const int32_t* __
                 }
             if (!missing) break;
             __nanosleep(ns);
-            if (ns < 256) ns <<= 1;
+            if (ns < ns_max) ns <<= 1;
         }
 #pragma unroll
         for (int k = 0; k < kChunk; ++k)
@@ -565,11 +602,13 @@ std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks) {
         launch(k_levels_lower, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, level.p, f->counter.p);
         PD_LAUNCH_CHECK();
         sort_by_level(c, level.p, n, f->order_lo, f->nlevels_lo);
+
         launch(k_fill_int, c.grid_for(n, BS), BS, 0, c.stream, level.p, n, -1);
         PD_CUDA(cudaMemsetAsync(f->counter.p, 0, sizeof(unsigned long long), c.stream));
         launch(k_levels_upper, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, level.p, f->counter.p);
         PD_LAUNCH_CHECK();
         sort_by_level(c, level.p, n, f->order_up, f->nlevels_up);
+
     }
     ilu0_refactor(c, *f);
     return f;
@@ -610,7 +649,18 @@ void ilu0_refactor(Ctx& c, Ilu0& f) {
     }
 }
 
+static void configure_polling_once() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    if (const char* e = getenv("PD_POLL_NS_MAX")) {
+        unsigned int v = (unsigned int)atoi(e);
+        if (v >= 32) PD_CUDA(cudaMemcpyToSymbol(poll_ns_max, &v, sizeof(v)));
+    }
+}
+
 void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int want) {
+    configure_polling_once();
     const int64_t n = f.n;
     if (n == 0) return;
     if (b == x) throw ConfigError("ILU(0) solve needs distinct input and output buffers");
@@ -756,4 +806,77 @@ void dense_lu_solve(Ctx& c, const DenseLU& f, const double* b, double* x) {
     PD_LAUNCH_CHECK();
 }
 
+}  // namespace pd
+
+namespace pd {
+// ------------------------------------------------------------------ coarsest-level inverse
+// The V-cycle's coarsest solve (multigrid.py:259-260) runs once per cycle on
+// the same matrix, so the hierarchy forms A_c^{-1} from the device LU factors
+// at setup (n_c RHS solves, one CTA each) and applies it as one GEMV per
+// cycle: n_c^2 * 8 bytes streamed at HBM/L2 rate instead of 2*n_c dependent
+// substitution steps on one SM.
+__global__ void k_lu_inverse_cols(const double* __restrict__ LU, const int32_t* __restrict__ piv,
+                                  int64_t n, double* inv_rowmajor) {
+    extern __shared__ double xs[];
+    const int64_t j = blockIdx.x;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) xs[i] = (i == j) ? 1.0 : 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int64_t i = 0; i < n; ++i) {
+            int64_t p = piv[i];
+            if (p != i) { double t = xs[i]; xs[i] = xs[p]; xs[p] = t; }
+        }
+    __syncthreads();
+    for (int64_t k = 0; k < n; ++k) {
+        const double xk = xs[k];
+        for (int64_t i = k + 1 + threadIdx.x; i < n; i += blockDim.x) xs[i] -= LU[i + k * n] * xk;
+        __syncthreads();
+    }
+    for (int64_t k = n - 1; k >= 0; --k) {
+        if (threadIdx.x == 0) xs[k] = xs[k] / LU[k + k * n];
+        __syncthreads();
+        const double xk = xs[k];
+        for (int64_t i = threadIdx.x; i < k; i += blockDim.x) xs[i] -= LU[i + k * n] * xk;
+        __syncthreads();
+    }
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) inv_rowmajor[i * n + j] = xs[i];
+}
+
+// x = Ainv b, one warp per row, fixed lane-strided order + shuffle tree (deterministic)
+__global__ void k_gemv_rows(const double* __restrict__ A, const double* __restrict__ b,
+                            double* __restrict__ x, int64_t n) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nw) {
+        const double* row = A + i * n;
+        double s = 0.0;
+        for (int64_t k = lane; k < n; k += 32) s = fma(row[k], __ldg(b + k), s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+        if (lane == 0) x[i] = s;
+    }
+}
+
+DevBuf<double> dense_inverse(Ctx& c, const DenseLU& f) {
+    const int64_t n = f.n;
+    DevBuf<double> inv(std::max<int64_t>(n * n, 1));
+    if (n == 0) return inv;
+    static bool attr = false;
+    if (!attr) {
+        PD_CUDA(cudaFuncSetAttribute(k_lu_inverse_cols, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     227 * 1024));
+        attr = true;
+    }
+    launch(k_lu_inverse_cols, (unsigned)n, 256, n * sizeof(double), c.stream, f.lu.p, f.piv.p, n,
+           inv.p);
+    PD_LAUNCH_CHECK();
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    return inv;
+}
+
+void dense_inverse_apply(Ctx& c, const double* inv, int64_t n, const double* b, double* x) {
+    if (n == 0) return;
+    launch(k_gemv_rows, c.grid_for(n * 32, 256, 8), 256, 0, c.stream, inv, b, x, n);
+}
 }  // namespace pd
