@@ -81,6 +81,7 @@ int pd_mg_create(void *ctx, int nlevels, void **mats, void **R, void **P, int nu
 int pd_mg_level_matrix(void *mg, int level, void **csr_out); /* borrowed handle */
 int pd_mg_level_precond(void *mg, int level, void **ilu_out); /* borrowed ILU/block-Jacobi */
 int pd_mg_refactor(void *ctx, void *mg);                     /* after value updates */
+int pd_mg_set_fine_operator(void *mg, void *stop); /* takes ownership; NULL detaches */
 int pd_mg_vcycle(void *ctx, void *mg, const double *b, double *x); /* multigrid.py:268-273 */
 int pd_mg_solve(void *ctx, void *mg, const double *b, double *x, double tol_rel,
                 double tol_abs, int max_cycles, pd_solve_report *rep, double *hist,
@@ -96,6 +97,22 @@ int pd_reaction(void *ctx, int kind, int deriv, const double *u, double *out, in
 int pd_axpy_to(void *ctx, double *y, const double *x, const double *d, double s, int64_t n);
 int pd_norm(void *ctx, const double *x, int64_t n, double *host_out); /* synchronising */
 int pd_scale(void *ctx, double *y, const double *x, double s, int64_t n);
+
+/* ---- K1: matrix-free space-time operator (spacetime.py:77-80,117-142).
+ *      L = I (x) (Kq (x) Mh + dt Mq (x) Kh) + S_{-1} (x) (-Jq (x) Mh), with
+ *      Jq = l0 l1^T (right Radau: only the last column).  `apply` is bitwise
+ *      the assembled CSR SpMV; mode 0 y=Lx, 1 y=b-Lx, 2 y=b+Lx; halo = the
+ *      previous step's last-node values for a time slab (NULL: none).
+ *      `residual` = F(u) in the reference's blockwise order; kind 0 none,
+ *      1 cubic, 2 Fisher. */
+int pd_stop_create(void *ctx, int64_t Nt, int M, int64_t S, const double *Kq, const double *Mq,
+                   const double *l0, double dt, void *Kh_csr, const double *mh_host,
+                   void **op_out);
+int pd_stop_destroy(void *op);
+int pd_stop_apply(void *op, const double *x, double *y, int mode, const double *b,
+                  const double *halo);
+int pd_stop_residual(void *op, const double *u, const double *rhs, double *out, double gamma,
+                     int kind);
 
 /* ---- SDC / PFASST building blocks, batched over W workers of a window
  *      (pfasst.py:60-303).  State layout: U[W][M][S], U0[W][S], tau[W][M][S]. */

@@ -63,6 +63,12 @@ _SIGNATURES = {
     "pd_mg_solve": (_int, [_vp, _vp, _vp, _vp, _dbl, _dbl, _int, ctypes.POINTER(SolveReportC),
                            _vp, _int]),
     "pd_mg_destroy": (_int, [_vp]),
+    "pd_mg_set_fine_operator": (_int, [_vp, _vp]),
+    "pd_stop_create": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _vp, _dbl, _vp, _vp,
+                              ctypes.POINTER(_vp)]),
+    "pd_stop_destroy": (_int, [_vp]),
+    "pd_stop_apply": (_int, [_vp, _vp, _vp, _int, _vp, _vp]),
+    "pd_stop_residual": (_int, [_vp, _vp, _vp, _vp, _dbl, _int]),
     "pd_st_residual_csr": (_int, [_vp, _vp, _vp, _dbl, _int, _vp, _vp, _vp, _vp]),
     "pd_reaction": (_int, [_vp, _int, _int, _vp, _vp, _i64]),
     "pd_axpy_to": (_int, [_vp, _vp, _vp, _vp, _dbl, _i64]),

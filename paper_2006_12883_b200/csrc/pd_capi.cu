@@ -207,6 +207,12 @@ int pd_mg_level_precond(void* mg, int level, void** ilu_out) {
         *ilu_out = M->level_precond(level);
     });
 }
+int pd_mg_set_fine_operator(void* mg, void* stop) {
+    return guarded([&] {
+        auto* M = H<pd::Multigrid>(mg, "multigrid");
+        M->set_fine_operator(std::unique_ptr<pd::StOp>(static_cast<pd::StOp*>(stop)));
+    });
+}
 int pd_mg_refactor(void* ctx, void* mg) {
     (void)ctx;
     return guarded([&] { H<pd::Multigrid>(mg, "multigrid")->refactor(); });

@@ -282,7 +282,7 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
         ilu0_solve(c, *M, vcur.p, z.p, ph, GM_RUN);
         zin = z.p;
     }
-    csr_spmv(c, *A, zin, w.p, SPMV_SET, nullptr, ph, GM_RUN);
+    apply_A(c, *A, op, zin, w.p, SPMV_SET, nullptr, ph, GM_RUN);
     const int passes = std::min(mgs_passes, restart + 1);
     for (int i = 0; i < passes; ++i)
         launch(k_gm_mgs, gr, KB, 0, c.stream, st.p, i, w.p, V.p, n, c.red_partials.p,
@@ -298,7 +298,7 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
         du = z.p;
     }
     launch(k_gm_update_x, g, KB, 0, c.stream, st.p, xg.p, du, n);
-    csr_spmv(c, *A, xg.p, rg.p, SPMV_RESID, b, ph, GM_FINISH, norm2.p, nullptr);
+    apply_A(c, *A, op, xg.p, rg.p, SPMV_RESID, b, ph, GM_FINISH, norm2.p, nullptr);
     launch(k_gm_restart, 1, 1, 0, c.stream, st.p, norm2.p, hist.p);
     PD_LAUNCH_CHECK();
 }
@@ -318,11 +318,11 @@ std::vector<double> Gmres::history(int total) {
     return h;
 }
 
-void enqueue_gmres_smooth(Ctx& c, Gmres& g, const Csr& A, const double* b, double* x,
-                          double* r_work, int nu) {
+void enqueue_gmres_smooth(Ctx& c, Gmres& g, const Csr& A, const StOp* op, const double* b,
+                          double* x, double* r_work, int nu) {
     const int64_t n = A.nrows;
     // r = b - A x with |r|^2 (the GMRES initial residual; x0 = 0 so r0 = r)
-    csr_spmv(c, A, x, r_work, SPMV_RESID, b, nullptr, 0, c.scalars.p + 8, nullptr);
+    apply_A(c, A, op, x, r_work, SPMV_RESID, b, nullptr, 0, c.scalars.p + 8, nullptr);
     g.enqueue_init(r_work, c.scalars.p + 8, 1e-13, 0.0);
     for (int s = 0; s < nu; ++s) g.enqueue_slot(s, s + 2, r_work);
     launch(k_gm_apply, c.grid_for(n, KB, 8), KB, 0, c.stream, g.dev(), x, g.x(), n);
@@ -365,6 +365,12 @@ Multigrid::Multigrid(Ctx& c_, std::vector<std::unique_ptr<Csr>> mats,
     refactor();
 }
 
+void Multigrid::set_fine_operator(std::unique_ptr<StOp> op) {
+    if (op && op->size() != lv[0].n) throw ConfigError("fine operator size does not match level 1");
+    fine_op = std::move(op);
+    if (lv.size() > 1 && lv[0].gm) lv[0].gm->set_operator(fine_op.get());
+}
+
 void Multigrid::refactor() {
     const int L = (int)lv.size();
     for (int l = 0; l + 1 < L; ++l) {
@@ -393,14 +399,17 @@ void Multigrid::cycle(int l) {
         else dense_lu_solve(c, *coarse, b, x);
         return;
     }
-    for (int s = 0; s < smooth_solves; ++s) enqueue_gmres_smooth(c, *m.gm, *m.A, b, x, m.r.p, nu);
-    csr_spmv(c, *m.A, x, m.r.p, SPMV_RESID, b);
+    const StOp* op = (l == 0) ? fine_op.get() : nullptr;
+    for (int s = 0; s < smooth_solves; ++s)
+        enqueue_gmres_smooth(c, *m.gm, *m.A, op, b, x, m.r.p, nu);
+    apply_A(c, *m.A, op, x, m.r.p, SPMV_RESID, b);
     MgLevel& nx = lv[l + 1];
     csr_spmv(c, *m.R, m.r.p, nx.b.p, SPMV_SET, nullptr);
     if (l + 1 < L - 1) vec_fill(c, nx.x.p, nx.n, 0.0);
     cycle(l + 1);
     csr_spmv(c, *m.P, nx.x.p, x, SPMV_ADD, x);
-    for (int s = 0; s < smooth_solves; ++s) enqueue_gmres_smooth(c, *m.gm, *m.A, b, x, m.r.p, nu);
+    for (int s = 0; s < smooth_solves; ++s)
+        enqueue_gmres_smooth(c, *m.gm, *m.A, op, b, x, m.r.p, nu);
 }
 
 void Multigrid::enqueue_vcycle(const double* b, double* x) {
@@ -441,7 +450,7 @@ Multigrid::Report Multigrid::solve(const double* b, double* x, double tol_rel, d
     MgLevel& f = lv[0];
     const int64_t n = f.n;
     double* r = f.r.p;
-    csr_spmv(c, *f.A, x, r, SPMV_RESID, b, nullptr, 0, res2.p, nullptr);
+    apply_A(c, *f.A, fine_op.get(), x, r, SPMV_RESID, b, nullptr, 0, res2.p, nullptr);
     double h2 = 0.0;
     PD_CUDA(cudaMemcpyAsync(&h2, res2.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     PD_CUDA(cudaStreamSynchronize(c.stream));
@@ -456,7 +465,7 @@ Multigrid::Report Multigrid::solve(const double* b, double* x, double tol_rel, d
         }
         enqueue_vcycle(b, x);
         PD_CUDA(cudaMemsetAsync(nonfinite.p, 0, sizeof(int), c.stream));
-        csr_spmv(c, *f.A, x, r, SPMV_RESID, b, nullptr, 0, res2.p, nonfinite.p);
+        apply_A(c, *f.A, fine_op.get(), x, r, SPMV_RESID, b, nullptr, 0, res2.p, nonfinite.p);
         int bad = 0;
         PD_CUDA(cudaMemcpyAsync(&h2, res2.p, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
         PD_CUDA(cudaMemcpyAsync(&bad, nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));

@@ -5,6 +5,7 @@
 #pragma once
 
 #include "pd_internal.h"
+#include "pd_stencil.h"
 
 namespace pd {
 
@@ -34,11 +35,13 @@ class Gmres {
     double* x() { return xg.p; }
     int64_t size() const { return n; }
     GmDev* dev() { return st.p; }
+    void set_operator(const StOp* o) { op = o; }
     std::vector<double> history(int total);
 
    private:
     Ctx& c;
     const Csr* A;
+    const StOp* op = nullptr;  // matrix-free A (level 0 of a structured hierarchy)
     Ilu0* M;
     int64_t n;
     int restart, max_it;
@@ -50,8 +53,8 @@ class Gmres {
 // Enqueue x += GMRES(A, b - A x) with ILU/block-Jacobi right preconditioning,
 // restart=min(nu,restart), max_it=nu, tol_rel=1e-13, tol_abs=0: exactly one
 // smoothing solve of multigrid.py:243-256.  No host synchronisation.
-void enqueue_gmres_smooth(Ctx& c, Gmres& g, const Csr& A, const double* b, double* x,
-                          double* r_work, int nu);
+void enqueue_gmres_smooth(Ctx& c, Gmres& g, const Csr& A, const StOp* op, const double* b,
+                          double* x, double* r_work, int nu);
 
 struct MgLevel {
     std::unique_ptr<Csr> A, R, P;  // R/P: transfer to the next coarser level (unused on coarsest)
@@ -70,6 +73,8 @@ class Multigrid {
     void refactor();
     Csr& level_matrix(int l) { return *lv[l].A; }
     Ilu0* level_precond(int l) { return lv[l].pre.get(); }
+    // level 0 applies A through a matrix-free operator (values must equal the CSR's)
+    void set_fine_operator(std::unique_ptr<StOp> op);
     int num_levels() const { return (int)lv.size(); }
     int64_t fine_size() const { return lv[0].n; }
     // x <- V-cycle(b, x)  (device pointers, n = fine size); no host sync
@@ -88,6 +93,7 @@ class Multigrid {
     Ctx& c;
     std::vector<MgLevel> lv;
     std::unique_ptr<DenseLU> coarse;
+    std::unique_ptr<StOp> fine_op;
     DevBuf<double> coarse_inv;  // A_c^{-1} (row-major) when n_c <= kCoarseInverseMax
     int nu, partitions, restart, smooth_solves;
     DevBuf<double> res2;

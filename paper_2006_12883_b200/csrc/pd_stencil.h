@@ -1,0 +1,35 @@
+// K1 matrix-free space-time operator (see pd_stencil.cu).
+#pragma once
+
+#include "pd_internal.h"
+
+namespace pd {
+
+constexpr int kStMaxM = 9;
+
+struct StOp {
+    Ctx& c;
+    int64_t Nt, M, S;
+    double dt;
+    double Kq[kStMaxM * kStMaxM], Mq[kStMaxM * kStMaxM], l0[kStMaxM];
+    std::unique_ptr<Csr> Kh;
+    DevBuf<double> mh;
+    StOp(Ctx& c, int64_t Nt, int M, int64_t S, const double* Kq, const double* Mq,
+         const double* l0, double dt, const Csr& Kh, const double* mh_host);
+    int64_t size() const { return Nt * M * S; }
+    // same contract as csr_spmv (modes 0/1/2, guard, fused |y|^2, non-finite flag on x)
+    void apply(const double* x, double* y, int mode, const double* b, const int* guard = nullptr,
+               int want = 0, double* norm2_out = nullptr, int* nonfinite = nullptr,
+               const double* halo = nullptr) const;
+    void residual(const double* u, const double* rhs, double* out, double gamma, int kind) const;
+};
+
+// y = A x through the structured operator when present, else the CSR
+inline void apply_A(Ctx& c, const Csr& A, const StOp* op, const double* x, double* y, int mode,
+                    const double* b, const int* guard = nullptr, int want = 0,
+                    double* norm2 = nullptr, int* nonfinite = nullptr) {
+    if (op) op->apply(x, y, mode, b, guard, want, norm2, nonfinite);
+    else csr_spmv(c, A, x, y, mode, b, guard, want, norm2, nonfinite);
+}
+
+}  // namespace pd

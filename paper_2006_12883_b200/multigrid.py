@@ -197,6 +197,11 @@ class MultigridHierarchy:
             raise ConfigurationError(
                 f"matrix size {A.shape[0]} does not match level 1 size {self.dims[0].size}")
         mats = self._galerkin(A)
+        if self._mg is not None and getattr(self, "_has_fine_op", False):
+            # a new fine matrix (e.g. a Newton Jacobian) no longer matches the
+            # matrix-free operator attached by build_hierarchy
+            N.call("pd_mg_set_fine_operator", self._mg, None)
+            self._has_fine_op = False
         if self._mg is not None and all(d.same_pattern(m) for d, m in zip(self._dev_mats, mats)):
             for d, m in zip(self._dev_mats, mats):
                 d.set_values(m.data)
@@ -221,6 +226,19 @@ class MultigridHierarchy:
             self._dev_mats = dev  # borrowed views for pattern checks/value updates
         self.matrices = mats
         self.setup_time = time.perf_counter() - t0
+
+    def attach_fine_operator(self, system) -> None:
+        """Apply level 1 matrix-free (K1, bitwise the system's global CSR product).
+
+        The CSR stays the input of the level-1 ILU(0) factorization; every
+        other use of A_1 (smoother GMRES, residuals, restriction input, the
+        solve's stopping test) streams only vectors.
+        """
+        if self._mg is None:
+            return
+        op = system.stencil_operator_handle(self.ctx)
+        N.call("pd_mg_set_fine_operator", self._mg, op)  # ownership moves to the hierarchy
+        self._has_fine_op = True
 
     def _destroy(self):
         if self._mg is not None:
@@ -316,8 +334,11 @@ def build_hierarchy(system, strategy: str, L: int, nu: int, partitions: int = 1,
         raise ConfigurationError("coarsest spatial level has fewer than 2 dofs")
     transfers = _build_transfers(dims, pairs)
     A = matrix if matrix is not None else system.global_matrix()
-    return MultigridHierarchy(A, strategy, dims, transfers, nu=nu, partitions=partitions,
-                              restart=restart, smooth_solves=smooth_solves)
+    h = MultigridHierarchy(A, strategy, dims, transfers, nu=nu, partitions=partitions,
+                           restart=restart, smooth_solves=smooth_solves)
+    if matrix is None:
+        h.attach_fine_operator(system)
+    return h
 
 
 def mg_linear_solver(hierarchy: MultigridHierarchy, tol_rel=1e-9, tol_abs=1e-9, max_cycles=1000,
