@@ -397,6 +397,73 @@ __global__ void k_terminal(const double* U, double* out, int W, int M, int64_t S
     }
 }
 
+// Implicit-mode nonlinear node solve (pfasst.py:134-152), one thread per
+// worker, entirely on device: Newton on g(u) = mh u + q (Kh u + gamma mh r(u)) - b
+// with J = Mh + q (Kh + gamma diag(mh r'(u))) factored exactly each step
+// (tridiagonal Thomas = the ILU(0) the reference preconditions with, which
+// makes its inner GMRES converge in one step).  Stops at
+// ||g|| <= 1e-12 max(1, ||b||); 50 steps without convergence -> error bit 4.
+__global__ void k_node_newton_tri(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ kv, const double* __restrict__ mh,
+                                  int64_t S, double q, double gamma, int kind,
+                                  const double* __restrict__ b, double* x, double* gbuf,
+                                  double* lbuf, double* ubuf, int W, int* err) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= W) return;
+    const double* bw = b + (int64_t)w * S;
+    double* u = x + (int64_t)w * S;
+    double* g = gbuf + (int64_t)w * S;
+    double* l = lbuf + (int64_t)w * S;
+    double* d = ubuf + (int64_t)w * S;
+    double bn = 0.0;
+    for (int64_t j = 0; j < S; ++j) bn = fma(bw[j], bw[j], bn);
+    const double scale = fmax(1.0, sqrt(bn));
+    for (int it = 0; it < 50; ++it) {
+        double gn = 0.0;
+        for (int64_t j = 0; j < S; ++j) {
+            double kuj = 0.0;
+            for (int64_t p = rp[j]; p < rp[j + 1]; ++p) kuj = add(kuj, mul(kv[p], u[ci[p]]));
+            const double inner = add(kuj, mul(mul(gamma, mh[j]), react(kind, u[j])));
+            const double gj = sub(add(mul(mh[j], u[j]), mul(q, inner)), bw[j]);
+            g[j] = gj;
+            gn = fma(gj, gj, gn);
+        }
+        if (!(sqrt(gn) > mul(1e-12, scale))) {
+            if (!isfinite(gn)) atomicOr(err, 4);
+            return;
+        }
+        // Thomas on J delta = -g (J tridiagonal; entries rebuilt per row)
+        double uprev = 0.0, cprev = 0.0, yprev = 0.0;
+        for (int64_t j = 0; j < S; ++j) {
+            double a = 0.0, dj = 0.0, c = 0.0;
+            for (int64_t p = rp[j]; p < rp[j + 1]; ++p) {
+                if (ci[p] == j - 1) a = mul(q, kv[p]);
+                else if (ci[p] == j + 1) c = mul(q, kv[p]);
+                else if (ci[p] == j)
+                    dj = add(mh[j], mul(q, add(kv[p], mul(gamma, mul(mh[j], react_d(kind, u[j]))))));
+            }
+            double lj = 0.0;
+            if (j > 0) {
+                lj = a / uprev;
+                dj = sub(dj, mul(lj, cprev));
+            }
+            const double yj = sub(-g[j], mul(lj, yprev));
+            l[j] = c;   // keep the superdiagonal for the back sweep
+            d[j] = dj;
+            g[j] = yj;  // forward-substituted rhs
+            uprev = dj;
+            cprev = c;
+            yprev = yj;
+        }
+        double xn = 0.0;
+        for (int64_t j = S - 1; j >= 0; --j) {
+            xn = sub(g[j], mul(l[j], xn)) / d[j];
+            u[j] = add(u[j], xn);
+        }
+    }
+    atomicOr(err, 4);
+}
+
 Small small_from(const double* h, int r, int cols) {
     Small s;
     std::memset(&s, 0, sizeof(s));
@@ -469,8 +536,9 @@ void sdc_sweep(SdcLevelDev& L, double* U, const double* U0, const double* tau, i
     const int64_t n = (int64_t)W * M * S;
     const bool imex = L.imex && L.gamma != 0.0;
     if (W > L.maxW) throw ConfigError("too many workers for this SDC level");
-    if (L.gamma != 0.0 && !imex)
-        throw ConfigError("implicit-mode nonlinear node solves run with mode='imex' on the device");
+    if (L.gamma != 0.0 && !imex && L.solver != 0)
+        throw ConfigError("implicit-mode nonlinear node solves need a tridiagonal Kh on the "
+                          "device (use mode='imex', the reference default for gamma > 0)");
     feval(L, U, L.fi_old.p, L.fe_old.p, W, M, 0);
     if (imex) {
         launch(k_sdc_base, c.grid_for(n, TB), TB, 0, c.stream, U0, L.fi_old.p, L.fe_old.p, tau,
@@ -488,7 +556,15 @@ void sdc_sweep(SdcLevelDev& L, double* U, const double* U0, const double* tau, i
                L.QDI, L.QDE, imex ? 1 : 0);
         launch(k_gather_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, U, L.x.p, W, M, S,
                m);
-        node_solve(L, m, L.bvec.p, L.x.p, W, 2);
+        if (L.gamma != 0.0 && !imex) {
+            // the back sweep updates u in place: x holds the guess U[m]
+            launch(k_node_newton_tri, (W + 31) / 32, 32, 0, c.stream, L.Kh->rowptr.p,
+                   L.Kh->col.p, L.Kh->val.p, L.mh.p, S, L.dt * L.QDI.a[m * M + m], L.gamma,
+                   L.kind, (const double*)L.bvec.p, L.x.p, L.r.p, L.rhs.p, L.fe_old.p,
+                   W, L.err.p);
+        } else {
+            node_solve(L, m, L.bvec.p, L.x.p, W, 2);
+        }
         launch(k_scatter_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.x.p, U, W, M, S,
                m);
         // f of the new node value (stored in the node-m slot of fi_new/fe_new)

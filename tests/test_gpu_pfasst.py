@@ -105,3 +105,15 @@ def test_divergent_window_reports_nc():
                                      mode="imex")
     u, rep = PF.pfasst_run(hier, prob.u0(mesh.vertices), 4, 4, max_iters=150)
     assert not rep.converged and rep.diverged
+
+
+def test_pfasst_monodomain_implicit_newton_node_solves(golden):
+    """Implicit mode: nonlinear node solves by on-device Newton (pfasst.py:134-152)."""
+    g = golden("pfasst_fem1d")
+    prob = pd.monodomain_problem()
+    mesh = pd.SpaceMesh(64, prob.X)
+    hier = PF.build_pfasst_hierarchy(2, mesh, pd.TimeGrid(16, prob.T), prob.gamma, L=2, nu=1,
+                                     mode="implicit")
+    x, rep = PF.pfasst_run(hier, prob.u0(mesh.vertices), 16, 4, tol_rel=1e-9, tol_abs=1e-9)
+    assert rep.inner_iterations == g["mono_implicit_inner"].tolist()
+    assert per_node_rel(x, g["mono_implicit_x"], (16, 2, 65)) < 1e-9
