@@ -140,41 +140,9 @@ int pd_gmres(void* ctx, void* A, void* ilu, const double* b, const double* x0, d
     return guarded([&] {
         pd::Ctx& c = *C(ctx);
         pd::Csr& M = *H<pd::Csr>(A, "matrix");
-        if (M.nrows != M.ncols) throw pd::ConfigError("GMRES needs a square matrix");
-        if (max_it < 0) throw pd::ConfigError("max_it must be nonnegative");
-        const int64_t n = M.nrows;
-        pd::Gmres g(c, &M, static_cast<pd::Ilu0*>(ilu), n, restart, std::max(max_it, 1));
-        // r0 = b - A x0 (x0 = 0 when absent: r0 = b, exactly as b - A@0)
-        pd::DevBuf<double> r0(std::max<int64_t>(n, 1)), zero;
-        const double* xs = x0;
-        if (!xs) {
-            zero.alloc(std::max<int64_t>(n, 1));
-            pd::vec_fill(c, zero.p, n, 0.0);
-            xs = zero.p;
-        }
-        pd::csr_spmv(c, M, xs, r0.p, pd::SPMV_RESID, b, nullptr, 0, c.scalars.p + 16, nullptr);
-        g.enqueue_init(r0.p, c.scalars.p + 16, tol_rel, tol_abs, x0);
-        pd::GmDev s = g.read_state();
-        // host mirrors (phase, j) after every Arnoldi step; guards cover the rest
-        int slot = 0;
-        while (s.phase != pd::GM_DONE && s.total < std::max(max_it, 1)) {
-            const int j_eff = (s.phase == pd::GM_START) ? 0 : s.j;
-            g.enqueue_slot(slot++, j_eff + 2, b);
-            s = g.read_state();
-        }
-        if (s.err == 1) throw pd::SolverError("non-finite initial residual in GMRES");
-        if (s.err == 2) throw pd::SolverError("non-finite residual in GMRES iteration");
-        if (s.err == 3) throw pd::SolverError("non-finite residual in GMRES restart");
-        // the engine accumulates x = x0 + psolve(V y) per cycle, as the reference
-        if (s.cycles > 0) {
-            pd::vec_copy(c, x, g.x(), n);
-        } else {
-            if (x0) pd::vec_copy(c, x, x0, n);
-            else pd::vec_fill(c, x, n, 0.0);
-        }
-        auto h = g.history(s.total);
-        PD_CUDA(cudaStreamSynchronize(c.stream));
-        fill_report(rep, s.total, s.converged != 0, s.diverged != 0, h, hist, hist_cap);
+        auto r = pd::gmres_run(c, M, static_cast<pd::Ilu0*>(ilu), b, x0, x, tol_rel, tol_abs,
+                               restart, max_it);
+        fill_report(rep, r.iterations, r.converged, r.diverged, r.hist, hist, hist_cap);
     });
 }
 

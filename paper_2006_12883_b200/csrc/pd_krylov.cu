@@ -329,6 +329,48 @@ void enqueue_gmres_smooth(Ctx& c, Gmres& g, const Csr& A, const StOp* op, const 
     PD_LAUNCH_CHECK();
 }
 
+GmresResult gmres_run(Ctx& c, const Csr& A, Ilu0* M, const double* b, const double* x0, double* x,
+                      double tol_rel, double tol_abs, int restart, int max_it) {
+    if (A.nrows != A.ncols) throw ConfigError("GMRES needs a square matrix");
+    if (max_it < 0) throw ConfigError("max_it must be nonnegative");
+    const int64_t n = A.nrows;
+    Gmres g(c, &A, M, n, restart, std::max(max_it, 1));
+    // r0 = b - A x0 (x0 = 0 when absent: r0 = b, exactly as b - A@0)
+    DevBuf<double> r0(std::max<int64_t>(n, 1)), zero;
+    const double* xs = x0;
+    if (!xs) {
+        zero.alloc(std::max<int64_t>(n, 1));
+        vec_fill(c, zero.p, n, 0.0);
+        xs = zero.p;
+    }
+    csr_spmv(c, A, xs, r0.p, SPMV_RESID, b, nullptr, 0, c.scalars.p + 16, nullptr);
+    g.enqueue_init(r0.p, c.scalars.p + 16, tol_rel, tol_abs, x0);
+    GmDev s = g.read_state();
+    // the host mirrors (phase, j) after every Arnoldi step; guards cover the rest
+    int slot = 0;
+    while (s.phase != GM_DONE && s.total < std::max(max_it, 1)) {
+        const int j_eff = (s.phase == GM_START) ? 0 : s.j;
+        g.enqueue_slot(slot++, j_eff + 2, b);
+        s = g.read_state();
+    }
+    if (s.err == 1) throw SolverError("non-finite initial residual in GMRES");
+    if (s.err == 2) throw SolverError("non-finite residual in GMRES iteration");
+    if (s.err == 3) throw SolverError("non-finite residual in GMRES restart");
+    // the engine accumulates x = x0 + psolve(V y) per cycle, as the reference
+    if (s.cycles > 0) {
+        if (x != g.x()) vec_copy(c, x, g.x(), n);
+    } else {
+        if (x0) vec_copy(c, x, x0, n);
+        else vec_fill(c, x, n, 0.0);
+    }
+    GmresResult r;
+    r.hist = g.history(s.total);
+    r.iterations = s.total;
+    r.converged = s.converged != 0;
+    r.diverged = s.diverged != 0;
+    return r;
+}
+
 // ------------------------------------------------------------------ Multigrid
 Multigrid::Multigrid(Ctx& c_, std::vector<std::unique_ptr<Csr>> mats,
                      std::vector<std::unique_ptr<Csr>> R, std::vector<std::unique_ptr<Csr>> P,

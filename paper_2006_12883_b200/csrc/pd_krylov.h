@@ -50,6 +50,16 @@ class Gmres {
     const double* r0 = nullptr;
 };
 
+// Full restarted GMRES (linalg.py:215-311) with host-mirrored control
+// (one sync per Arnoldi step): x = x0 + ...; x may alias x0.
+struct GmresResult {
+    int iterations = 0;
+    bool converged = false, diverged = false;
+    std::vector<double> hist;
+};
+GmresResult gmres_run(Ctx& c, const Csr& A, Ilu0* M, const double* b, const double* x0, double* x,
+                      double tol_rel, double tol_abs, int restart, int max_it);
+
 // Enqueue x += GMRES(A, b - A x) with ILU/block-Jacobi right preconditioning,
 // restart=min(nu,restart), max_it=nu, tol_rel=1e-13, tol_abs=0: exactly one
 // smoothing solve of multigrid.py:243-256.  No host synchronisation.

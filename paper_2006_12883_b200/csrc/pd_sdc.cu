@@ -21,10 +21,12 @@
 #include "../../include/paradiff_b200.h"
 #include "pd_device.cuh"
 #include "pd_internal.h"
+#include "pd_krylov.h"
 
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <string>
 #include <vector>
 
 namespace pd {
@@ -200,6 +202,8 @@ struct SdcLevelDev {
     DevBuf<double> tl, tu, tc;
     // dense factors (solver 1)
     std::vector<std::unique_ptr<DenseLU>> dlu;
+    // ILU(0) of each node operator (solver 2: the reference's GMRES path)
+    std::vector<std::unique_ptr<Ilu0>> ilu;
     // scratch
     DevBuf<double> fi_old, fe_old, f_tot, base, fi_new, fe_new, rhs, bvec, x, r, tmp;
     DevBuf<double> partials, beta0, thr, beta, lowest;
@@ -498,6 +502,21 @@ static void node_apply_inverse(SdcLevelDev& L, int m, const double* r, double* z
 // x (in: guess, out: solution) for W workers; b = mh*rhs (W x S contiguous)
 static void node_solve(SdcLevelDev& L, int m, const double* b, double* x, int W, int rounds) {
     Ctx& c = L.c;
+    if (L.solver == 2) {
+        // pfasst.py:118-132 verbatim: GMRES(30, max 200) + ILU(0), x0 = guess,
+        // tol_rel 1e-13, tol_abs 1e-13 max(1, |b|); worker by worker
+        const int64_t S = L.S;
+        for (int w = 0; w < W; ++w) {
+            const double* bw = b + (int64_t)w * S;
+            double* xw = x + (int64_t)w * S;
+            const double bn = vec_norm_host(c, bw, S);
+            auto r = gmres_run(c, *L.Am[m], L.ilu[m].get(), bw, xw, xw, 1e-13,
+                               1e-13 * std::max(1.0, bn), 30, 200);
+            if (r.diverged)
+                throw SolverError("node solve failed at node " + std::to_string(m), m);
+        }
+        return;
+    }
     const int64_t S = L.S;
     const Csr& A = *L.Am[m];
     double* bn = L.tmp.p;  // W norms
@@ -675,8 +694,9 @@ int pd_sdc_level_create(void* ctx, void* Kh, const double* mh_host, int M, const
             }
             if (!has_d) throw pd::ConfigError("Kh pattern must contain the diagonal");
         }
-        L->solver = tri ? 0 : 1;
-        if (!tri && S > 28000) throw pd::ConfigError("general node operator too large for the dense node solver");
+        const char* force = getenv("PD_NODE_SOLVER");
+        const bool want_gmres = force && std::string(force) == "gmres";
+        L->solver = tri ? 0 : ((S <= 4096 && !want_gmres) ? 1 : 2);
         for (int m = 0; m < M; ++m) {
             const double q = dt * QDI[m * M + m];
             std::vector<double> av(K->nnz);
@@ -695,6 +715,8 @@ int pd_sdc_level_create(void* ctx, void* Kh, const double* mh_host, int M, const
                 pd::launch(pd::k_tri_factor, 1, 1, 0, c.stream, L->Am[m]->rowptr.p, L->Am[m]->col.p,
                            L->Am[m]->val.p, S, L->tl.p + m * S, L->tu.p + m * S, L->tc.p + m * S,
                            L->err.p);
+        } else if (L->solver == 2) {
+            for (int m = 0; m < M; ++m) L->ilu.push_back(pd::ilu0_create(c, *L->Am[m], 1));
         } else {
             for (int m = 0; m < M; ++m) L->dlu.push_back(pd::dense_lu_from_csr(c, *L->Am[m]));
             static bool attr = false;

@@ -117,3 +117,16 @@ def test_pfasst_monodomain_implicit_newton_node_solves(golden):
     x, rep = PF.pfasst_run(hier, prob.u0(mesh.vertices), 16, 4, tol_rel=1e-9, tol_abs=1e-9)
     assert rep.inner_iterations == g["mono_implicit_inner"].tolist()
     assert per_node_rel(x, g["mono_implicit_x"], (16, 2, 65)) < 1e-9
+
+
+def test_c2_small_pfasst_reference_gmres_node_solves(golden, monkeypatch):
+    """Node solves by the reference's own ILU(0)-GMRES(30) on device (pfasst.py:118-132)."""
+    monkeypatch.setenv("PD_NODE_SOLVER", "gmres")
+    g = golden("c2_small")
+    spec = pd.StencilSpec(2, 15, "dirichlet", 1.0)
+    ops = pd.fd_space(spec)
+    hier = PF.build_pfasst_hierarchy(3, ops.mesh, pd.TimeGrid(8, 8 / 64), 0.0, L=2, nu=1,
+                                     space=ops, M_coarse=2)
+    x, rep = PF.pfasst_run(hier, g["u0"], 8, 4, tol_rel=1e-9, tol_abs=1e-9)
+    assert rep.inner_iterations == g["PF_P4_inner"].tolist()
+    assert per_node_rel(x, g["PF_P4_x"], (8, 3, 225)) < 1e-10
