@@ -251,5 +251,70 @@ def main():
     save("c2_small", **out)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--configs" not in sys.argv:
     main()
+
+
+def fisher_patch():
+    """Monkeypatch the four reaction globals to Fisher-KPP."""
+    import paradiff.pfasst as ppf
+    import paradiff.spacetime as pst
+
+    saved = (pst.reaction, pst.reaction_deriv, ppf.reaction, ppf.reaction_deriv)
+    fr = lambda u: u**2 - u  # noqa: E731
+    fd = lambda u: 2.0 * u - 1.0  # noqa: E731
+    pst.reaction, pst.reaction_deriv, ppf.reaction, ppf.reaction_deriv = fr, fd, fr, fd
+
+    def restore():
+        pst.reaction, pst.reaction_deriv, ppf.reaction, ppf.reaction_deriv = saved
+
+    return restore
+
+
+def configs_reduced():
+    out = {}
+    # C3: 2D periodic Fisher-KPP, gamma = 1, dt = 0.01, M = 3 (reduced 16^2 x 8 steps)
+    cfg3 = PB.baseline_config("C3", n=16, Nt=8)
+    u03 = cfg3.u0()
+    out["c3_u0"] = u03
+    restore = fisher_patch()
+    try:
+        sys3 = assemble_system(make_tableau(3), injected(cfg3.spec), TimeGrid(cfg3.Nt, cfg3.T),
+                               cfg3.gamma, u03)
+        h = fd_mg(sys3, cfg3.spec, "STMG", 2, 3, 1, cfg3.Nt, 3)
+        x, rep = newton_solve(sys3, mg_linear_solver(h, tol_rel=1e-9, tol_abs=1e-9), tol=1e-9)
+        out["c3_newton_x"], out["c3_newton_its"] = x, rep.iterations
+        out["c3_newton_inner"] = np.array(rep.inner_iterations)
+        hier = fd_pfasst(cfg3.spec, 3, 2, cfg3.dt, cfg3.gamma, "imex", 1)
+        x, rep = pfasst_run(hier, u03, cfg3.Nt, 4, tol_rel=1e-9, tol_abs=1e-9)
+        out["c3_pf_x"], out["c3_pf_its"] = x, rep.iterations
+        out["c3_pf_inner"] = np.array(rep.inner_iterations)
+    finally:
+        restore()
+    # C4: 3D Dirichlet heat, M = 5 (coarse 3), dt = 1/256 (reduced 7^3 x 8 steps)
+    cfg4 = PB.baseline_config("C4", n=7, Nt=8)
+    u04 = cfg4.u0()
+    out["c4_u0"] = u04
+    hier = fd_pfasst(cfg4.spec, 5, 3, cfg4.dt, 0.0, "implicit", 1)
+    x, rep = pfasst_run(hier, u04, cfg4.Nt, 4, tol_rel=1e-9, tol_abs=1e-9)
+    out["c4_pf_x"], out["c4_pf_its"] = x, rep.iterations
+    out["c4_pf_inner"] = np.array(rep.inner_iterations)
+    sys4 = assemble_system(make_tableau(5), injected(cfg4.spec), TimeGrid(cfg4.Nt, cfg4.T), 0.0, u04)
+    h = fd_mg(sys4, cfg4.spec, "SMG", 2, 3, 2, cfg4.Nt, 5)
+    x, rep = h.solve(sys4.rhs(), tol_rel=1e-10, tol_abs=1e-10)
+    out["c4_smg_x"], out["c4_smg_its"] = x, rep.iterations
+    # C5: 3D periodic Allen-Cahn-type (cubic), coef 0.1, gamma 1, dt 1e-3 (reduced 8^3 x 4)
+    cfg5 = PB.baseline_config("C5", n=8, Nt=4)
+    u05 = cfg5.u0()
+    out["c5_u0"] = u05
+    sys5 = assemble_system(make_tableau(3), injected(cfg5.spec), TimeGrid(cfg5.Nt, cfg5.T),
+                           cfg5.gamma, u05)
+    h = fd_mg(sys5, cfg5.spec, "STMG", 2, 3, 1, cfg5.Nt, 3)
+    x, rep = newton_solve(sys5, mg_linear_solver(h, tol_rel=1e-8, tol_abs=1e-8), tol=1e-8)
+    out["c5_newton_x"], out["c5_newton_its"] = x, rep.iterations
+    out["c5_newton_inner"] = np.array(rep.inner_iterations)
+    save("configs_reduced", **out)
+
+
+if __name__ == "__main__" and "--configs" in sys.argv:
+    configs_reduced()

@@ -130,3 +130,47 @@ def test_c2_small_pfasst_reference_gmres_node_solves(golden, monkeypatch):
     x, rep = PF.pfasst_run(hier, g["u0"], 8, 4, tol_rel=1e-9, tol_abs=1e-9)
     assert rep.inner_iterations == g["PF_P4_inner"].tolist()
     assert per_node_rel(x, g["PF_P4_x"], (8, 3, 225)) < 1e-10
+
+
+def test_reduced_baseline_configs_on_device(golden):
+    """C3/C4/C5 at reduced size on the GPU path vs the real reference's fixtures."""
+    g = golden("configs_reduced")
+    # C3: Newton + STMG (Fisher) and PFASST IMEX
+    cfg = pd.baseline_config("C3", n=16, Nt=8)
+    ops = pd.fd_space(cfg.spec)
+    s = pd.assemble_system(pd.make_tableau(3), ops, pd.TimeGrid(cfg.Nt, cfg.T), cfg.gamma,
+                           cfg.u0(), reaction_kind="fisher")
+    h = pd.build_hierarchy(s, "STMG", 2, 3)
+    x, rep = pd.newton_solve(s, pd.mg_linear_solver(h, tol_rel=1e-9, tol_abs=1e-9), tol=1e-9)
+    assert rep.iterations == int(g["c3_newton_its"])
+    assert rep.inner_iterations == g["c3_newton_inner"].tolist()
+    assert per_node_rel(x, g["c3_newton_x"], (8, 3, 256)) < 1e-10
+    hier = PF.build_pfasst_hierarchy(3, ops.mesh, pd.TimeGrid(cfg.Nt, cfg.T), cfg.gamma, L=2,
+                                     nu=1, mode="imex", space=ops, M_coarse=2,
+                                     reaction_kind="fisher")
+    x, rep = PF.pfasst_run(hier, cfg.u0(), cfg.Nt, 4, tol_rel=1e-9, tol_abs=1e-9)
+    assert rep.inner_iterations == g["c3_pf_inner"].tolist()
+    assert per_node_rel(x, g["c3_pf_x"], (8, 3, 256)) < 1e-10
+    # C4: 3D PFASST M=5 / coarse 3 and SMG
+    cfg = pd.baseline_config("C4", n=7, Nt=8)
+    ops = pd.fd_space(cfg.spec)
+    hier = PF.build_pfasst_hierarchy(5, ops.mesh, pd.TimeGrid(cfg.Nt, cfg.T), 0.0, L=2, nu=1,
+                                     space=ops, M_coarse=3)
+    x, rep = PF.pfasst_run(hier, cfg.u0(), cfg.Nt, 4, tol_rel=1e-9, tol_abs=1e-9)
+    assert rep.inner_iterations == g["c4_pf_inner"].tolist()
+    assert per_node_rel(x, g["c4_pf_x"], (8, 5, 343)) < 1e-10
+    s = pd.assemble_system(pd.make_tableau(5), ops, pd.TimeGrid(cfg.Nt, cfg.T), 0.0, cfg.u0())
+    h = pd.build_hierarchy(s, "SMG", 2, 3, partitions=2)
+    x, rep = h.solve(s.rhs(), tol_rel=1e-10, tol_abs=1e-10)
+    assert rep.iterations == int(g["c4_smg_its"])
+    assert per_node_rel(x, g["c4_smg_x"], (8, 5, 343)) < 1e-10
+    # C5: 3D periodic cubic Newton + STMG
+    cfg = pd.baseline_config("C5", n=8, Nt=4)
+    ops = pd.fd_space(cfg.spec)
+    s = pd.assemble_system(pd.make_tableau(3), ops, pd.TimeGrid(cfg.Nt, cfg.T), cfg.gamma,
+                           cfg.u0())
+    h = pd.build_hierarchy(s, "STMG", 2, 3)
+    x, rep = pd.newton_solve(s, pd.mg_linear_solver(h, tol_rel=1e-8, tol_abs=1e-8), tol=1e-8)
+    assert rep.iterations == int(g["c5_newton_its"])
+    assert rep.inner_iterations == g["c5_newton_inner"].tolist()
+    assert per_node_rel(x, g["c5_newton_x"], (4, 3, 512)) < 1e-10

@@ -266,3 +266,39 @@ def test_reduction_order_floor(golden):
     assert worst_floor < 1e-11
     assert worst_strict > 1e-13  # nonzero: the floor is a property of the reference itself
     print(f"reduction-order floor: strict {worst_strict:.2e}, floored {worst_floor:.2e}")
+
+
+def test_reduced_baseline_configs_match_reference(golden):
+    """C3 (2D periodic Fisher: Newton+STMG, PFASST IMEX), C4 (3D PFASST M=5/3, SMG),
+    C5 (3D periodic cubic Newton+STMG) at reduced sizes vs the real reference."""
+    g = golden("configs_reduced")
+    # C3
+    cfg = PB.baseline_config("C3", n=16, Nt=8)
+    np.testing.assert_array_equal(cfg.u0(), g["c3_u0"])
+    ops = PB.fd_space(cfg.spec)
+    s = O.OSystem(O.tableau(3), ops.Kh, ops.lumped_diagonal, cfg.Nt, cfg.T, cfg.gamma, cfg.u0(),
+                  reaction="fisher")
+    mg = fd_oracle_hierarchy(s, cfg.spec, "STMG", 2, 3, 1)
+    x, rep = O.newton(s, O.mg_newton_solver(mg), tol=1e-9)
+    assert rep.iterations == int(g["c3_newton_its"])
+    assert rep.inner_iterations == g["c3_newton_inner"].tolist()
+    assert per_node_rel(x, g["c3_newton_x"], (8, 3, 256)) < 1e-10
+    levels, trs = fd_oracle_pfasst(cfg.spec, 3, 2, cfg.dt, cfg.gamma, "imex", "fisher")
+    x, rep = O.pfasst(levels, trs, 1, cfg.u0(), cfg.Nt, 4, tol_rel=1e-9, tol_abs=1e-9)
+    assert rep.inner_iterations == g["c3_pf_inner"].tolist()
+    assert per_node_rel(x, g["c3_pf_x"], (8, 3, 256)) < 1e-10
+    # C4
+    cfg = PB.baseline_config("C4", n=7, Nt=8)
+    levels, trs = fd_oracle_pfasst(cfg.spec, 5, 3, cfg.dt, 0.0)
+    x, rep = O.pfasst(levels, trs, 1, cfg.u0(), cfg.Nt, 4, tol_rel=1e-9, tol_abs=1e-9)
+    assert rep.inner_iterations == g["c4_pf_inner"].tolist()
+    assert per_node_rel(x, g["c4_pf_x"], (8, 5, 343)) < 1e-10
+    # C5
+    cfg = PB.baseline_config("C5", n=8, Nt=4)
+    ops = PB.fd_space(cfg.spec)
+    s = O.OSystem(O.tableau(3), ops.Kh, ops.lumped_diagonal, cfg.Nt, cfg.T, cfg.gamma, cfg.u0())
+    mg = fd_oracle_hierarchy(s, cfg.spec, "STMG", 2, 3, 1)
+    x, rep = O.newton(s, O.mg_newton_solver(mg, 1e-8, 1e-8), tol=1e-8)
+    assert rep.iterations == int(g["c5_newton_its"])
+    assert rep.inner_iterations == g["c5_newton_inner"].tolist()
+    assert per_node_rel(x, g["c5_newton_x"], (4, 3, 512)) < 1e-10
