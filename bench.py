@@ -201,13 +201,18 @@ def run_b200(args):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = lib.pd_launch_count()
     cycles = 0
+    ncu_region = bool(os.environ.get("PD_NCU_REGION"))  # ncu --profile-from-start off
     with ClockSampler(local) as clk:
+        if ncu_region:
+            torch.cuda.profiler.start()
         ev0.record()
         for _ in range(args.steps):
             rep = one_solve()
             cycles += rep.iterations
         ev1.record()
         torch.cuda.synchronize()
+        if ncu_region:
+            torch.cuda.profiler.stop()
     if dist:
         dist.barrier()
     launches = lib.pd_launch_count() - launches0

@@ -118,6 +118,10 @@ struct Ilu0 {
     DevBuf<int> ep;                 // device-resident sweep epoch (factorization)
     DevBuf<double> scratch;         // lower-sweep output, kept armed with the pending sentinel
     int nlevels_lo = 0, nlevels_up = 0;
+    // level-ordered copies of each sweep's entries (task t = t-th row in level order)
+    DevBuf<int64_t> tp_lo, tp_up;
+    DevBuf<int32_t> tcol_lo, tcol_up;
+    DevBuf<double> tval_lo, tval_up, tdiag;
     std::vector<std::pair<int64_t, int64_t>> ranges;
     const Csr& pat() const { return use_masked ? masked : *pattern; }
 };

@@ -468,11 +468,11 @@ __device__ __forceinline__ double accumulate_polling(double s, const int32_t* __
 }
 
 // lower: y_i = b_i - sum_{p < diag} L_p y_col (unit diagonal), linalg.py:104-108
-__global__ void k_trsv_lower(int64_t n, const int64_t* __restrict__ rp,
-                             const int32_t* __restrict__ ci, const double* __restrict__ fac,
-                             const int64_t* __restrict__ diag, const int32_t* __restrict__ order,
-                             const double* __restrict__ b, double* y, double* x_rearm,
-                             unsigned long long* counter, const int* guard, int want) {
+__global__ void k_trsv_lower(int64_t n, const int64_t* __restrict__ lp,
+                             const int32_t* __restrict__ lcol, const double* __restrict__ lval,
+                             const int32_t* __restrict__ order, const double* __restrict__ b,
+                             double* y, double* x_rearm, unsigned long long* counter,
+                             const int* guard, int want) {
     if (guard_off(guard, want)) return;
     for (;;) {
         int64_t base = fetch_batch(counter);
@@ -480,7 +480,7 @@ __global__ void k_trsv_lower(int64_t n, const int64_t* __restrict__ rp,
         int64_t t = base + threadIdx.x;
         if (t < n) {
             const int64_t i = order[t];
-            const double s = accumulate_polling(b[i], ci, fac, y, rp[i], diag[i]);
+            const double s = accumulate_polling(b[i], lcol, lval, y, lp[t], lp[t + 1]);
             st_pending(x_rearm + i);
             st_strong(y + i, s);
         }
@@ -488,9 +488,9 @@ __global__ void k_trsv_lower(int64_t n, const int64_t* __restrict__ rp,
 }
 
 // upper: x_i = (y_i - sum_{p > diag} U_p x_col) / U_diag, linalg.py:109-113
-__global__ void k_trsv_upper(int64_t n, const int64_t* __restrict__ rp,
-                             const int32_t* __restrict__ ci, const double* __restrict__ fac,
-                             const int64_t* __restrict__ diag, const int32_t* __restrict__ order,
+__global__ void k_trsv_upper(int64_t n, const int64_t* __restrict__ up,
+                             const int32_t* __restrict__ ucol, const double* __restrict__ uval,
+                             const double* __restrict__ udiag, const int32_t* __restrict__ order,
                              double* y, double* x, unsigned long long* counter, const int* guard,
                              int want) {
     if (guard_off(guard, want)) return;
@@ -500,12 +500,40 @@ __global__ void k_trsv_upper(int64_t n, const int64_t* __restrict__ rp,
         int64_t t = base + threadIdx.x;
         if (t < n) {
             const int64_t i = order[t];
-            const int64_t d = diag[i];
             const double yi = y[i];
-            const double s = accumulate_polling(yi, ci, fac, x, d + 1, rp[i + 1]);
+            const double s = accumulate_polling(yi, ucol, uval, x, up[t], up[t + 1]);
             st_pending(y + i);  // re-arm the lower scratch for the next solve
-            st_strong(x + i, s / fac[d]);
+            st_strong(x + i, s / udiag[t]);
         }
+    }
+}
+
+// Level-ordered factor layout: the entries each sweep needs, stored task by
+// task in the sweep's level order, so consecutive threads stream consecutive
+// memory instead of gathering scattered natural-order CSR rows.
+__global__ void k_task_counts(int64_t n, const int64_t* rp, const int64_t* diag,
+                              const int32_t* order, int upper, int64_t* cnt) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = order[t];
+        cnt[t + 1] = upper ? rp[i + 1] - diag[i] - 1 : diag[i] - rp[i];
+    }
+}
+
+__global__ void k_task_gather(int64_t n, const int64_t* rp, const int32_t* ci, const double* fac,
+                              const int64_t* diag, const int32_t* order, int upper,
+                              const int64_t* tp, int32_t* tcol, double* tval, double* tdiag) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = order[t];
+        const int64_t d = diag[i];
+        const int64_t src = upper ? d + 1 : rp[i];
+        const int64_t cnt = tp[t + 1] - tp[t];
+        for (int64_t k = 0; k < cnt; ++k) {
+            tcol[tp[t] + k] = ci[src + k];
+            tval[tp[t] + k] = fac[src + k];
+        }
+        if (upper) tdiag[t] = fac[d];
     }
 }
 
@@ -614,6 +642,38 @@ std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks) {
     return f;
 }
 
+static void build_task_layout(Ctx& c, Ilu0& f) {
+    const Csr& P = f.pat();
+    const int64_t n = f.n;
+    for (int upper = 0; upper < 2; ++upper) {
+        DevBuf<int64_t>& tp = upper ? f.tp_up : f.tp_lo;
+        DevBuf<int32_t>& tcol = upper ? f.tcol_up : f.tcol_lo;
+        DevBuf<double>& tval = upper ? f.tval_up : f.tval_lo;
+        const int32_t* order = upper ? f.order_up.p : f.order_lo.p;
+        if (!tp.p) {  // pattern-only part, once per hierarchy
+            tp.alloc(n + 1);
+            PD_CUDA(cudaMemsetAsync(tp.p, 0, sizeof(int64_t), c.stream));
+            launch(k_task_counts, c.grid_for(n, BS), BS, 0, c.stream, n, P.rowptr.p, f.diag.p,
+                   order, upper, tp.p);
+            size_t tb = 0;
+            PD_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tb, tp.p, tp.p, n + 1, c.stream));
+            DevBuf<unsigned char> tmp(tb);
+            PD_CUDA(cub::DeviceScan::InclusiveSum(tmp.p, tb, tp.p, tp.p, n + 1, c.stream));
+            int64_t total = 0;
+            PD_CUDA(cudaMemcpyAsync(&total, tp.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                    c.stream));
+            PD_CUDA(cudaStreamSynchronize(c.stream));
+            tcol.alloc(std::max<int64_t>(total, 1));
+            tval.alloc(std::max<int64_t>(total, 1));
+            if (upper) f.tdiag.alloc(n);
+        }
+        launch(k_task_gather, c.grid_for(n, BS), BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p,
+               f.diag.p, order, upper, tp.p, tcol.p, tval.p, upper ? f.tdiag.p : (double*)nullptr);
+        PD_LAUNCH_CHECK();
+    }
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+}
+
 void ilu0_refactor(Ctx& c, Ilu0& f) {
     const Csr& P = f.pat();
     const int64_t n = f.n;
@@ -647,6 +707,7 @@ void ilu0_refactor(Ctx& c, Ilu0& f) {
         }
         throw SolverError("zero pivot in ILU(0) at row " + std::to_string(row), row);
     }
+    build_task_layout(c, f);
 }
 
 static void configure_polling_once() {
@@ -667,10 +728,10 @@ void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, i
     const Csr& P = f.pat();
     const int g = c.grid_for(n, BS, sweep_blocks_per_sm());
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, guard, want);
-    launch(k_trsv_lower, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
+    launch(k_trsv_lower, g, BS, 0, c.stream, n, f.tp_lo.p, f.tcol_lo.p, f.tval_lo.p,
            f.order_lo.p, b, f.scratch.p, x, f.counter.p, guard, want);
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, guard, want);
-    launch(k_trsv_upper, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
+    launch(k_trsv_upper, g, BS, 0, c.stream, n, f.tp_up.p, f.tcol_up.p, f.tval_up.p, f.tdiag.p,
            f.order_up.p, f.scratch.p, x, f.counter.p, guard, want);
     PD_LAUNCH_CHECK();
 }

@@ -14,6 +14,8 @@ struct StOp {
     double Kq[kStMaxM * kStMaxM], Mq[kStMaxM * kStMaxM], l0[kStMaxM];
     std::unique_ptr<Csr> Kh;
     DevBuf<double> mh;
+    DevBuf<double> coef;  // one time block of Aqh values, [m][m'][p of Kh] (L2-resident)
+    int64_t nnzK = 0;
     StOp(Ctx& c, int64_t Nt, int M, int64_t S, const double* Kq, const double* Mq,
          const double* l0, double dt, const Csr& Kh, const double* mh_host);
     int64_t size() const { return Nt * M * S; }
