@@ -116,9 +116,14 @@ int pd_stop_residual(void *op, const double *u, const double *rhs, double *out, 
 
 /* ---- SDC / PFASST building blocks, batched over W workers of a window
  *      (pfasst.py:60-303).  State layout: U[W][M][S], U0[W][S], tau[W][M][S]. */
+/* spec_* (optional, NULL to skip): Kh = spec_s * sum over spec_dim axes of T,
+ * T = Phi diag(spec_mu) Phi^T (spec_n x spec_n, Phi row-major, orthonormal);
+ * enables the exact spectral node solver for structured FD operators. */
 int pd_sdc_level_create(void *ctx, void *Kh, const double *mh_host, int M, const double *Q,
                         const double *QDI, const double *QDE, double dt, double gamma,
-                        int reaction, int imex, int max_workers, void **lvl_out); /* SdcLevel */
+                        int reaction, int imex, int max_workers, const double *spec_phi,
+                        const double *spec_mu, int spec_dim, int64_t spec_n, double spec_s,
+                        void **lvl_out); /* SdcLevel */
 int pd_sdc_level_destroy(void *lvl);
 int pd_sdc_sweep(void *lvl, double *U, const double *U0, const double *tau, int W); /* :155-200 */
 int pd_sdc_residual(void *lvl, const double *U, const double *U0, const double *tau, int W,

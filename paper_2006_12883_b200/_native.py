@@ -74,7 +74,7 @@ _SIGNATURES = {
     "pd_axpy_to": (_int, [_vp, _vp, _vp, _vp, _dbl, _i64]),
     "pd_norm": (_int, [_vp, _vp, _i64, ctypes.POINTER(_dbl)]),
     "pd_sdc_level_create": (_int, [_vp, _vp, _vp, _int, _vp, _vp, _vp, _dbl, _dbl, _int, _int,
-                                   _int, ctypes.POINTER(_vp)]),
+                                   _int, _vp, _vp, _int, _i64, _dbl, ctypes.POINTER(_vp)]),
     "pd_sdc_level_destroy": (_int, [_vp]),
     "pd_sdc_sweep": (_int, [_vp, _vp, _vp, _vp, _int]),
     "pd_sdc_residual": (_int, [_vp, _vp, _vp, _vp, _int, _vp]),

@@ -204,6 +204,11 @@ struct SdcLevelDev {
     std::vector<std::unique_ptr<DenseLU>> dlu;
     // ILU(0) of each node operator (solver 2: the reference's GMRES path)
     std::vector<std::unique_ptr<Ilu0>> ilu;
+    // spectral inverse (solver 3): Kh = s * sum_axes T_axis, T = Phi diag(mu) Phi^T
+    int spec_dim = 0;
+    int64_t spec_n = 0;
+    double spec_s = 0.0, spec_mh = 0.0;
+    DevBuf<double> phi, mu, spec_tmp;
     // scratch
     DevBuf<double> fi_old, fe_old, f_tot, base, fi_new, fe_new, rhs, bvec, x, r, tmp;
     DevBuf<double> partials, beta0, thr, beta, lowest;
@@ -468,6 +473,40 @@ __global__ void k_node_newton_tri(const int64_t* __restrict__ rp, const int32_t*
     atomicOr(err, 4);
 }
 
+// Mode product along one axis of W stacked n^dim grids (C order, last axis
+// fastest): out[.., a, ..] = sum_i Mat(a, i) in[.., i, ..] with Mat = Phi^T
+// (transpose=1: forward transform) or Phi (transpose=0: back transform).
+__global__ void k_mode_apply(const double* __restrict__ in, double* __restrict__ out,
+                             int64_t total, int64_t n, int64_t stride,
+                             const double* __restrict__ phi, int transpose) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = (t / stride) % n;
+        const double* base = in + (t - a * stride);
+        double acc = 0.0;
+        for (int64_t i = 0; i < n; ++i) {
+            const double mv = transpose ? phi[i * n + a] : phi[a * n + i];
+            acc = fma(mv, base[i * stride], acc);
+        }
+        out[t] = acc;
+    }
+}
+
+// z /= (mh + q*s*sum_axes mu_{i_axis})  (eigenvalues of the node operator)
+__global__ void k_spec_scale(double* z, int64_t total, int64_t n, int dim,
+                             const double* __restrict__ mu, double mh, double qs) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = t;
+        double lam = 0.0;
+        for (int d = 0; d < dim; ++d) {
+            lam += mu[r % n];
+            r /= n;
+        }
+        z[t] = z[t] / fma(qs, lam, mh);
+    }
+}
+
 Small small_from(const double* h, int r, int cols) {
     Small s;
     std::memset(&s, 0, sizeof(s));
@@ -489,6 +528,33 @@ static void bnorm(SdcLevelDev& L, const double* x, int64_t n, int64_t stride, in
 
 static void node_apply_inverse(SdcLevelDev& L, int m, const double* r, double* z, int W) {
     Ctx& c = L.c;
+    if (L.solver == 3) {
+        // z = Phi^(x)dim diag(1/lambda) Phi^T(x)dim r  (exact inverse up to rounding);
+        // ping-pong between spec_tmp and z (r is never written)
+        const int64_t total = (int64_t)W * L.S;
+        double* T1 = L.spec_tmp.p;
+        double* T2 = z;
+        const double* src = r;
+        int64_t stride = 1;
+        for (int d = 0; d < L.spec_dim; ++d, stride *= L.spec_n) {
+            double* dst = (src == T1) ? T2 : T1;
+            launch(k_mode_apply, c.grid_for(total, TB), TB, 0, c.stream, src, dst, total,
+                   L.spec_n, stride, (const double*)L.phi.p, 1);
+            src = dst;
+        }
+        launch(k_spec_scale, c.grid_for(total, TB), TB, 0, c.stream, const_cast<double*>(src),
+               total, L.spec_n, L.spec_dim, (const double*)L.mu.p, L.spec_mh,
+               L.dt * L.QDI.a[m * L.M + m] * L.spec_s);
+        stride = 1;
+        for (int d = 0; d < L.spec_dim; ++d, stride *= L.spec_n) {
+            double* dst = (src == T1) ? T2 : T1;
+            launch(k_mode_apply, c.grid_for(total, TB), TB, 0, c.stream, src, dst, total,
+                   L.spec_n, stride, (const double*)L.phi.p, 0);
+            src = dst;
+        }
+        if (src != z) vec_copy(c, z, src, total);
+        return;
+    }
     if (L.solver == 0) {
         const int64_t S = L.S;
         launch(k_tri_solve, (W + 63) / 64, 64, 0, c.stream, L.tl.p + m * S, L.tu.p + m * S,
@@ -646,7 +712,9 @@ extern "C" {
 
 int pd_sdc_level_create(void* ctx, void* Kh, const double* mh_host, int M, const double* Q,
                         const double* QDI, const double* QDE, double dt, double gamma,
-                        int reaction, int imex, int max_workers, void** out) {
+                        int reaction, int imex, int max_workers, const double* spec_phi,
+                        const double* spec_mu, int spec_dim, int64_t spec_n, double spec_s,
+                        void** out) {
     return guarded_sdc([&] {
         auto& c = *static_cast<pd::Ctx*>(ctx);
         auto* K = static_cast<pd::Csr*>(Kh);
@@ -696,7 +764,26 @@ int pd_sdc_level_create(void* ctx, void* Kh, const double* mh_host, int M, const
         }
         const char* force = getenv("PD_NODE_SOLVER");
         const bool want_gmres = force && std::string(force) == "gmres";
-        L->solver = tri ? 0 : ((S <= 4096 && !want_gmres) ? 1 : 2);
+        const bool spectral = spec_phi && spec_mu && spec_dim >= 1 && !want_gmres;
+        L->solver = tri ? 0 : (spectral ? 3 : ((S <= 4096 && !want_gmres) ? 1 : 2));
+        if (L->solver == 3) {
+            int64_t sz = 1;
+            for (int d = 0; d < spec_dim; ++d) sz *= spec_n;
+            if (sz != S) throw pd::ConfigError("spectral description does not match Kh");
+            for (int64_t i = 0; i < S; ++i)
+                if (mh_host[i] != mh_host[0])
+                    throw pd::ConfigError("spectral node solver needs a constant mass");
+            L->spec_dim = spec_dim;
+            L->spec_n = spec_n;
+            L->spec_s = spec_s;
+            L->spec_mh = mh_host[0];
+            L->phi.alloc(spec_n * spec_n);
+            L->mu.alloc(spec_n);
+            PD_CUDA(cudaMemcpy(L->phi.p, spec_phi, spec_n * spec_n * sizeof(double),
+                               cudaMemcpyHostToDevice));
+            PD_CUDA(cudaMemcpy(L->mu.p, spec_mu, spec_n * sizeof(double), cudaMemcpyHostToDevice));
+            L->spec_tmp.alloc((int64_t)max_workers * S);
+        }
         for (int m = 0; m < M; ++m) {
             const double q = dt * QDI[m * M + m];
             std::vector<double> av(K->nnz);
@@ -717,6 +804,8 @@ int pd_sdc_level_create(void* ctx, void* Kh, const double* mh_host, int M, const
                            L->err.p);
         } else if (L->solver == 2) {
             for (int m = 0; m < M; ++m) L->ilu.push_back(pd::ilu0_create(c, *L->Am[m], 1));
+        } else if (L->solver == 3) {
+            // nothing to factor: the inverse is applied spectrally
         } else {
             for (int m = 0; m < M; ++m) L->dlu.push_back(pd::dense_lu_from_csr(c, *L->Am[m]));
             static bool attr = false;

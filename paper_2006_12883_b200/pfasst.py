@@ -104,6 +104,7 @@ class SdcLevel:
         Kd = DeviceCsr(self.Kh, self.ctx)
         mh = _host(self.mh)
         T = self.tableau
+        phi, mu, sdim, sn, ss = self._spectral()
         h = ctypes.c_void_p()
         N.call("pd_sdc_level_create", self.ctx.handle, Kd.handle,
                mh.ctypes.data_as(ctypes.c_void_p), self.M,
@@ -111,9 +112,30 @@ class SdcLevel:
                _host(T.QDeltaImplicit).ctypes.data_as(ctypes.c_void_p),
                _host(T.QDeltaExplicit).ctypes.data_as(ctypes.c_void_p), self.dt, self.gamma,
                _REACTION[self.reaction_kind], 1 if self.mode == "imex" else 0, int(workers),
+               phi.ctypes.data_as(ctypes.c_void_p) if phi is not None else None,
+               mu.ctypes.data_as(ctypes.c_void_p) if mu is not None else None, sdim, sn, ss,
                ctypes.byref(h))
         self._dev, self._cap = h, workers
         return h
+
+    def _spectral(self):
+        """Eigen-description of a structured FD Kh (enables the spectral node solver).
+
+        Kh = s * sum_axes T (problems.stencil_matrix) with the 1D second
+        difference T = Phi diag(mu) Phi^T (orthonormal, numpy eigh — host M x M
+        scale setup).  The device applies (mh + q Kh)^{-1} exactly up to
+        rounding and keeps the reference's refinement/residual test on the CSR.
+        """
+        spec = getattr(self.space, "stencil", None)
+        if spec is None or spec.dim < 2:
+            return None, None, 0, 0, 0.0
+        from .problems import _second_difference
+
+        Tm = _second_difference(spec.n, spec.bc).toarray()
+        mu, phi = np.linalg.eigh(Tm)
+        s = spec.coef * spec.h ** spec.dim / spec.h ** 2
+        return (np.ascontiguousarray(phi, dtype=np.float64),
+                np.ascontiguousarray(mu, dtype=np.float64), spec.dim, spec.n, float(s))
 
     def _release(self):
         if self._dev is not None:
