@@ -126,6 +126,8 @@ int pd_sdc_level_create(void *ctx, void *Kh, const double *mh_host, int M, const
                         void **lvl_out); /* SdcLevel */
 int pd_sdc_level_destroy(void *lvl);
 int pd_sdc_sweep(void *lvl, double *U, const double *U0, const double *tau, int W); /* :155-200 */
+int pd_sdc_chain(void *lvl, double *U, double *U0, const double *tau, int W, const double *u0c,
+                 int nu); /* coarsest serial chain, pfasst.py:441-455 */
 int pd_sdc_residual(void *lvl, const double *U, const double *U0, const double *tau, int W,
                     double *res_dev);                            /* :107-115, per worker */
 int pd_sdc_coll_op(void *lvl, const double *U, double *out, int W); /* C(u) = u - dt Q F(u) */

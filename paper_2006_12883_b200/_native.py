@@ -77,6 +77,7 @@ _SIGNATURES = {
                                    _int, _vp, _vp, _int, _i64, _dbl, ctypes.POINTER(_vp)]),
     "pd_sdc_level_destroy": (_int, [_vp]),
     "pd_sdc_sweep": (_int, [_vp, _vp, _vp, _vp, _int]),
+    "pd_sdc_chain": (_int, [_vp, _vp, _vp, _vp, _int, _vp, _int]),
     "pd_sdc_residual": (_int, [_vp, _vp, _vp, _vp, _int, _vp]),
     "pd_sdc_coll_op": (_int, [_vp, _vp, _vp, _int]),
     "pd_sdc_errors": (_int, [_vp, ctypes.POINTER(_int)]),

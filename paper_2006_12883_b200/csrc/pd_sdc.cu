@@ -198,6 +198,7 @@ struct SdcLevelDev {
     DevBuf<double> mh;
     // node operators A_m = diag(mh) + dt*qdi[m][m]*Kh
     std::vector<std::unique_ptr<Csr>> Am;
+    DevBuf<double> Aval;  // all node operators' values, [m][nnz] (same pattern as Kh)
     // tridiagonal factors (solver 0): lower l (M x S), pivots u (M x S), super c (M x S)
     DevBuf<double> tl, tu, tc;
     // dense factors (solver 1)
@@ -412,13 +413,13 @@ __global__ void k_terminal(const double* U, double* out, int W, int M, int64_t S
 // (tridiagonal Thomas = the ILU(0) the reference preconditions with, which
 // makes its inner GMRES converge in one step).  Stops at
 // ||g|| <= 1e-12 max(1, ||b||); 50 steps without convergence -> error bit 4.
-__global__ void k_node_newton_tri(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
-                                  const double* __restrict__ kv, const double* __restrict__ mh,
-                                  int64_t S, double q, double gamma, int kind,
-                                  const double* __restrict__ b, double* x, double* gbuf,
-                                  double* lbuf, double* ubuf, int W, int* err) {
-    const int w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w >= W) return;
+__device__ void node_newton_tri_worker(const int64_t* __restrict__ rp,
+                                       const int32_t* __restrict__ ci,
+                                       const double* __restrict__ kv,
+                                       const double* __restrict__ mh, int64_t S, double q,
+                                       double gamma, int kind, const double* __restrict__ b,
+                                       double* x, double* gbuf, double* lbuf, double* ubuf, int w,
+                                       int* err) {
     const double* bw = b + (int64_t)w * S;
     double* u = x + (int64_t)w * S;
     double* g = gbuf + (int64_t)w * S;
@@ -471,6 +472,16 @@ __global__ void k_node_newton_tri(const int64_t* __restrict__ rp, const int32_t*
         }
     }
     atomicOr(err, 4);
+}
+
+__global__ void k_node_newton_tri(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ kv, const double* __restrict__ mh,
+                                  int64_t S, double q, double gamma, int kind,
+                                  const double* __restrict__ b, double* x, double* gbuf,
+                                  double* lbuf, double* ubuf, int W, int* err) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w >= W) return;
+    node_newton_tri_worker(rp, ci, kv, mh, S, q, gamma, kind, b, x, gbuf, lbuf, ubuf, w, err);
 }
 
 // Mode product along one axis of W stacked n^dim grids (C order, last axis
@@ -603,6 +614,228 @@ static void node_solve(SdcLevelDev& L, int m, const double* b, double* x, int W,
     launch(k_any_open, (W + 127) / 128, 128, 0, c.stream, L.done.p, W, L.err.p);
 }
 
+// ---------------------------------------------------------------- fused small-S sweep
+// One warp owns one worker's whole sweep (pfasst.py:155-200) for a tridiagonal
+// Kh: f evaluations, the base, and every node solve (reference-style
+// refinement with the exact Thomas factors, or the implicit Newton) without a
+// kernel launch per node.  Used for the batched fine sweep (grid over
+// workers) and for the coarsest serial chain (one warp walks the workers).
+struct FusedSweep {
+    int64_t S;
+    int M, imex, kind;
+    double dt, gamma;
+    Small A1, A2, QDI, QDE;
+    const int64_t *krp, *arp;
+    const int32_t *kci, *aci;
+    const double *kv, *av;  // Kh and the node operators (values [m][nnz])
+    int64_t annz;
+    const double *mh, *tl, *tu, *tc;
+    double *fi_old, *fe_old, *base, *fi_new, *fe_new, *r, *x, *b;
+    int* err;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__device__ void fused_sweep_worker(const FusedSweep& F, double* U, const double* U0,
+                                   const double* tau, int w, int lane) {
+    const int64_t S = F.S;
+    const int M = F.M;
+    const int64_t MS = (int64_t)M * S;
+    double* fio = F.fi_old + w * MS;
+    double* feo = F.fe_old + w * MS;
+    double* bas = F.base + w * MS;
+    double* fin = F.fi_new + w * MS;
+    double* fen = F.fe_new + w * MS;
+    double* r = F.r + w * S;
+    double* x = F.x + w * S;
+    double* b = F.b + w * S;
+    const bool imex = F.imex && F.gamma != 0.0;
+    // f(U): fi = -Kh U / mh, fe = -gamma r(U)
+    for (int64_t idx = lane; idx < MS; idx += 32) {
+        const int64_t j = idx % S;
+        const double* um = U + (idx - j);
+        double sacc = 0.0;
+        for (int64_t p = F.krp[j]; p < F.krp[j + 1]; ++p) sacc = add(sacc, mul(F.kv[p], um[F.kci[p]]));
+        fio[idx] = (-sacc) / F.mh[j];
+        feo[idx] = F.gamma == 0.0 ? 0.0 : mul(-F.gamma, react(F.kind, U[idx]));
+    }
+    __syncwarp();
+    // base = U0 + dt*(A1 f1 (+ A2 f2)) (+ tau)
+    bool bad = false;
+    for (int64_t idx = lane; idx < MS; idx += 32) {
+        const int64_t j = idx % S;
+        const int m = (int)(idx / S);
+        double acc = 0.0, acc2 = 0.0;
+        for (int k = 0; k < M; ++k) {
+            const double f1 = imex ? fio[k * S + j] : add(fio[k * S + j], feo[k * S + j]);
+            acc = add(acc, mul(F.A1.a[m * M + k], f1));
+            if (imex) acc2 = add(acc2, mul(F.A2.a[m * M + k], feo[k * S + j]));
+        }
+        if (imex) acc = add(acc, acc2);
+        double v = add(U0[j], mul(F.dt, acc));
+        if (tau) v = add(v, tau[idx]);
+        bas[idx] = v;
+        if (!isfinite(v)) bad = true;
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(F.err, 1);
+    __syncwarp();
+    for (int m = 0; m < M; ++m) {
+        for (int64_t j = lane; j < S; j += 32) {
+            double rh = bas[m * S + j];
+            for (int k = 0; k < m; ++k) {
+                rh = add(rh, mul(mul(F.dt, F.QDI.a[m * M + k]), fin[k * S + j]));
+                if (imex) rh = add(rh, mul(mul(F.dt, F.QDE.a[m * M + k]), fen[k * S + j]));
+            }
+            b[j] = mul(F.mh[j], rh);
+            x[j] = U[m * S + j];
+        }
+        __syncwarp();
+        if (F.gamma != 0.0 && !imex) {
+            if (lane == 0)
+                node_newton_tri_worker(F.krp, F.kci, F.kv, F.mh, S, mul(F.dt, F.QDI.a[m * M + m]),
+                                       F.gamma, F.kind, b, x, r, fio, feo, 0, F.err);
+            __syncwarp();
+        } else {
+            const double* am = F.av + (int64_t)m * F.annz;
+            const double* tl = F.tl + (int64_t)m * S;
+            const double* tu = F.tu + (int64_t)m * S;
+            const double* tc = F.tc + (int64_t)m * S;
+            double bn = 0.0, beta = 0.0;
+            for (int64_t j = lane; j < S; j += 32) {
+                double sacc = 0.0;
+                for (int64_t p = F.arp[j]; p < F.arp[j + 1]; ++p) sacc = add(sacc, mul(am[p], x[F.aci[p]]));
+                r[j] = sub(b[j], sacc);
+                bn = fma(b[j], b[j], bn);
+                beta = fma(r[j], r[j], beta);
+            }
+            bn = sqrt(warp_sum(bn));
+            beta = sqrt(warp_sum(beta));
+            const double thr = fmax(mul(1e-13, fmax(1.0, bn)), mul(1e-13, beta));
+            double lowest = beta;
+            bool done = !(beta > thr);
+            for (int round = 0; round < 3 && !done; ++round) {
+                __syncwarp();
+                if (lane == 0) {  // z = U^{-1} L^{-1} r (Thomas = ILU(0) of the tridiagonal)
+                    double y = r[0];
+                    r[0] = y;
+                    for (int64_t i = 1; i < S; ++i) {
+                        y = sub(r[i], mul(tl[i], y));
+                        r[i] = y;
+                    }
+                    double xn = r[S - 1] / tu[S - 1];
+                    r[S - 1] = xn;
+                    for (int64_t i = S - 2; i >= 0; --i) {
+                        xn = sub(r[i], mul(tc[i], xn)) / tu[i];
+                        r[i] = xn;
+                    }
+                }
+                __syncwarp();
+                for (int64_t j = lane; j < S; j += 32) x[j] = add(x[j], r[j]);
+                __syncwarp();
+                beta = 0.0;
+                for (int64_t j = lane; j < S; j += 32) {
+                    double sacc = 0.0;
+                    for (int64_t p = F.arp[j]; p < F.arp[j + 1]; ++p)
+                        sacc = add(sacc, mul(am[p], x[F.aci[p]]));
+                    r[j] = sub(b[j], sacc);
+                    beta = fma(r[j], r[j], beta);
+                }
+                beta = sqrt(warp_sum(beta));
+                if (!isfinite(beta) || beta > mul(10.0, lowest)) {
+                    if (lane == 0) atomicOr(F.err, 4);
+                    done = true;
+                    break;
+                }
+                lowest = fmin(lowest, beta);
+                done = !(beta > thr);
+            }
+            if (!done && lane == 0) atomicOr(F.err, 8);
+            __syncwarp();
+        }
+        // U[m] = x ; f of the new node value
+        for (int64_t j = lane; j < S; j += 32) U[m * S + j] = x[j];
+        __syncwarp();
+        for (int64_t j = lane; j < S; j += 32) {
+            double sacc = 0.0;
+            for (int64_t p = F.krp[j]; p < F.krp[j + 1]; ++p) sacc = add(sacc, mul(F.kv[p], x[F.kci[p]]));
+            const double fdiff = (-sacc) / F.mh[j];
+            const double freac = F.gamma == 0.0 ? 0.0 : mul(-F.gamma, react(F.kind, x[j]));
+            fin[m * S + j] = imex ? fdiff : add(fdiff, freac);
+            fen[m * S + j] = freac;
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void k_fused_sweep(FusedSweep F, double* U, const double* U0, const double* tau,
+                              int W) {
+    const int w = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (w >= W) return;
+    const int64_t MS = (int64_t)F.M * F.S;
+    fused_sweep_worker(F, U + w * MS, U0 + (int64_t)w * F.S, tau ? tau + w * MS : nullptr, w,
+                       lane);
+}
+
+// coarsest serial chain (pfasst.py:441-455): worker w starts from worker w-1's
+// terminal of THIS iteration; one warp walks all workers
+__global__ void k_fused_chain(FusedSweep F, double* U, double* U0, const double* tau, int W,
+                              const double* u0c, int nu) {
+    const int lane = threadIdx.x & 31;
+    const int64_t S = F.S, MS = (int64_t)F.M * S;
+    for (int w = 0; w < W; ++w) {
+        double* U0w = U0 + (int64_t)w * S;
+        const double* src = w == 0 ? u0c : U + (int64_t)(w - 1) * MS + (F.M - 1) * S;
+        for (int64_t j = lane; j < S; j += 32) U0w[j] = src[j];
+        __syncwarp();
+        for (int k = 0; k < nu; ++k)
+            fused_sweep_worker(F, U + w * MS, U0w, tau ? tau + w * MS : nullptr, w, lane);
+    }
+}
+
+static FusedSweep fused_params(SdcLevelDev& L) {
+    FusedSweep F;
+    F.S = L.S;
+    F.M = L.M;
+    F.imex = L.imex;
+    F.kind = L.kind;
+    F.dt = L.dt;
+    F.gamma = L.gamma;
+    const bool imex = L.imex && L.gamma != 0.0;
+    F.A1 = L.A_imp;
+    F.A2 = L.A_exp;
+    (void)imex;
+    F.QDI = L.QDI;
+    F.QDE = L.QDE;
+    F.krp = L.Kh->rowptr.p;
+    F.kci = L.Kh->col.p;
+    F.kv = L.Kh->val.p;
+    F.arp = L.Am[0]->rowptr.p;
+    F.aci = L.Am[0]->col.p;
+    F.av = L.Aval.p;
+    F.annz = L.Am[0]->nnz;
+    F.mh = L.mh.p;
+    F.tl = L.tl.p;
+    F.tu = L.tu.p;
+    F.tc = L.tc.p;
+    F.fi_old = L.fi_old.p;
+    F.fe_old = L.fe_old.p;
+    F.base = L.base.p;
+    F.fi_new = L.fi_new.p;
+    F.fe_new = L.fe_new.p;
+    F.r = L.r.p;
+    F.x = L.x.p;
+    F.b = L.bvec.p;
+    F.err = L.err.p;
+    return F;
+}
+
+static bool fused_ok(const SdcLevelDev& L) { return L.solver == 0 && !getenv("PD_NO_FUSED_SWEEP"); }
+
 static void feval(SdcLevelDev& L, const double* U, double* fi, double* fe, int W, int nodes,
                   int64_t stride_w) {
     // fi = -Kh U / mh ; fe = -gamma r(U) ; vectors: W*nodes of length S at stride S
@@ -624,6 +857,12 @@ void sdc_sweep(SdcLevelDev& L, double* U, const double* U0, const double* tau, i
     if (L.gamma != 0.0 && !imex && L.solver != 0)
         throw ConfigError("implicit-mode nonlinear node solves need a tridiagonal Kh on the "
                           "device (use mode='imex', the reference default for gamma > 0)");
+    if (fused_ok(L)) {
+        launch(k_fused_sweep, (unsigned)((W * 32 + 127) / 128), 128, 0, c.stream, fused_params(L),
+               U, U0, tau, W);
+        PD_LAUNCH_CHECK();
+        return;
+    }
     feval(L, U, L.fi_old.p, L.fe_old.p, W, M, 0);
     if (imex) {
         launch(k_sdc_base, c.grid_for(n, TB), TB, 0, c.stream, U0, L.fi_old.p, L.fe_old.p, tau,
@@ -792,6 +1031,10 @@ int pd_sdc_level_create(void* ctx, void* Kh, const double* mh_host, int M, const
                     av[p] = (ci[p] == i ? mh_host[i] : 0.0) + q * kv[p];
             L->Am.push_back(pd::csr_upload(c, S, S, K->nnz, rp.data(), ci.data(), av.data(), false));
         }
+        L->Aval.alloc((int64_t)M * std::max<int64_t>(K->nnz, 1));
+        for (int m = 0; m < M; ++m)
+            PD_CUDA(cudaMemcpy(L->Aval.p + (int64_t)m * K->nnz, L->Am[m]->val.p,
+                               K->nnz * sizeof(double), cudaMemcpyDeviceToDevice));
         L->err.alloc(1);
         PD_CUDA(cudaMemset(L->err.p, 0, sizeof(int)));
         if (tri) {
@@ -838,6 +1081,30 @@ int pd_sdc_level_destroy(void* lvl) {
 int pd_sdc_sweep(void* lvl, double* U, const double* U0, const double* tau, int W) {
     return guarded_sdc(
         [&] { pd::sdc_sweep(*static_cast<pd::SdcLevelDev*>(lvl), U, U0, tau, W); });
+}
+
+// coarsest serial chain over W workers: U0[0] = u0c, U0[w] = terminal of w-1,
+// nu sweeps each (pfasst.py:441-455)
+int pd_sdc_chain(void* lvl, double* U, double* U0, const double* tau, int W, const double* u0c,
+                 int nu) {
+    return guarded_sdc([&] {
+        auto& L = *static_cast<pd::SdcLevelDev*>(lvl);
+        pd::Ctx& c = L.c;
+        const int64_t S = L.S, MS = (int64_t)L.M * S;
+        if (pd::fused_ok(L)) {
+            pd::launch(pd::k_fused_chain, 1, 32, 0, c.stream, pd::fused_params(L), U, U0, tau, W,
+                       u0c, nu);
+            PD_LAUNCH_CHECK();
+            return;
+        }
+        for (int w = 0; w < W; ++w) {
+            const double* src = w == 0 ? u0c : U + (int64_t)(w - 1) * MS + (L.M - 1) * S;
+            PD_CUDA(cudaMemcpyAsync(U0 + (int64_t)w * S, src, S * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, c.stream));
+            for (int k = 0; k < nu; ++k)
+                pd::sdc_sweep(L, U + w * MS, U0 + (int64_t)w * S, tau ? tau + w * MS : nullptr, 1);
+        }
+    });
 }
 
 // per-worker ||U - U0 - dt Q F(U) - tau||_F into res (device, W doubles)

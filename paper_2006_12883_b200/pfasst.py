@@ -536,13 +536,8 @@ class GpuPfasstEngine:
         c = self.h.levels[-1]
         Mc, Sc = c.M, c.ndof
         U, U0, tau = self.U[-1], self.U0[-1], self.tau[-1]
-        for w in range(self.W):
-            if w == 0:
-                self._c("pd_scale", _vp(U0), _vp(u0c), 1.0, Sc)
-            else:
-                self._c("pd_terminal", _vp(U, (w - 1) * Mc * Sc), _vp(U0, w * Sc), 1, Mc, Sc)
-            for _ in range(self.h.nu):
-                c.sweep_dev(U, U0, tau, 1, w_off=w)
+        N.call("pd_sdc_chain", c.device(self.W), _vp(U), _vp(U0), _vp(tau), self.W, _vp(u0c),
+               int(self.h.nu))
         self._c("pd_terminal", _vp(U, (self.W - 1) * Mc * Sc), _vp(self.c_out), 1, Mc, Sc)
         return self.c_out
 
