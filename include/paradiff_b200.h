@@ -82,6 +82,17 @@ int pd_mg_level_matrix(void *mg, int level, void **csr_out); /* borrowed handle 
 int pd_mg_level_precond(void *mg, int level, void **ilu_out); /* borrowed ILU/block-Jacobi */
 int pd_mg_refactor(void *ctx, void *mg);                     /* after value updates */
 int pd_mg_set_fine_operator(void *mg, void *stop); /* takes ownership; NULL detaches */
+/* device Newton refresh (multigrid.py:224-241, §8(f)1): T[l] = R_l A_l patterns in
+ * scipy's stored (unsorted) order, ownership moves to the hierarchy; then
+ * set_fine_values recomputes every Galerkin level on device (bitwise scipy's
+ * csr_matmat order) and refactors ILU(0)s and the coarsest LU. */
+int pd_mg_set_galerkin_intermediates(void *mg, int n, void **T);
+int pd_mg_set_fine_values(void *mg, const double *vals_dev);
+/* J = L + gamma (I (x) Mqh) diag(r'(u)) values on L's pattern (spacetime.py:144-151);
+ * Mq_dev: M x M, mh_dev: S (device); kind 1 cubic, 2 Fisher */
+int pd_jacobian_values(void *ctx, int64_t Nt, int M, int64_t S, double dt, double gamma, int kind,
+                       const double *Mq_dev, const double *mh_dev, void *L, const double *u,
+                       double *jv);
 int pd_mg_vcycle(void *ctx, void *mg, const double *b, double *x); /* multigrid.py:268-273 */
 int pd_mg_solve(void *ctx, void *mg, const double *b, double *x, double tol_rel,
                 double tol_abs, int max_cycles, pd_solve_report *rep, double *hist,

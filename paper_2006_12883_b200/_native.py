@@ -64,6 +64,10 @@ _SIGNATURES = {
                            _vp, _int]),
     "pd_mg_destroy": (_int, [_vp]),
     "pd_mg_set_fine_operator": (_int, [_vp, _vp]),
+    "pd_mg_set_galerkin_intermediates": (_int, [_vp, _int, _vp]),
+    "pd_mg_set_fine_values": (_int, [_vp, _vp]),
+    "pd_jacobian_values": (_int, [_vp, _i64, _int, _i64, _dbl, _dbl, _int, _vp, _vp, _vp, _vp,
+                                  _vp]),
     "pd_stop_create": (_int, [_vp, _i64, _int, _i64, _vp, _vp, _vp, _dbl, _vp, _vp,
                               ctypes.POINTER(_vp)]),
     "pd_stop_destroy": (_int, [_vp]),

@@ -181,6 +181,25 @@ int pd_mg_set_fine_operator(void* mg, void* stop) {
         M->set_fine_operator(std::unique_ptr<pd::StOp>(static_cast<pd::StOp*>(stop)));
     });
 }
+int pd_mg_set_galerkin_intermediates(void* mg, int n, void** T) {
+    return guarded([&] {
+        std::vector<std::unique_ptr<pd::Csr>> v;
+        for (int l = 0; l < n; ++l) v.emplace_back(H<pd::Csr>(T[l], "intermediate"));
+        H<pd::Multigrid>(mg, "multigrid")->set_galerkin_intermediates(std::move(v));
+    });
+}
+int pd_mg_set_fine_values(void* mg, const double* vals) {
+    return guarded([&] { H<pd::Multigrid>(mg, "multigrid")->set_fine_values(vals); });
+}
+int pd_jacobian_values(void* ctx, int64_t Nt, int M, int64_t S, double dt, double gamma, int kind,
+                       const double* Mq_dev, const double* mh_dev, void* L, const double* u,
+                       double* jv) {
+    return guarded([&] {
+        if (kind != 1 && kind != 2) throw pd::ConfigError("unknown reaction kind");
+        pd::jacobian_values(*C(ctx), Nt, M, S, dt, gamma, kind, Mq_dev, mh_dev,
+                            *H<pd::Csr>(L, "L"), u, jv);
+    });
+}
 int pd_mg_refactor(void* ctx, void* mg) {
     (void)ctx;
     return guarded([&] { H<pd::Multigrid>(mg, "multigrid")->refactor(); });

@@ -158,6 +158,13 @@ void ilu0_refactor(Ctx& c, Ilu0& f);  // recompute numeric factor from the patte
 void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard = nullptr,
                 int want = 0);
 
+// fixed-pattern SpGEMM values (scipy csr_matmat accumulation order)
+void spgemm_values(Ctx& c, const Csr& A, const Csr& B, Csr& C);
+// J = L + gamma (I (x) Mqh) diag(r'(u)) values on L's pattern
+void jacobian_values(Ctx& c, int64_t Nt, int M, int64_t S, double dt, double gamma, int kind,
+                     const double* Mq_dev, const double* mh_dev, const Csr& L, const double* u,
+                     double* jv);
+
 // dense LU
 std::unique_ptr<DenseLU> dense_lu_from_csr(Ctx& c, const Csr& A);
 void dense_lu_solve(Ctx& c, const DenseLU& f, const double* b, double* x);

@@ -413,6 +413,27 @@ void Multigrid::set_fine_operator(std::unique_ptr<StOp> op) {
     if (lv.size() > 1 && lv[0].gm) lv[0].gm->set_operator(fine_op.get());
 }
 
+void Multigrid::set_galerkin_intermediates(std::vector<std::unique_ptr<Csr>> T) {
+    if (T.size() + 1 != lv.size()) throw ConfigError("need one R*A intermediate per transfer");
+    for (size_t l = 0; l < T.size(); ++l)
+        if (T[l]->nrows != lv[l].R->nrows || T[l]->ncols != lv[l].n)
+            throw ConfigError("R*A intermediate has the wrong shape");
+    galerkin_T = std::move(T);
+}
+
+void Multigrid::set_fine_values(const double* vals) {
+    if (galerkin_T.empty() && lv.size() > 1)
+        throw ConfigError("device Galerkin refresh needs the R*A intermediate patterns");
+    Csr& A0 = *lv[0].A;
+    PD_CUDA(cudaMemcpyAsync(A0.val.p, vals, A0.nnz * sizeof(double), cudaMemcpyDeviceToDevice,
+                            c.stream));
+    for (size_t l = 0; l + 1 < lv.size(); ++l) {
+        spgemm_values(c, *lv[l].R, *lv[l].A, *galerkin_T[l]);
+        spgemm_values(c, *galerkin_T[l], *lv[l].P, *lv[l + 1].A);
+    }
+    refactor();
+}
+
 void Multigrid::refactor() {
     const int L = (int)lv.size();
     for (int l = 0; l + 1 < L; ++l) {

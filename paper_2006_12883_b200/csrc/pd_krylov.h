@@ -81,6 +81,10 @@ class Multigrid {
               int smooth_solves);
     // replace level matrix values (same patterns) and refactor (Newton refresh)
     void refactor();
+    // device Galerkin: T_l = R_l A_l (scipy's stored order), A_{l+1} = T_l P_l
+    void set_galerkin_intermediates(std::vector<std::unique_ptr<Csr>> T);
+    // new fine values (device pointer, fine pattern) -> Galerkin -> refactor
+    void set_fine_values(const double* vals);
     Csr& level_matrix(int l) { return *lv[l].A; }
     Ilu0* level_precond(int l) { return lv[l].pre.get(); }
     // level 0 applies A through a matrix-free operator (values must equal the CSR's)
@@ -104,6 +108,7 @@ class Multigrid {
     std::vector<MgLevel> lv;
     std::unique_ptr<DenseLU> coarse;
     std::unique_ptr<StOp> fine_op;
+    std::vector<std::unique_ptr<Csr>> galerkin_T;
     DevBuf<double> coarse_inv;  // A_c^{-1} (row-major) when n_c <= kCoarseInverseMax
     int nu, partitions, restart, smooth_solves;
     DevBuf<double> res2;

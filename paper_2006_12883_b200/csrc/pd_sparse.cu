@@ -941,3 +941,85 @@ void dense_inverse_apply(Ctx& c, const double* inv, int64_t n, const double* b, 
     launch(k_gemv_rows, c.grid_for(n * 32, 256, 8), 256, 0, c.stream, inv, b, x, n);
 }
 }  // namespace pd
+
+namespace pd {
+// ------------------------------------------------------------------ fixed-pattern SpGEMM
+// C = A B (values only) on a pattern fixed at setup, accumulating every entry
+// in scipy csr_matmat's order: rows of A in stored order, rows of B in stored
+// order, sums[k] += a*b separately rounded (sparsetools csr.h).  With A = R
+// and B = A_l, then A = (R A_l) in its stored (scipy first-touch) order and
+// B = P, the coarse operator equals the reference's `R @ A @ P` bitwise
+// (multigrid.py:232-233).  One thread per row of C; C rows hold <= a few
+// hundred entries, located by linear scan of the row's stored columns.
+__global__ void k_spgemm_values(int64_t nrows, const int64_t* __restrict__ arp,
+                                const int32_t* __restrict__ aci, const double* __restrict__ av,
+                                const int64_t* __restrict__ brp, const int32_t* __restrict__ bci,
+                                const double* __restrict__ bv, const int64_t* __restrict__ crp,
+                                const int32_t* __restrict__ cci, double* __restrict__ cv) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nrows;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c0 = crp[i], c1 = crp[i + 1];
+        for (int64_t q = c0; q < c1; ++q) cv[q] = 0.0;
+        for (int64_t jj = arp[i]; jj < arp[i + 1]; ++jj) {
+            const int64_t j = aci[jj];
+            const double v = av[jj];
+            for (int64_t kk = brp[j]; kk < brp[j + 1]; ++kk) {
+                const int32_t k = bci[kk];
+                int64_t q = c0;
+                while (q < c1 && cci[q] != k) ++q;
+                if (q < c1) cv[q] = add(cv[q], mul(v, bv[kk]));
+            }
+        }
+    }
+}
+
+void spgemm_values(Ctx& c, const Csr& A, const Csr& B, Csr& C) {
+    if (A.nrows != C.nrows || A.ncols != B.nrows || B.ncols != C.ncols)
+        throw ConfigError("fixed-pattern SpGEMM shape mismatch");
+    if (C.nrows == 0) return;
+    launch(k_spgemm_values, c.grid_for(C.nrows, BS, 8), BS, 0, c.stream, C.nrows, A.rowptr.p,
+           A.col.p, A.val.p, B.rowptr.p, B.col.p, B.val.p, C.rowptr.p, C.col.p, C.val.p);
+    PD_LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------ Newton Jacobian values
+// J = L + gamma (I (x) Mqh) diag(r'(u)) on L's pattern (spacetime.py:144-151):
+// for an entry of row (n,m,j) at column (n,m',j): Jv = fl(Lv + fl(gamma*fl(Mqh*r'(u_col))))
+// with Mqh = fl(dt*fl(Mq[m][m']*mh_j)); every other entry is L's value.
+__global__ void k_jacobian_values(int64_t N, int M, int64_t S, double dt, double gamma, int kind,
+                                  const double* __restrict__ Mq, const double* __restrict__ mh,
+                                  const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                  const double* __restrict__ lv, const double* __restrict__ u,
+                                  double* __restrict__ jv) {
+    const int64_t MS = (int64_t)M * S;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < N;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t n = r / MS, rem = r - n * MS;
+        const int m = (int)(rem / S);
+        const int64_t j = rem - (int64_t)m * S;
+        for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
+            const int64_t col = ci[p];
+            double val = lv[p];
+            const int64_t nc = col / MS, remc = col - nc * MS;
+            const int mc = (int)(remc / S);
+            if (nc == n && remc - (int64_t)mc * S == j) {
+                const double u0 = u[col];
+                const double g = kind == 1 ? sub(mul(3.0, mul(u0, u0)), 1.0) : sub(mul(2.0, u0), 1.0);
+                const double mqh = mul(dt, mul(Mq[m * M + mc], mh[j]));
+                val = add(val, mul(gamma, mul(mqh, g)));
+            }
+            jv[p] = val;
+        }
+    }
+}
+
+void jacobian_values(Ctx& c, int64_t Nt, int M, int64_t S, double dt, double gamma, int kind,
+                     const double* Mq_dev, const double* mh_dev, const Csr& L, const double* u,
+                     double* jv) {
+    const int64_t N = Nt * M * S;
+    if (L.nrows != N) throw ConfigError("Jacobian pattern does not match the space-time grid");
+    launch(k_jacobian_values, c.grid_for(N, BS, 8), BS, 0, c.stream, N, M, S, dt, gamma, kind,
+           Mq_dev, mh_dev, L.rowptr.p, L.col.p, L.val.p, u, jv);
+    PD_LAUNCH_CHECK();
+}
+}  // namespace pd

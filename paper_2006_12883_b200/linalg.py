@@ -51,9 +51,11 @@ def kron(A, B) -> sp.csr_matrix:
 class DeviceCsr:
     """A CSR matrix resident in HBM (int64 row pointers, int32 columns, fp64)."""
 
-    def __init__(self, A, ctx: N.Context | None = None):
+    def __init__(self, A, ctx: N.Context | None = None, canonical: bool = True):
         self.ctx = ctx or N.context()
-        A = as_csr(A)
+        # canonical=False keeps the stored entry order (e.g. scipy's unsorted
+        # R @ A intermediate, whose order the device Galerkin replays)
+        A = as_csr(A) if canonical else sp.csr_matrix(A)
         self.shape = A.shape
         self.nnz = int(A.nnz)
         rp = np.ascontiguousarray(A.indptr, dtype=np.int64)

@@ -184,9 +184,17 @@ class MultigridHierarchy:
         return len(self.dims)
 
     def _galerkin(self, A) -> list[sp.csr_matrix]:
+        """R A P per level exactly as multigrid.py:232-233 evaluates it: (R @ A) @ P.
+
+        The unsorted intermediates R @ A are kept: the device Galerkin refresh
+        replays their stored order so later levels stay bitwise scipy's.
+        """
         mats = [A]
+        self._Ts = []
         for t in self.transfers:
-            mats.append(as_csr(t.restriction @ mats[-1] @ t.prolongation))
+            T = t.restriction @ mats[-1]
+            self._Ts.append(T)
+            mats.append(as_csr(T @ t.prolongation))
         return mats
 
     def set_fine_matrix(self, A) -> None:
@@ -226,6 +234,29 @@ class MultigridHierarchy:
             self._dev_mats = dev  # borrowed views for pattern checks/value updates
         self.matrices = mats
         self.setup_time = time.perf_counter() - t0
+
+    # ---- device Newton refresh (§8(f)1) --------------------------------------
+    def enable_device_refresh(self) -> None:
+        """Upload the R@A intermediates; later fine values are refreshed on device."""
+        if self._mg is None or getattr(self, "_device_refresh", False):
+            return
+        Ts = [DeviceCsr(T, self.ctx, canonical=False) for T in self._Ts]
+        arr = (ctypes.c_void_p * max(len(Ts), 1))(*[d.handle for d in Ts])
+        N.call("pd_mg_set_galerkin_intermediates", self._mg, len(Ts), arr)
+        for d in Ts:
+            d.release()
+        self._device_refresh = True
+
+    def set_fine_values_dev(self, vals) -> None:
+        """New fine-level values on the existing pattern (CUDA tensor, nnz doubles):
+        Galerkin products and all factorizations are recomputed on device."""
+        if getattr(self, "_has_fine_op", False):
+            N.call("pd_mg_set_fine_operator", self._mg, None)
+            self._has_fine_op = False
+        N.call("pd_mg_set_fine_values", self._mg, N.ptr(vals))
+
+    def fine_pattern_matches(self, A) -> bool:
+        return bool(self._dev_mats) and self._dev_mats[0].same_pattern(A)
 
     def attach_fine_operator(self, system) -> None:
         """Apply level 1 matrix-free (K1, bitwise the system's global CSR product).
@@ -346,7 +377,16 @@ def mg_linear_solver(hierarchy: MultigridHierarchy, tol_rel=1e-9, tol_abs=1e-9, 
     """Newton inner solver refreshing the hierarchy per Jacobian (multigrid.py:339-364)."""
 
     def solver(J, rhs):
-        hierarchy.set_fine_matrix(J)
+        from .spacetime import DeviceJacobian
+
+        if isinstance(J, DeviceJacobian):
+            if getattr(hierarchy, "_device_refresh", False):
+                hierarchy.set_fine_values_dev(J.values)  # all on device
+            else:
+                hierarchy.set_fine_matrix(J.host())  # first step: patterns from scipy
+                hierarchy.enable_device_refresh()
+        else:
+            hierarchy.set_fine_matrix(J)
         if fixed_cycles is not None:
             bd = N.to_device(rhs, hierarchy.ctx)
             x = N.zeros(bd.numel(), hierarchy.ctx)
@@ -358,4 +398,5 @@ def mg_linear_solver(hierarchy: MultigridHierarchy, tol_rel=1e-9, tol_abs=1e-9, 
             return N.like_input(x, rhs), rep
         return hierarchy.solve(rhs, tol_rel=tol_rel, tol_abs=tol_abs, max_cycles=max_cycles)
 
+    solver.device_jacobian = True  # newton_solve may hand over device-side Jacobians
     return solver

@@ -153,3 +153,41 @@ def test_newton_mg_matches_reference(golden):
     assert rep.inner_iterations == g["inner"].tolist()
     assert rep.damped_steps == int(g["damped"])
     assert per_node_rel(x, g["x"], (8, 2, 33)) < 1e-9
+
+
+def test_device_jacobian_bitwise_equals_scipy():
+    """pd_jacobian_values reproduces spacetime.py:144-151 (scipy J) bitwise on L's pattern."""
+    prob = pd.monodomain_problem()
+    mesh = pd.SpaceMesh(32, prob.X)
+    s = pd.assemble_system(pd.make_tableau(3), pd.assemble_space(mesh), pd.TimeGrid(4, prob.T),
+                           prob.gamma, prob.u0(mesh.vertices))
+    u = np.random.default_rng(2).standard_normal(s.size)
+    Jh = pd.linalg.as_csr(s.jacobian(u))  # the hierarchy canonicalises J (multigrid.py:226)
+    Jd = s.jacobian_device(u)
+    L = s.global_matrix()
+    assert np.array_equal(Jh.indptr, L.indptr) and np.array_equal(Jh.indices, L.indices)
+    np.testing.assert_array_equal(Jd.values.cpu().numpy(), Jh.data)
+
+
+def test_device_galerkin_refresh_bitwise_equals_scipy():
+    """Device R A P (scipy csr_matmat order) equals the host Galerkin levels bitwise."""
+    prob = pd.monodomain_problem()
+    mesh = pd.SpaceMesh(32, prob.X)
+    s = pd.assemble_system(pd.make_tableau(2), pd.assemble_space(mesh), pd.TimeGrid(8, prob.T),
+                           prob.gamma, prob.u0(mesh.vertices))
+    h = pd.build_hierarchy(s, "SMG", 3, 3)
+    u1 = np.random.default_rng(3).standard_normal(s.size)
+    u2 = np.random.default_rng(4).standard_normal(s.size)
+    h.set_fine_matrix(s.jacobian(u1))
+    h.enable_device_refresh()
+    h.set_fine_values_dev(s.jacobian_device(u2).values)
+    host = pd.build_hierarchy(s, "SMG", 3, 3, matrix=s.jacobian(u2)).matrices
+    import ctypes
+    from paper_2006_12883_b200 import _native as N
+    for l in range(1, 3):
+        hnd = ctypes.c_void_p()
+        N.call("pd_mg_level_matrix", h._mg, l, ctypes.byref(hnd))
+        M = host[l]
+        dev = pd.DeviceCsr.borrowed(hnd, M.shape, M.nnz, h.ctx)
+        x = np.random.default_rng(l).standard_normal(M.shape[1])
+        np.testing.assert_array_equal(dev.dot(x), M @ x)
