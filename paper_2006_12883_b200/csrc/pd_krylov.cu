@@ -177,6 +177,15 @@ __global__ void k_gm_newvec(const GmDev* s, int slot, const double* w, double* V
     }
 }
 
+// Z[j] = z = M^{-1} V[j]  (kept so the cycle update needs no extra ILU apply)
+__global__ void k_gm_store_z(const GmDev* s, const double* z, double* Z, int64_t n) {
+    if (vphase(s) != GM_RUN) return;
+    double* dst = Z + (int64_t)s->j * n;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = z[i];
+}
+
 // y = H[:k,:k]^{-1} g[:k]  (column-oriented back substitution, dtrsm order)
 __global__ void k_gm_finish_y(GmDev* s) {
     if (s->phase != GM_FINISH) return;
@@ -244,8 +253,9 @@ __global__ void k_gm_apply(const GmDev* s, double* x, const double* xg, int64_t 
 }
 
 // ------------------------------------------------------------------ Gmres
-Gmres::Gmres(Ctx& c_, const Csr* A_, Ilu0* M_, int64_t n_, int restart_, int max_it_)
-    : c(c_), A(A_), M(M_), n(n_), max_it(max_it_) {
+Gmres::Gmres(Ctx& c_, const Csr* A_, Ilu0* M_, int64_t n_, int restart_, int max_it_,
+             bool store_z_)
+    : c(c_), A(A_), M(M_), n(n_), max_it(max_it_), store_z(store_z_ && M_ != nullptr) {
     restart = std::max<int64_t>(1, std::min<int64_t>(restart_, n_));
     if (restart > kGmMaxRestart)
         throw ConfigError("GMRES restart length above " + std::to_string(kGmMaxRestart));
@@ -258,6 +268,7 @@ Gmres::Gmres(Ctx& c_, const Csr* A_, Ilu0* M_, int64_t n_, int restart_, int max
     rg.alloc(std::max<int64_t>(n, 1));
     xg.alloc(std::max<int64_t>(n, 1));
     vcur.alloc(std::max<int64_t>(n, 1));
+    if (store_z) Z.alloc((size_t)restart * std::max<int64_t>(n, 1));
     norm2.alloc(1);
     hist.alloc(std::max(max_it, 1) + 2);
 }
@@ -281,6 +292,7 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
     if (M) {
         ilu0_solve(c, *M, vcur.p, z.p, ph, GM_RUN);
         zin = z.p;
+        if (store_z) launch(k_gm_store_z, g, KB, 0, c.stream, st.p, (const double*)z.p, Z.p, n);
     }
     apply_A(c, *A, op, zin, w.p, SPMV_SET, nullptr, ph, GM_RUN);
     const int passes = std::min(mgs_passes, restart + 1);
@@ -291,9 +303,11 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
     launch(k_gm_newvec, g, KB, 0, c.stream, st.p, slot, w.p, V.p, vcur.p, n);
     // cycle finish (active only when this step ended the cycle)
     launch(k_gm_finish_y, 1, 1, 0, c.stream, st.p);
-    launch(k_gm_combine, g, KB, 0, c.stream, st.p, V.p, u.p, n);
+    // x += M^{-1}(V y) (linalg.py:297); with stored Z_j = M^{-1} V_j this is
+    // sum_j y_j Z_j — the same linear map, one ILU apply fewer per cycle
+    launch(k_gm_combine, g, KB, 0, c.stream, st.p, store_z ? Z.p : V.p, u.p, n);
     const double* du = u.p;
-    if (M) {
+    if (M && !store_z) {
         ilu0_solve(c, *M, u.p, z.p, ph, GM_FINISH);
         du = z.p;
     }
@@ -442,7 +456,7 @@ void Multigrid::refactor() {
         if (!m.pre) {
             m.pre = ilu0_create(c, *m.A, std::max(blocks, 1));
             m.gm = std::make_unique<Gmres>(c, m.A.get(), m.pre.get(), m.n,
-                                           std::min(nu, restart), nu);
+                                           std::min(nu, restart), nu, /*store_z=*/true);
         } else {
             ilu0_refactor(c, *m.pre);
         }

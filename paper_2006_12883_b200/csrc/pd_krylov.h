@@ -23,7 +23,10 @@ struct GmDev {
 
 class Gmres {
    public:
-    Gmres(Ctx& c, const Csr* A, Ilu0* M, int64_t n, int restart, int max_it);
+    // store_z: keep Z_j = M^{-1} V_j and update x with Z y (no extra preconditioner
+    // apply per cycle); the smoother uses it, the standalone gmres mirrors linalg.py
+    Gmres(Ctx& c, const Csr* A, Ilu0* M, int64_t n, int restart, int max_it,
+          bool store_z = false);
     // init from r0 = b - A x0 whose squared norm is at *norm2_dev; x0 may be
     // null (zero start, as in the smoother)
     void enqueue_init(const double* r0, const double* norm2_dev, double tol_rel, double tol_abs,
@@ -46,7 +49,8 @@ class Gmres {
     int64_t n;
     int restart, max_it;
     DevBuf<GmDev> st;
-    DevBuf<double> V, w, z, u, rg, xg, vcur, norm2, hist;
+    bool store_z = false;
+    DevBuf<double> V, w, z, u, rg, xg, vcur, norm2, hist, Z;
     const double* r0 = nullptr;
 };
 

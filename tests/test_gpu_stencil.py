@@ -66,4 +66,6 @@ def test_hierarchy_with_matrix_free_fine_level(golden):
     x1, r1 = h_mf.solve(system.rhs(), tol_rel=1e-10, tol_abs=1e-10)
     x2, r2 = h_csr.solve(system.rhs(), tol_rel=1e-10, tol_abs=1e-10)
     assert r1.iterations == r2.iterations == int(g["SMG_P2_its"])
-    np.testing.assert_array_equal(x1, x2)
+    # K1 is bitwise the CSR product, but its fused |r|^2 reduces in another
+    # order (2D grid), so iterates agree to rounding, not bit for bit
+    assert np.linalg.norm(x1 - x2) <= 1e-12 * np.linalg.norm(x2)
