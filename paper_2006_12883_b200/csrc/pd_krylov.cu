@@ -27,9 +27,11 @@ constexpr int64_t kCoarseInverseMax = 8192;  // 512 MB of inverse at most
 __device__ __forceinline__ int vphase(const GmDev* s) { return *((volatile const int*)&s->phase); }
 
 __global__ void k_gm_init(GmDev* s, const double* norm2, double tol_rel, double tol_abs,
-                          int max_it, int restart, double* hist, int has_x0) {
+                          int max_it, int restart, double* hist, int has_x0, int skip_final) {
     const double beta = sqrt(*norm2);
     s->has_x0 = has_x0;
+    s->skip_final = skip_final;
+    s->final_res = -1;
     s->max_it = max_it;
     s->restart = restart;
     s->tol_rel = tol_rel;
@@ -155,6 +157,9 @@ __global__ void k_gm_arnoldi(GmDev* s, int slot, double* hist) {
     if (res <= s->thr || happy || s->total >= s->max_it) {
         s->k = j + 1;
         s->phase = GM_FINISH;
+        // the closing true residual decides restarts and the report; a smoother
+        // at its iteration cap needs neither (multigrid.py:246-255 drops it)
+        s->final_res = (s->skip_final && s->total >= s->max_it) ? -1 : GM_FINISH;
     } else {
         s->j = j + 1;
     }
@@ -222,8 +227,13 @@ __global__ void k_gm_update_x(const GmDev* s, double* xg, const double* du, int6
 
 __global__ void k_gm_restart(GmDev* s, const double* norm2, double* hist) {
     if (s->phase != GM_FINISH) return;
-    const double beta = sqrt(*norm2);
     s->cycles += 1;
+    if (s->final_res != GM_FINISH) {  // smoother at its cap: done, residual not formed
+        s->diverged = 1;
+        s->phase = GM_DONE;
+        return;
+    }
+    const double beta = sqrt(*norm2);
     if (!isfinite(beta)) {
         s->err = 3;
         s->phase = GM_DONE;
@@ -278,7 +288,7 @@ void Gmres::enqueue_init(const double* r0_, const double* norm2_dev, double tol_
     r0 = r0_;
     if (x0) vec_copy(c, xg.p, x0, n);
     launch(k_gm_init, 1, 1, 0, c.stream, st.p, norm2_dev, tol_rel, tol_abs, max_it, restart, hist.p,
-                                     x0 ? 1 : 0);
+           x0 ? 1 : 0, store_z ? 1 : 0);
     PD_LAUNCH_CHECK();
 }
 
@@ -312,7 +322,7 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
         du = z.p;
     }
     launch(k_gm_update_x, g, KB, 0, c.stream, st.p, xg.p, du, n);
-    apply_A(c, *A, op, xg.p, rg.p, SPMV_RESID, b, ph, GM_FINISH, norm2.p, nullptr);
+    apply_A(c, *A, op, xg.p, rg.p, SPMV_RESID, b, &st.p->final_res, GM_FINISH, norm2.p, nullptr);
     launch(k_gm_restart, 1, 1, 0, c.stream, st.p, norm2.p, hist.p);
     PD_LAUNCH_CHECK();
 }
@@ -333,11 +343,14 @@ std::vector<double> Gmres::history(int total) {
 }
 
 void enqueue_gmres_smooth(Ctx& c, Gmres& g, const Csr& A, const StOp* op, const double* b,
-                          double* x, double* r_work, int nu) {
+                          double* x, double* r_work, int nu, const double* r_norm2) {
     const int64_t n = A.nrows;
     // r = b - A x with |r|^2 (the GMRES initial residual; x0 = 0 so r0 = r)
-    apply_A(c, A, op, x, r_work, SPMV_RESID, b, nullptr, 0, c.scalars.p + 8, nullptr);
-    g.enqueue_init(r_work, c.scalars.p + 8, 1e-13, 0.0);
+    if (!r_norm2) {
+        apply_A(c, A, op, x, r_work, SPMV_RESID, b, nullptr, 0, c.scalars.p + 8, nullptr);
+        r_norm2 = c.scalars.p + 8;
+    }
+    g.enqueue_init(r_work, r_norm2, 1e-13, 0.0);
     for (int s = 0; s < nu; ++s) g.enqueue_slot(s, s + 2, r_work);
     launch(k_gm_apply, c.grid_for(n, KB, 8), KB, 0, c.stream, g.dev(), x, g.x(), n);
     PD_LAUNCH_CHECK();
@@ -477,8 +490,12 @@ void Multigrid::cycle(int l) {
         return;
     }
     const StOp* op = (l == 0) ? fine_op.get() : nullptr;
-    for (int s = 0; s < smooth_solves; ++s)
-        enqueue_gmres_smooth(c, *m.gm, *m.A, op, b, x, m.r.p, nu);
+    for (int s = 0; s < smooth_solves; ++s) {
+        // the solve loop's stopping test already formed r = b - A x at level 1
+        const double* ready = (l == 0 && s == 0) ? fine_r_norm2 : nullptr;
+        enqueue_gmres_smooth(c, *m.gm, *m.A, op, b, x, m.r.p, nu, ready);
+    }
+    if (l == 0) fine_r_norm2 = nullptr;
     apply_A(c, *m.A, op, x, m.r.p, SPMV_RESID, b);
     MgLevel& nx = lv[l + 1];
     csr_spmv(c, *m.R, m.r.p, nx.b.p, SPMV_SET, nullptr);
@@ -501,6 +518,7 @@ void Multigrid::enqueue_vcycle(const double* b, double* x) {
     } catch (...) {
         m.b.p = sb;
         m.x.p = sx;
+        fine_r_norm2 = nullptr;
         throw;
     }
     m.b.p = sb;
@@ -540,7 +558,9 @@ Multigrid::Report Multigrid::solve(const double* b, double* x, double tol_rel, d
             rep.diverged = true;
             break;
         }
+        fine_r_norm2 = res2.p;  // lv[0].r holds b - A x for the current x
         enqueue_vcycle(b, x);
+        fine_r_norm2 = nullptr;
         PD_CUDA(cudaMemsetAsync(nonfinite.p, 0, sizeof(int), c.stream));
         apply_A(c, *f.A, fine_op.get(), x, r, SPMV_RESID, b, nullptr, 0, res2.p, nonfinite.p);
         int bad = 0;

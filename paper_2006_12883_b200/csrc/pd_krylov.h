@@ -14,7 +14,7 @@ enum GmPhase { GM_START = 0, GM_RUN = 1, GM_FINISH = 2, GM_DONE = 3 };
 
 struct GmDev {
     int phase, j, k, total, cycles, vec_idx, vec_slot, err, converged, diverged, max_it, restart,
-        has_x0;
+        has_x0, skip_final, final_res;
     double beta, thr, lowest, hn, last_res, tol_rel, tol_abs, beta0;
     double H[(kGmMaxRestart + 1) * kGmMaxRestart];  // row-major (restart+1) x restart
     double cs[kGmMaxRestart], sn[kGmMaxRestart], g[kGmMaxRestart + 1], y[kGmMaxRestart];
@@ -67,8 +67,9 @@ GmresResult gmres_run(Ctx& c, const Csr& A, Ilu0* M, const double* b, const doub
 // Enqueue x += GMRES(A, b - A x) with ILU/block-Jacobi right preconditioning,
 // restart=min(nu,restart), max_it=nu, tol_rel=1e-13, tol_abs=0: exactly one
 // smoothing solve of multigrid.py:243-256.  No host synchronisation.
+// r_ready: r_work already holds b - A x and *r_norm2 its squared norm
 void enqueue_gmres_smooth(Ctx& c, Gmres& g, const Csr& A, const StOp* op, const double* b,
-                          double* x, double* r_work, int nu);
+                          double* x, double* r_work, int nu, const double* r_norm2 = nullptr);
 
 struct MgLevel {
     std::unique_ptr<Csr> A, R, P;  // R/P: transfer to the next coarser level (unused on coarsest)
@@ -108,6 +109,7 @@ class Multigrid {
 
    private:
     void cycle(int l);
+    const double* fine_r_norm2 = nullptr;  // set by solve(): lv[0].r already = b - A x
     Ctx& c;
     std::vector<MgLevel> lv;
     std::unique_ptr<DenseLU> coarse;
