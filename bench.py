@@ -259,10 +259,14 @@ def run_b200(args):
     alg_bytes = (12.0 * nnz_row + 24.0) * system.size
     peak, peak_kind = peaks()
     achieved = alg_bytes / t_ilu / 1e9
+    kernel = ("k_wf_sweep<lower>+k_wf_sweep<upper>" if h.wavefront and h.wavefront[0]
+              else "k_trsv_lower+k_trsv_upper")
     traffic = None
     tfile = ROOT / "profiles" / "ilu_traffic.json"
-    if tfile.exists():
-        traffic = json.loads(tfile.read_text()).get("bytes_per_launch")
+    if tfile.exists():  # ncu DRAM bytes of the same sweep pair (only if it is the one timed)
+        tj = json.loads(tfile.read_text())
+        if tj.get("kernel") == kernel:
+            traffic = tj.get("bytes_per_launch")
 
     if rank == 0:
         cpu = None
@@ -285,7 +289,7 @@ def run_b200(args):
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "k_trsv_lower+k_trsv_upper (fine-level ILU(0) apply)",
+                         "kernel": kernel + " (fine-level ILU(0) apply)",
                          "alg_bytes_per_launch": alg_bytes, "ms_per_launch": t_ilu * 1e3,
                          "peak_kind": peak_kind},
             "cpu_baseline": cpu,

@@ -59,6 +59,16 @@ int pd_ilu0_create(void *ctx, void *csr, int nblocks, void **ilu_out); /* synchr
 int pd_ilu0_refactor(void *ctx, void *ilu);                            /* synchronising */
 int pd_ilu0_solve(void *ctx, void *ilu, const double *b, double *x);
 int pd_ilu0_levels(void *ilu, int32_t *lower_levels, int32_t *upper_levels); /* host out */
+/* Structured wavefront sweeps for rows laid out [task][ngroup][nline][npoint]
+ * (2D FD space-time: one time step = M node grids of nline x npoint points):
+ * one CTA per task, one thread per (grid, line), in-task dependencies through
+ * shared memory, per-step factor values staged by TMA bulk copies.  Same
+ * arithmetic as pd_ilu0_solve (bitwise); *applied = 0 when the schedule does
+ * not fit (the level-scheduled sweeps stay in use).  ring <= 0 selects the
+ * default ring depth (8).  A faster schedule for linalg.py:104-113; the
+ * reference has no counterpart. */
+int pd_ilu0_set_wavefront(void *ctx, void *ilu, int64_t ngroup, int64_t nline, int64_t npoint,
+                          int ring, int *applied);                    /* synchronising */
 int pd_ilu0_destroy(void *ilu);
 
 /* ---- dense LU of the coarsest level (linalg.py:196-209 DenseLU) ---------- */
@@ -75,7 +85,8 @@ int pd_gmres(void *ctx, void *A, void *ilu, const double *b, const double *x0, d
 
 /* ---- space-time multigrid (multigrid.py:197-305 MultigridHierarchy).
  *      Takes ownership of the level matrices mats[0..L) (Galerkin products,
- *      multigrid.py:232-233) and of R[0..L-1), P[0..L-1).  ---------------- */
+ *      multigrid.py:232-233) and of R[0..L-1), P[0..L-1), also when it fails
+ *      (they are freed then).  --------------------------------------------- */
 int pd_mg_create(void *ctx, int nlevels, void **mats, void **R, void **P, int nu,
                  int partitions, int restart, int smooth_solves, void **mg_out);
 int pd_mg_level_matrix(void *mg, int level, void **csr_out); /* borrowed handle */

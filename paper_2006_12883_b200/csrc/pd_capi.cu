@@ -119,6 +119,15 @@ int pd_ilu0_levels(void* ilu, int32_t* lo, int32_t* up) {
         if (up) *up = f->nlevels_up;
     });
 }
+int pd_ilu0_set_wavefront(void* ctx, void* ilu, int64_t ngroup, int64_t nline, int64_t npoint,
+                          int ring, int* applied) {
+    return guarded([&] {
+        auto* c = H<pd::Ctx>(ctx, "ctx");
+        auto* f = H<pd::Ilu0>(ilu, "ilu");
+        const bool ok = pd::ilu0_set_wavefront(*c, *f, ngroup, nline, npoint, ring);
+        if (applied) *applied = ok ? 1 : 0;
+    });
+}
 int pd_ilu0_destroy(void* ilu) {
     return guarded([&] { delete static_cast<pd::Ilu0*>(ilu); });
 }

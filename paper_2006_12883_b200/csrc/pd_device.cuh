@@ -114,5 +114,23 @@ __device__ __forceinline__ void grid_sum_finish(double v, double* partials, unsi
     }
 }
 
+// Value-as-flag words: a sweep output starts as this signalling-NaN payload and
+// is published with one single-copy-atomic 64-bit store (pd_sparse.cu).
+constexpr unsigned long long kPending = 0x7ff4a5a55a5a0001ull;  // signalling-NaN payload
+
+__device__ __forceinline__ unsigned long long ld_strong_u64(const double* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_strong(double* p, double v) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v))
+                 : "memory");
+}
+__device__ __forceinline__ void st_pending(double* p) {
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(kPending) : "memory");
+}
+
+
 }  // namespace dev
 }  // namespace pd

@@ -103,6 +103,24 @@ struct Csr {
     DevBuf<double> val;
 };
 
+// Structured wavefront schedule of one ILU(0) triangular sweep (pd_wavefront.cu):
+// tasks of G node grids x nline lines x npoint points (one CTA each, thread =
+// (grid, line)), per-step blocks of pattern ids + factor values in `blob`.
+struct WfPlan {
+    int64_t n = 0, nslot = 0;
+    int ntask = 0, T = 0, nline = 0, npoint = 0, R = 0, pwo = 0, maxS = 0, blocks = 0, npat = 0,
+        ng = 0;
+    size_t smem = 0, stage_bytes = 0;
+    DevBuf<int32_t> nsteps;
+    DevBuf<int64_t> boff, bofs, q0;
+    DevBuf<int32_t> pattern;         // per pattern: len, ng, global offsets
+    DevBuf<int16_t> offs;            // per pattern and ring phase: source offsets
+    DevBuf<unsigned char> blob;      // step blocks
+    DevBuf<int32_t> srow, sstride, scount;  // value gather slots (one per row)
+    DevBuf<int64_t> sval, sdiag;
+    DevBuf<unsigned long long> trace;  // PD_WF_TRACE diagnostics
+};
+
 // ILU(0) factors with level schedules (see pd_sparse.cu).
 struct Ilu0 {
     int64_t n = 0;
@@ -123,6 +141,7 @@ struct Ilu0 {
     DevBuf<int32_t> tcol_lo, tcol_up;
     DevBuf<double> tval_lo, tval_up, tdiag;
     std::vector<std::pair<int64_t, int64_t>> ranges;
+    std::unique_ptr<WfPlan> wf_lo, wf_up;  // structured sweeps (optional)
     const Csr& pat() const { return use_masked ? masked : *pattern; }
 };
 
@@ -157,6 +176,13 @@ std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks);
 void ilu0_refactor(Ctx& c, Ilu0& f);  // recompute numeric factor from the pattern's values
 void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard = nullptr,
                 int want = 0);
+// structured wavefront sweeps (pd_wavefront.cu): false = schedule not applicable
+bool ilu0_set_wavefront(Ctx& c, Ilu0& f, int64_t ngroup, int64_t nline, int64_t npoint,
+                        int ring);
+void wf_gather(Ctx& c, Ilu0& f);
+// fill a sweep output with the value-as-flag pending sentinel (coalesced)
+void arm_pending(Ctx& c, double* y, int64_t n, const int* guard, int want);  // refresh plan values after a (re)factorization
+void wf_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int want);
 
 // fixed-pattern SpGEMM values (scipy csr_matmat accumulation order)
 void spgemm_values(Ctx& c, const Csr& A, const Csr& B, Csr& C);

@@ -408,24 +408,9 @@ __global__ void k_ilu0_factor(int64_t n, const int64_t* __restrict__ rp,
 // atomic), and dependants poll the value itself, so readiness and data arrive
 // in the same L2 round trip — no per-row flag, no fences.  Each row prefetches
 // its factor entries before polling, then accumulates strictly in CSR order
-// (linalg.py:104-113), separately rounded.  The lower sweep re-arms the upper
-// sweep's output words and the upper sweep re-arms the lower scratch, so no
-// extra initialisation pass is needed between solves.
-constexpr unsigned long long kPending = 0x7ff4a5a55a5a0001ull;  // signalling-NaN payload
+// (linalg.py:104-113), separately rounded.  Each sweep's output is armed with
+// the sentinel by one coalesced pass (arm_pending) right before it runs.
 __constant__ unsigned int poll_ns_max = 256;  // poll backoff cap (PD_POLL_NS_MAX)
-
-__device__ __forceinline__ unsigned long long ld_strong_u64(const double* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_strong(double* p, double v) {
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(__double_as_longlong(v))
-                 : "memory");
-}
-__device__ __forceinline__ void st_pending(double* p) {
-    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(kPending) : "memory");
-}
 
 // s -= sum_{p in [p0,p1)} fac[p] * src[col[p]]  (in order), polling unpublished entries
 template <int kChunk = 16>
@@ -471,8 +456,8 @@ __device__ __forceinline__ double accumulate_polling(double s, const int32_t* __
 __global__ void k_trsv_lower(int64_t n, const int64_t* __restrict__ lp,
                              const int32_t* __restrict__ lcol, const double* __restrict__ lval,
                              const int32_t* __restrict__ order, const double* __restrict__ b,
-                             double* y, double* x_rearm, unsigned long long* counter,
-                             const int* guard, int want) {
+                             double* y, unsigned long long* counter, const int* guard,
+                             int want) {
     if (guard_off(guard, want)) return;
     for (;;) {
         int64_t base = fetch_batch(counter);
@@ -481,7 +466,6 @@ __global__ void k_trsv_lower(int64_t n, const int64_t* __restrict__ lp,
         if (t < n) {
             const int64_t i = order[t];
             const double s = accumulate_polling(b[i], lcol, lval, y, lp[t], lp[t + 1]);
-            st_pending(x_rearm + i);
             st_strong(y + i, s);
         }
     }
@@ -502,7 +486,6 @@ __global__ void k_trsv_upper(int64_t n, const int64_t* __restrict__ up,
             const int64_t i = order[t];
             const double yi = y[i];
             const double s = accumulate_polling(yi, ucol, uval, x, up[t], up[t + 1]);
-            st_pending(y + i);  // re-arm the lower scratch for the next solve
             st_strong(x + i, s / udiag[t]);
         }
     }
@@ -535,6 +518,27 @@ __global__ void k_task_gather(int64_t n, const int64_t* rp, const int32_t* ci, c
         }
         if (upper) tdiag[t] = fac[d];
     }
+}
+
+// Arms a sweep's output words with the pending sentinel: one coalesced pass
+// (per-row re-arming stores inside the sweeps cost one scattered L2
+// transaction each; this costs ~n*8 bytes of streaming writes).
+__global__ void k_arm(double* y, int64_t n, const int* guard, int want) {
+    if (guard_off(guard, want)) return;
+    unsigned long long* u = reinterpret_cast<unsigned long long*>(y);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if ((reinterpret_cast<uintptr_t>(y) & 15) == 0) {
+        ulonglong2* u2 = reinterpret_cast<ulonglong2*>(y);
+        for (int64_t k = i; k < n / 2; k += stride) u2[k] = make_ulonglong2(kPending, kPending);
+        if (i == 0 && (n & 1)) u[n - 1] = kPending;
+    } else {
+        for (int64_t k = i; k < n; k += stride) u[k] = kPending;
+    }
+}
+
+void arm_pending(Ctx& c, double* y, int64_t n, const int* guard, int want) {
+    if (n > 0) launch(k_arm, c.grid_for(n / 2 + 1, BS, 4), BS, 0, c.stream, y, n, guard, want);
 }
 
 __global__ void k_fill_pending(double* y, int64_t n) {
@@ -708,6 +712,7 @@ void ilu0_refactor(Ctx& c, Ilu0& f) {
         throw SolverError("zero pivot in ILU(0) at row " + std::to_string(row), row);
     }
     build_task_layout(c, f);
+    wf_gather(c, f);
 }
 
 static void configure_polling_once() {
@@ -725,11 +730,16 @@ void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, i
     const int64_t n = f.n;
     if (n == 0) return;
     if (b == x) throw ConfigError("ILU(0) solve needs distinct input and output buffers");
-    const Csr& P = f.pat();
+    if (f.wf_lo) {
+        wf_solve(c, f, b, x, guard, want);
+        return;
+    }
     const int g = c.grid_for(n, BS, sweep_blocks_per_sm());
+    arm_pending(c, f.scratch.p, n, guard, want);
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, guard, want);
     launch(k_trsv_lower, g, BS, 0, c.stream, n, f.tp_lo.p, f.tcol_lo.p, f.tval_lo.p,
-           f.order_lo.p, b, f.scratch.p, x, f.counter.p, guard, want);
+           f.order_lo.p, b, f.scratch.p, f.counter.p, guard, want);
+    arm_pending(c, x, n, guard, want);
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, guard, want);
     launch(k_trsv_upper, g, BS, 0, c.stream, n, f.tp_up.p, f.tcol_up.p, f.tval_up.p, f.tdiag.p,
            f.order_up.p, f.scratch.p, x, f.counter.p, guard, want);

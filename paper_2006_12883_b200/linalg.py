@@ -139,6 +139,10 @@ class Ilu0:
         N.call("pd_ilu0_levels", self.handle, ctypes.byref(lo), ctypes.byref(up))
         return lo.value, up.value
 
+    def set_wavefront(self, ngroup: int, nline: int, npoint: int, ring: int = 0) -> bool:
+        """Structured wavefront sweeps for rows laid out [task][ngroup][nline][npoint]."""
+        return set_wavefront(self.ctx, self.handle, ngroup, nline, npoint, ring)
+
     def solve_dev(self, b, out=None):
         self.ctx.sync_stream()
         out = N.empty(self.n, self.ctx) if out is None else out
@@ -154,6 +158,13 @@ class Ilu0:
                 N.load_library().pd_ilu0_destroy(self.handle)
         except Exception:
             pass
+
+
+def set_wavefront(ctx, ilu_handle, ngroup: int, nline: int, npoint: int, ring: int = 0) -> bool:
+    applied = ctypes.c_int()
+    N.call("pd_ilu0_set_wavefront", ctx.handle, ilu_handle, int(ngroup), int(nline), int(npoint),
+           int(ring), ctypes.byref(applied))
+    return bool(applied.value)
 
 
 def ilu0(A) -> Ilu0:

@@ -160,7 +160,7 @@ class MultigridHierarchy:
 
     def __init__(self, fine_matrix, strategy: str, dims: list[LevelDims],
                  transfers: list[TransferSet], nu: int, partitions: int, restart: int = 30,
-                 smooth_solves: int = 1):
+                 smooth_solves: int = 1, grids: list | None = None):
         if nu < 1:
             raise ConfigurationError("need at least one smoothing iteration")
         if len(transfers) != len(dims) - 1:
@@ -177,6 +177,10 @@ class MultigridHierarchy:
         self._mg = None
         self._dev_mats: list[DeviceCsr] = []
         self.setup_time = 0.0
+        # per-level (nline, npoint) of the spatial grid planes (FD, dim >= 2):
+        # enables the structured wavefront ILU sweeps on those levels
+        self.grids = grids or [None] * len(dims)
+        self.wavefront: list[bool] = []
         self.set_fine_matrix(fine_matrix)
 
     @property
@@ -225,15 +229,31 @@ class MultigridHierarchy:
             arr_r = (ctypes.c_void_p * max(L - 1, 1))(*[d.handle for d in Rs])
             arr_p = (ctypes.c_void_p * max(L - 1, 1))(*[d.handle for d in Ps])
             h = ctypes.c_void_p()
-            N.call("pd_mg_create", ctx.handle, L, arr, arr_r, arr_p, int(self.nu),
-                   int(self.partitions), int(self.restart), int(self.smooth_solves),
-                   ctypes.byref(h))
-            for d in dev + Rs + Ps:
-                d.release()  # owned by the native hierarchy now
+            try:
+                N.call("pd_mg_create", ctx.handle, L, arr, arr_r, arr_p, int(self.nu),
+                       int(self.partitions), int(self.restart), int(self.smooth_solves),
+                       ctypes.byref(h))
+            finally:
+                for d in dev + Rs + Ps:
+                    d.release()  # pd_mg_create takes ownership (frees them on failure)
             self._mg = h
             self._dev_mats = dev  # borrowed views for pattern checks/value updates
+            self._enable_wavefront()
         self.matrices = mats
         self.setup_time = time.perf_counter() - t0
+
+    def _enable_wavefront(self) -> None:
+        from .linalg import set_wavefront
+
+        self.wavefront = []
+        for l in range(len(self.dims) - 1):
+            g = self.grids[l] if l < len(self.grids) else None
+            ok = False
+            if g is not None:
+                ilu = ctypes.c_void_p()
+                N.call("pd_mg_level_precond", self._mg, l, ctypes.byref(ilu))
+                ok = set_wavefront(self.ctx, ilu, self.dims[l].m, g[0], g[1])
+            self.wavefront.append(ok)
 
     # ---- device Newton refresh (§8(f)1) --------------------------------------
     def enable_device_refresh(self) -> None:
@@ -337,7 +357,7 @@ def _space_levels(system, L: int):
         specs.append(specs[-1].coarse())
     sizes = [s.ndof for s in specs]
     pairs = [fd_transfers(specs[l]) for l in range(L - 1)]
-    return sizes, pairs, None
+    return sizes, pairs, specs
 
 
 def build_hierarchy(system, strategy: str, L: int, nu: int, partitions: int = 1,
@@ -359,14 +379,17 @@ def build_hierarchy(system, strategy: str, L: int, nu: int, partitions: int = 1,
             if nt % 2**l:
                 raise ConfigurationError(
                     f"STMG: Nt={nt} not divisible by 2^{l} needed for level {l + 1}")
-    sizes, pairs, _ = _space_levels(system, L)
+    sizes, pairs, specs = _space_levels(system, L)
     dims = _level_dims(strategy, L, nt, m, sizes)
+    # 2D FD grids: a time step is [node][line][point] with n points per axis
+    grids = ([(sp_.n, sp_.n) if sp_.dim == 2 else None for sp_ in specs]
+             if isinstance(specs, list) else None)
     if dims[-1].nx_dofs < 2 and spec is None:
         raise ConfigurationError("coarsest spatial level has fewer than 2 dofs")
     transfers = _build_transfers(dims, pairs)
     A = matrix if matrix is not None else system.global_matrix()
     h = MultigridHierarchy(A, strategy, dims, transfers, nu=nu, partitions=partitions,
-                           restart=restart, smooth_solves=smooth_solves)
+                           restart=restart, smooth_solves=smooth_solves, grids=grids)
     if matrix is None:
         h.attach_fine_operator(system)
     return h

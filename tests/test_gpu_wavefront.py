@@ -1,0 +1,107 @@
+"""GPU parity of the structured wavefront ILU(0) sweeps (csrc/pd_wavefront.cu).
+
+The wavefront executor only reschedules rows; every row still accumulates in
+CSR order with separately rounded operations, so solves must be bitwise those
+of the numba reference (restated by oracle/ilu0.c, pinned to the golden
+vectors in test_oracle_golden.py) — for the fine space-time matrix, for
+Galerkin coarse levels (9/27-point couplings), for block-Jacobi masking, for
+periodic wrap-around and for 3D planes.
+"""
+
+import numpy as np
+import pytest
+
+import paper_2006_12883_b200 as pd
+from oracle import paradiff_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _system(name, n, Nt):
+    cfg = pd.baseline_config(name, n=n, Nt=Nt)
+    return cfg, pd.assemble_system(pd.make_tableau(cfg.M), pd.fd_space(cfg.spec),
+                                   pd.TimeGrid(cfg.Nt, cfg.T), 0.0, cfg.u0())
+
+
+def _check(A, ngroup, nline, npoint, parts, seed=0, repeats=2, applies=True):
+    A = pd.linalg.as_csr(A)
+    rng = np.random.default_rng(seed)
+    dev = pd.BlockJacobiPrecond(A, parts) if parts > 1 else pd.Ilu0(A)
+    assert dev.set_wavefront(ngroup, nline, npoint) == applies
+    ref = O.OBlockJacobi(A, parts) if parts > 1 else O.OIlu0(A)
+    for _ in range(repeats):  # repeated solves exercise the re-arming protocol
+        b = rng.standard_normal(A.shape[0])
+        np.testing.assert_array_equal(dev.solve(b), ref.solve(b))
+
+
+@pytest.mark.parametrize("parts", [1, 2, 4])
+def test_wavefront_fine_2d_bitwise(parts):
+    cfg, s = _system("C2", 15, 8)
+    _check(s.global_matrix(), cfg.M, cfg.spec.n, cfg.spec.n, parts)
+
+
+def test_wavefront_periodic_2d_bitwise():
+    """Periodic wrap-around: the far in-line neighbour is read back from global memory."""
+    cfg, s = _system("C3", 16, 4)
+    assert cfg.spec.bc == "periodic"
+    _check(s.global_matrix(), cfg.M, cfg.spec.n, cfg.spec.n, 2)
+
+
+def test_wavefront_3d_planes_fall_back():
+    """3D planes couple to many other planes: not a wavefront task; level sweeps stay."""
+    cfg, s = _system("C4", 7, 4)
+    assert cfg.spec.dim == 3
+    _check(s.global_matrix(), 1, cfg.spec.n, cfg.spec.n, 2, applies=False)
+
+
+def test_wavefront_single_group_ring_and_globals_bitwise():
+    """One node grid per task (M=1 layout view): node couplings become globals."""
+    cfg, s = _system("C2", 15, 4)
+    A = pd.linalg.as_csr(s.global_matrix())
+    # a 2-group task view of a 1-node-per-task split still has <= 2 globals per row
+    _check(A, cfg.M, cfg.spec.n, cfg.spec.n, 4, seed=3)
+
+
+def test_wavefront_galerkin_levels_bitwise():
+    cfg, s = _system("C2", 31, 8)
+    h = pd.build_hierarchy(s, "SMG", 4, 2, partitions=2)
+    assert h.wavefront == [True, True, True]
+    spec = cfg.spec
+    for l, A in enumerate(h.matrices[:-1]):
+        _check(A, cfg.M, spec.n, spec.n, 2, seed=l)
+        spec = spec.coarse()
+
+
+def test_wavefront_rejects_mismatched_layout():
+    cfg, s = _system("C2", 15, 4)
+    ilu = pd.Ilu0(s.global_matrix())
+    assert not ilu.set_wavefront(3, 14, 15)  # task size does not divide the system
+    b = np.ones(s.size)
+    np.testing.assert_array_equal(ilu.solve(b), O.OIlu0(pd.linalg.as_csr(s.global_matrix())).solve(b))
+
+
+@pytest.mark.parametrize("strategy", ["SMG", "STMG"])
+def test_wavefront_mg_bitwise_vs_level_sweeps(monkeypatch, strategy):
+    """Same V-cycles with and without the wavefront executor: bitwise equal.
+
+    SMG levels all take the wavefront path; STMG's time-coarsened level couples
+    to every node of the previous coarse step (too many cross-task entries) and
+    keeps the level-scheduled sweeps.
+    """
+    cfg, s = _system("C2", 31, 8)
+    b = s.rhs()
+    out = {}
+    for mode in ("level", "wavefront"):
+        if mode == "level":
+            monkeypatch.setenv("PD_NO_WAVEFRONT", "1")
+        else:
+            monkeypatch.delenv("PD_NO_WAVEFRONT", raising=False)
+        h = pd.build_hierarchy(s, strategy, 3, 2, partitions=2)
+        if mode == "level":
+            assert h.wavefront == [False, False]
+        else:
+            assert h.wavefront == ([True, True] if strategy == "SMG" else [True, False])
+        out[mode] = h.solve(b, tol_rel=1e-10, tol_abs=1e-10)
+    (x1, r1), (x2, r2) = out["level"], out["wavefront"]
+    assert r1.iterations == r2.iterations and r1.converged
+    np.testing.assert_array_equal(x1, x2)
