@@ -56,7 +56,7 @@ constexpr int kChunk = 4;       // entries loaded together before their multiply
 // dthread for in-task results, (R + j)*Tp for the thread's polled cross-task
 // slots.  Every entry is then one conflict-free shared load.
 constexpr int kRmax = 16;
-constexpr int kRegEnt = 16;
+constexpr int kOffPad = 16;     // offset rows: at least this many entries, multiple of 8
 constexpr unsigned kBulkPieces = 8;  // bulk copy requests per step block     // entry offsets of the next row held in registers
 
 struct WfDev {
@@ -111,6 +111,12 @@ __device__ __forceinline__ unsigned long long ld_strong_if(bool pred, const doub
         : "l"(p), "r"((unsigned)pred)
         : "memory");
     return v;
+}
+__device__ __forceinline__ void st_strong4(double* p, double a, double b, double c, double d) {
+    asm volatile("st.relaxed.gpu.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p),
+                 "l"(__double_as_longlong(a)), "l"(__double_as_longlong(b)),
+                 "l"(__double_as_longlong(c)), "l"(__double_as_longlong(d))
+                 : "memory");
 }
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
     return (unsigned)__cvta_generic_to_shared(p);
@@ -234,15 +240,19 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1) k_wf_sweep(WfDev
         };
         const int64_t qline = P.q0[task] + (int64_t)t * P.npoint;  // sweep position of x = 0
         int seq = 0, phase = 0;  // rows done on this line, and seq mod R
+        // results are published per aligned 4-row sector (one 32-byte store instead
+        // of four scattered 8-byte ones); a line's last rows are flushed at its end
+        double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+        int wcnt = 0;
+        const bool y32 = (reinterpret_cast<uintptr_t>(y) & 31) == 0;
         double xs[NG], xn[NG];
         double bn = 0.0;
         // The thread's next row, prepared one step ahead: right-hand side and
         // cross-task values (loads that land while the current step computes;
         // unconditional or predicated inside one instruction, so no select
-        // waits on them), entry count and source offsets (registers).
+        // waits on them) and its entry counts.
         int n_len = 0, n_ng = 0;
-        uint32_t n_off[kRegEnt / 2];
-        auto prefetch = [&](const RowView& v, int64_t q, int ph) {
+        auto prefetch = [&](const RowView& v, int64_t q) {
             int64_t row = 0;
             const int32_t* pat = spat;
             n_len = 0;
@@ -252,16 +262,6 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1) k_wf_sweep(WfDev
                 pat = spat + v.pid * kPatHdr;
                 n_len = pat[0];
                 n_ng = pat[1];
-                const uint4* o4 =
-                    reinterpret_cast<const uint4*>(soff + ((size_t)v.pid * R + ph) * pwo);
-#pragma unroll
-                for (int k = 0; k < kRegEnt / 8; ++k) {
-                    const uint4 w = o4[k];
-                    n_off[4 * k] = w.x;
-                    n_off[4 * k + 1] = w.y;
-                    n_off[4 * k + 2] = w.z;
-                    n_off[4 * k + 3] = w.w;
-                }
             }
             bn = b[row];
 #pragma unroll
@@ -272,23 +272,19 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1) k_wf_sweep(WfDev
         };
         RowView nv = view_row(block_of(0), g, line);
         nv.active = nv.active && lane;
-        prefetch(nv, qline, 0);
+        prefetch(nv, qline);
         for (int s = 0; s < S; ++s) {
             // refill the stage freed by step s-1 (everyone passed the barrier)
             if (t == 0 && s + kStages - 1 < S) issue(s + kStages - 1);
             const RowView cv = nv;
             const double bb = bn;
             const int len = n_len, ng = n_ng;
-            uint32_t off[kRegEnt / 2];
-#pragma unroll
-            for (int k = 0; k < kRegEnt / 2; ++k) off[k] = n_off[k];
 #pragma unroll
             for (int j = 0; j < NG; ++j) xs[j] = xn[j];
             if (s + 1 < S) {
                 nv = view_row(block_of(s + 1), g, line);
                 nv.active = nv.active && lane;
-                const int nph = cv.active ? (phase + 1 == R ? 0 : phase + 1) : phase;
-                prefetch(nv, qline + seq + (cv.active ? 1 : 0), nph);
+                prefetch(nv, qline + seq + (cv.active ? 1 : 0));
             }
             if (cv.active) {
                 const int64_t q = qline + seq;
@@ -311,29 +307,44 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1) k_wf_sweep(WfDev
                         }
                 }
                 double acc = bb;
-#pragma unroll
-                for (int k0 = 0; k0 < kRegEnt; k0 += kChunk) {
-                    if (k0 >= len) break;  // a branch, not kRegEnt predicated slots
+                const int16_t* off = soff + ((size_t)cv.pid * R + phase) * pwo;
+                for (int k0 = 0; k0 < len; k0 += kChunk) {
+                    const short4 o = *reinterpret_cast<const short4*>(off + k0);
+                    const int oi[kChunk] = {o.x, o.y, o.z, o.w};
                     double v[kChunk], f[kChunk];
 #pragma unroll
                     for (int k = 0; k < kChunk; ++k)
                         if (k0 + k < len) {
-                            const uint32_t w = off[(k0 + k) >> 1];
-                            const int o = (int)(short)(((k0 + k) & 1) ? (w >> 16) : (w & 0xffffu));
-                            v[k] = myring[o];
+                            v[k] = myring[oi[k]];
                             f[k] = cv.val[(size_t)(k0 + k) * cv.cnt];
                         }
 #pragma unroll
                     for (int k = 0; k < kChunk; ++k)
                         if (k0 + k < len) acc = sub(acc, mul(f[k], v[k]));
                 }
-                if (len > kRegEnt) {  // long rows: remaining offsets from shared memory
-                    const int16_t* o2 = soff + ((size_t)cv.pid * R + phase) * pwo;
-                    for (int k = kRegEnt; k < len; ++k)
-                        acc = sub(acc, mul(cv.val[(size_t)k * cv.cnt], myring[o2[k]]));
-                }
                 if (UPPER) acc = acc / cv.dval[0];
-                st_strong(y + row, acc);
+                {
+                    const int sl = (int)(row & 3);
+                    w0 = sl == 0 ? acc : w0;
+                    w1 = sl == 1 ? acc : w1;
+                    w2 = sl == 2 ? acc : w2;
+                    w3 = sl == 3 ? acc : w3;
+                    ++wcnt;
+                    if ((UPPER ? sl == 0 : sl == 3) || seq + 1 == P.npoint) {
+                        const int64_t g0 = row & ~(int64_t)3;
+                        if (wcnt == 4 && y32) {
+                            st_strong4(y + g0, w0, w1, w2, w3);
+                        } else {  // partial sector: rows [lo, hi] of this group
+                            const int lo = UPPER ? sl : sl - wcnt + 1;
+                            const int hi = UPPER ? sl + wcnt - 1 : sl;
+                            if (lo <= 0 && 0 <= hi) st_strong(y + g0, w0);
+                            if (lo <= 1 && 1 <= hi) st_strong(y + g0 + 1, w1);
+                            if (lo <= 2 && 2 <= hi) st_strong(y + g0 + 2, w2);
+                            if (lo <= 3 && 3 <= hi) st_strong(y + g0 + 3, w3);
+                        }
+                        wcnt = 0;
+                    }
+                }
                 myring[phase * Tp] = acc;
                 ++seq;
                 phase = (phase + 1 == R) ? 0 : phase + 1;
@@ -424,7 +435,7 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
         while (xc + r < npoint && step[qc + r] <= step[q]) ++r;
         return r;
     };
-    int64_t R = 1;
+    int64_t R = 4;  // >= 4: an in-task entry read back from global memory is flushed
     for (int64_t q = 0; q < n; ++q) {
         int64_t p0, p1;
         ent(row_of(q), p0, p1);
@@ -485,7 +496,7 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
     }
     int maxlen = 1;
     for (auto& pt : pats) maxlen = std::max(maxlen, pt[0]);
-    const int pwo = (int)align_up(std::max(maxlen, kRegEnt), 8);
+    const int pwo = (int)align_up(std::max(maxlen, kOffPad), 8);
     hp.pwo = pwo;
     hp.pattern.assign(pats.size() * kPatHdr, 0);
     hp.offs.assign(pats.size() * R * pwo, 0);
