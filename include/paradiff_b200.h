@@ -64,11 +64,12 @@ int pd_ilu0_levels(void *ilu, int32_t *lower_levels, int32_t *upper_levels); /* 
  * one CTA per task, one thread per (grid, line), in-task dependencies through
  * shared memory, per-step factor values staged by TMA bulk copies.  Same
  * arithmetic as pd_ilu0_solve (bitwise); *applied = 0 when the schedule does
- * not fit (the level-scheduled sweeps stay in use).  ring <= 0 selects the
- * default ring depth (8).  A faster schedule for linalg.py:104-113; the
- * reference has no counterpart. */
+ * not fit (the level-scheduled sweeps stay in use).  ngroup_lower > 0 lets a
+ * lower-sweep task span ngroup_lower grids (several time steps: their time
+ * coupling then stays inside the CTA); 0 = ngroup.  A faster schedule for
+ * linalg.py:104-113; the reference has no counterpart. */
 int pd_ilu0_set_wavefront(void *ctx, void *ilu, int64_t ngroup, int64_t nline, int64_t npoint,
-                          int ring, int *applied);                    /* synchronising */
+                          int64_t ngroup_lower, int *applied);                    /* synchronising */
 int pd_ilu0_destroy(void *ilu);
 
 /* ---- dense LU of the coarsest level (linalg.py:196-209 DenseLU) ---------- */

@@ -120,11 +120,11 @@ int pd_ilu0_levels(void* ilu, int32_t* lo, int32_t* up) {
     });
 }
 int pd_ilu0_set_wavefront(void* ctx, void* ilu, int64_t ngroup, int64_t nline, int64_t npoint,
-                          int ring, int* applied) {
+                          int64_t ngroup_lower, int* applied) {
     return guarded([&] {
         auto* c = H<pd::Ctx>(ctx, "ctx");
         auto* f = H<pd::Ilu0>(ilu, "ilu");
-        const bool ok = pd::ilu0_set_wavefront(*c, *f, ngroup, nline, npoint, ring);
+        const bool ok = pd::ilu0_set_wavefront(*c, *f, ngroup, nline, npoint, ngroup_lower);
         if (applied) *applied = ok ? 1 : 0;
     });
 }

@@ -109,7 +109,7 @@ struct Csr {
 struct WfPlan {
     int64_t n = 0, nslot = 0;
     int ntask = 0, T = 0, nline = 0, npoint = 0, R = 0, pwo = 0, maxS = 0, blocks = 0, npat = 0,
-        ng = 0;
+        ng = 0, gu = 1, threads = 0;
     size_t smem = 0, stage_bytes = 0;
     DevBuf<int32_t> nsteps;
     DevBuf<int64_t> boff, bofs, q0;
@@ -178,7 +178,7 @@ void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard = 
                 int want = 0);
 // structured wavefront sweeps (pd_wavefront.cu): false = schedule not applicable
 bool ilu0_set_wavefront(Ctx& c, Ilu0& f, int64_t ngroup, int64_t nline, int64_t npoint,
-                        int ring);
+                        int64_t ngroup_lower);
 void wf_gather(Ctx& c, Ilu0& f);
 // fill a sweep output with the value-as-flag pending sentinel (coalesced)
 void arm_pending(Ctx& c, double* y, int64_t n, const int* guard, int want);  // refresh plan values after a (re)factorization

@@ -42,12 +42,13 @@ using namespace dev;
 namespace {
 
 constexpr int kStages = 3;      // staged step blocks (TMA bulk copies kStages-1 ahead)
-constexpr int kMaxGroups = 8;   // node grids per task
+constexpr int kMaxGroups = 24;  // node grids per task (M nodes x time steps)
 // cross-task (global) entries per row, prefetched one step ahead: kNgFine for
 // fine-level stencils (Jq couples one point), kNgWide for Galerkin levels
 // (R Mh P couples a 3x3 neighbourhood of the previous time step)
 constexpr int kNgFine = 2, kNgWide = 10;
-constexpr int kHdrInts = 6 * kMaxGroups;  // lo, cnt, W, pid_off, val_off, dval_off per group
+// step-block header: per group int4 {lo, cnt, pid_off, val_off}, then dval_off[G] (16-B padded)
+constexpr int hdr_ints(int G) { return (5 * G + 3) & ~3; }
 constexpr uint16_t kIdle = 0xFFFF;
 constexpr int kChunk = 4;       // entries loaded together before their multiply/subtract chain
 // Patterns: header [len, ng, goff[NG]] (int32) and, per ring phase (x mod R),
@@ -69,7 +70,7 @@ struct WfDev {
     const unsigned char* blob;
     unsigned long long* trace;
     int64_t n;
-    int ntask, T, nline, npoint, R, pwo, maxS, npat;
+    int ntask, T, nline, npoint, R, pwo, maxS, npat, G;
     size_t stage_bytes;
 };
 
@@ -92,6 +93,7 @@ WfDev wf_dev(WfPlan& p) {
     d.pwo = p.pwo;
     d.maxS = p.maxS;
     d.npat = p.npat;
+    d.G = p.T / p.nline;
     d.stage_bytes = p.stage_bytes;
     return d;
 }
@@ -155,66 +157,102 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
         : "memory");
 }
 
-struct RowView {  // this thread's slot in one step block
-    bool active;
-    int W, cnt, i;
-    const double* val;   // entry k at val[k * cnt]
-    const double* dval;  // upper diagonal
-    int pid;
-};
-
-__device__ __forceinline__ RowView view_row(const unsigned char* blk, int g, int line) {
-    const int32_t* h = reinterpret_cast<const int32_t*>(blk);
-    RowView v;
-    const int lo = h[g], cnt = h[kMaxGroups + g];
-    v.active = false;
-    v.cnt = cnt;
-    v.W = 0;
-    v.i = 0;
-    v.pid = kIdle;
-    v.val = v.dval = nullptr;
-    if (line < lo || line >= lo + cnt) return v;
-    v.i = line - lo;
-    v.pid = reinterpret_cast<const uint16_t*>(blk + h[3 * kMaxGroups + g])[v.i];
-    if (v.pid == kIdle) return v;
-    v.active = true;
-    v.W = h[2 * kMaxGroups + g];
-    v.val = reinterpret_cast<const double*>(blk + h[4 * kMaxGroups + g]) + v.i;
-    v.dval = reinterpret_cast<const double*>(blk + h[5 * kMaxGroups + g]) + v.i;
+// 32-bit shared-memory accessors: LDS/STS on shared-window addresses (no
+// generic-address conversion, no 64-bit address arithmetic).  volatile keeps
+// them ordered against __syncthreads / mbarrier waits.
+__device__ __forceinline__ double lds_f64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
     return v;
 }
+__device__ __forceinline__ int lds_s32(unsigned a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ unsigned lds_u16(unsigned a) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int2 lds_v2s32(unsigned a) {
+    int2 v;
+    asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ int4 lds_v4s32(unsigned a) {
+    int4 v;
+    asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void lds_v4s16(unsigned a, int& o0, int& o1, int& o2, int& o3) {
+    short x0, x1, x2, x3;
+    asm volatile("ld.shared.v4.s16 {%0, %1, %2, %3}, [%4];"
+                 : "=h"(x0), "=h"(x1), "=h"(x2), "=h"(x3)
+                 : "r"(a));
+    o0 = x0;
+    o1 = x1;
+    o2 = x2;
+    o3 = x3;
+}
+__device__ __forceinline__ void sts_f64(unsigned a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
 
-// One CTA per task (a time step: up to kMaxGroups node grids), tickets in
-// topological order so a CTA only waits on tasks already claimed by running
-// CTAs.  Thread t = g*nline + line walks points x = 0.. of line `line` of node
-// grid g (in sweep order).
-template <bool UPPER, int NG>
-__global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1) k_wf_sweep(WfDev P, const double* b, double* y,
-                                                     unsigned long long* counter,
-                                                     const int* guard, int want) {
+// One CTA per task (up to kMaxGroups node grids: the M nodes of one or more
+// time steps), tickets in topological order so a CTA only waits on tasks
+// already claimed by running CTAs.  Virtual thread v = g*nline + line walks
+// points x = 0.. of line `line` of grid g (in sweep order); a real thread runs
+// GU virtual threads (the GU node grids of its line: rows of one step are
+// independent, so their chains interleave and every thread gets the same
+// node mix).  Shared memory is addressed through 32-bit shared-window offsets.
+template <bool UPPER, int NG, int GU>
+__global__ void __launch_bounds__(GU == 1 ? (NG <= kNgFine ? 768 : 512) : 256, 1)
+    k_wf_sweep(WfDev P, const double* __restrict__ b, double* y, unsigned long long* counter,
+               const int* guard, int want) {
     if (guard_off(guard, want)) return;
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ unsigned long long bar[kStages];
     __shared__ int s_ticket;
     constexpr int kPatHdr = 2 + NG;
-    const int T = P.T, R = P.R, RW = P.R + NG, pwo = P.pwo, t = threadIdx.x;
-    unsigned char* stage = sm;  // kStages * stage_bytes
-    const int Tp = (T + 31) & ~31;
-    // ring, slot-major [RW][Tp]: lanes of a warp always hit distinct banks
-    double* ring = reinterpret_cast<double*>(sm + kStages * P.stage_bytes);
-    int64_t* sbofs = reinterpret_cast<int64_t*>(ring + (size_t)Tp * RW);    // [maxS + 1]
-    int32_t* spat = reinterpret_cast<int32_t*>(                           // [npat][kPatHdr]
-        (reinterpret_cast<uintptr_t>(sbofs + P.maxS + 1) + 15) & ~(uintptr_t)15);
-    int16_t* soff = reinterpret_cast<int16_t*>(spat + P.npat * kPatHdr);   // [npat][R][pwo]
+    constexpr int NGA = NG > 0 ? NG : 1;
+    const int T = P.T, R = P.R, pwo = P.pwo, G = P.G, t = threadIdx.x;
+    const unsigned Tp = (unsigned)(T + 31) & ~31u, RW = (unsigned)(R + NG);
+    const unsigned sb = (unsigned)P.stage_bytes;
+    // layout (bytes from sm): stages | ring [RW][Tp] f64 | bofs [maxS+1] | patterns | offsets
+    const unsigned o_ring = kStages * sb;
+    const unsigned o_bofs = o_ring + Tp * RW * 8u;
+    const unsigned o_pat = (o_bofs + (unsigned)(P.maxS + 1) * 8u + 15u) & ~15u;
+    const unsigned o_off = o_pat + (unsigned)(P.npat * kPatHdr) * 4u;
+    int64_t* sbofs = reinterpret_cast<int64_t*>(sm + o_bofs);
+    int32_t* spat = reinterpret_cast<int32_t*>(sm + o_pat);
+    int16_t* soff = reinterpret_cast<int16_t*>(sm + o_off);
     for (int i = t; i < P.npat * kPatHdr; i += blockDim.x) spat[i] = P.pattern[i];
     for (int i = t; i < P.npat * R * pwo; i += blockDim.x) soff[i] = P.offs[i];
-    const bool lane = t < T;
-    const int g = lane ? t / P.nline : 0, line = lane ? t % P.nline : -1;
-    double* myring = ring + (lane ? t : 0);
+    const unsigned u0 = smem_u32(sm);
+    const unsigned u_pat = u0 + o_pat, u_off = u0 + o_off;
+    const int nthr = T / GU;  // real threads with work
+    const bool lane = t < nthr;
+    const int line = lane ? t % P.nline : 0, tsub = lane ? t / P.nline : 0;
+    int gj[GU];
+    unsigned ringj[GU];
+    int qlj[GU];
+#pragma unroll
+    for (int j = 0; j < GU; ++j) {
+        gj[j] = tsub * GU + j;
+        ringj[j] = u0 + o_ring + (unsigned)(gj[j] * P.nline + line) * 8u;
+    }
+    const unsigned ring_step = Tp * 8u;             // bytes between ring slots
+    const unsigned off_row = (unsigned)pwo * 2u;    // bytes per (pattern, phase) offset row
+    const unsigned off_pat = (unsigned)R * off_row;  // bytes per pattern
     if (t == 0)
         for (int k = 0; k < kStages; ++k) mbar_init(&bar[k]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     unsigned uses = 0;  // blocks consumed by this CTA so far (stage = uses % kStages)
+    const int n = (int)P.n;
+    const bool y32 = (reinterpret_cast<uintptr_t>(y) & 31) == 0;
     for (;;) {
         __syncthreads();
         if (t == 0) s_ticket = (int)atomicAdd(counter, 1ull);
@@ -228,126 +266,174 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1) k_wf_sweep(WfDev
         __syncthreads();
         auto issue = [&](int s) {
             const unsigned st = (uses + s) % kStages;
-            bulk_load(stage + st * P.stage_bytes, P.blob + sbofs[s],
-                      (unsigned)(sbofs[s + 1] - sbofs[s]), &bar[st]);
+            bulk_load(sm + st * sb, P.blob + sbofs[s], (unsigned)(sbofs[s + 1] - sbofs[s]),
+                      &bar[st]);
         };
         if (t == 0)
             for (int s = 0; s < kStages - 1 && s < S; ++s) issue(s);
-        auto block_of = [&](int s) -> const unsigned char* {
+        auto block_of = [&](int s) -> unsigned {
             const unsigned k = uses + s;
             mbar_wait(&bar[k % kStages], (k / kStages) & 1u);
-            return stage + (k % kStages) * P.stage_bytes;
+            return u0 + (k % kStages) * sb;
         };
-        const int64_t qline = P.q0[task] + (int64_t)t * P.npoint;  // sweep position of x = 0
-        int seq = 0, phase = 0;  // rows done on this line, and seq mod R
-        // results are published per aligned 4-row sector (one 32-byte store instead
-        // of four scattered 8-byte ones); a line's last rows are flushed at its end
-        double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
-        int wcnt = 0;
-        const bool y32 = (reinterpret_cast<uintptr_t>(y) & 31) == 0;
-        double xs[NG], xn[NG];
-        double bn = 0.0;
-        // The thread's next row, prepared one step ahead: right-hand side and
-        // cross-task values (loads that land while the current step computes;
-        // unconditional or predicated inside one instruction, so no select
-        // waits on them) and its entry counts.
-        int n_len = 0, n_ng = 0;
-        auto prefetch = [&](const RowView& v, int64_t q) {
-            int64_t row = 0;
-            const int32_t* pat = spat;
-            n_len = 0;
-            n_ng = 0;
-            if (v.active) {
-                row = UPPER ? P.n - 1 - q : q;
-                pat = spat + v.pid * kPatHdr;
-                n_len = pat[0];
-                n_ng = pat[1];
-            }
-            bn = b[row];
+        const int q0 = (int)P.q0[task];
+        // per virtual thread: rows done on its line, ring phase, pending result sector
+        int seq[GU];
+        unsigned phase_b[GU], ring_ph[GU];
+        double w0[GU], w1[GU], w2[GU], w3[GU];
+        int wcnt[GU];
+        // the next row of each virtual thread, prepared one step ahead: descriptor,
+        // right-hand side and cross-task values (loads land while this step computes)
+        bool n_act[GU];
+        unsigned n_val[GU], n_stride[GU], n_dval[GU], n_pat[GU], n_ph[GU];
+        int n_len[GU], n_ng[GU];
+        double bn[GU], xn[GU][NGA];
 #pragma unroll
-            for (int j = 0; j < NG; ++j)
-                xn[j] = __longlong_as_double((long long)ld_strong_if(
-                    j < n_ng, y + row + (j < n_ng ? pat[2 + j] : 0),
-                    (unsigned long long)kPending));
+        for (int j = 0; j < GU; ++j) {
+            qlj[j] = q0 + (gj[j] * P.nline + line) * P.npoint;  // sweep position of x = 0
+            seq[j] = 0;
+            phase_b[j] = ring_ph[j] = 0;
+            w0[j] = w1[j] = w2[j] = w3[j] = 0.0;
+            wcnt[j] = 0;
+        }
+        auto view = [&](unsigned blk, int j, int q) {
+            const int4 h = lds_v4s32(blk + 16u * (unsigned)gj[j]);  // lo, cnt, pid_off, val_off
+            const int i = line - h.x;
+            bool act = lane && (unsigned)i < (unsigned)h.y;
+            unsigned pid = kIdle;
+            if (act) pid = lds_u16(blk + (unsigned)h.z + 2u * (unsigned)i);
+            act = act && pid != kIdle;
+            n_act[j] = act;
+            n_val[j] = blk + (unsigned)h.w + 8u * (unsigned)i;
+            n_stride[j] = 8u * (unsigned)h.y;
+            if (UPPER)
+                n_dval[j] = blk + (unsigned)lds_s32(blk + 16u * G + 4u * gj[j]) + 8u * (unsigned)i;
+            n_len[j] = 0;
+            n_ng[j] = 0;
+            int row = 0;
+            const unsigned pat = u_pat + pid * (unsigned)(kPatHdr * 4);
+            n_ph[j] = pat;
+            n_pat[j] = u_off + pid * off_pat;
+            if (act) {
+                const int2 lg = lds_v2s32(pat);
+                n_len[j] = lg.x;
+                n_ng[j] = lg.y;
+                row = UPPER ? n - 1 - q : q;
+            }
+            bn[j] = __ldg(b + row);
+#pragma unroll
+            for (int k = 0; k < NG; ++k) {
+                const bool pk = k < n_ng[j];
+                const int go = pk ? lds_s32(pat + 8u + 4u * k) : 0;
+                xn[j][k] = __longlong_as_double(
+                    (long long)ld_strong_if(pk, y + row + go, (unsigned long long)kPending));
+            }
         };
-        RowView nv = view_row(block_of(0), g, line);
-        nv.active = nv.active && lane;
-        prefetch(nv, qline);
+        {
+            const unsigned blk = block_of(0);
+#pragma unroll
+            for (int j = 0; j < GU; ++j) view(blk, j, qlj[j]);
+        }
         for (int s = 0; s < S; ++s) {
             // refill the stage freed by step s-1 (everyone passed the barrier)
             if (t == 0 && s + kStages - 1 < S) issue(s + kStages - 1);
-            const RowView cv = nv;
-            const double bb = bn;
-            const int len = n_len, ng = n_ng;
+            bool act[GU];
+            unsigned val[GU], stride[GU], dval[GU], pat[GU], ph[GU];
+            int len[GU], ng[GU];
+            double bb[GU], xs[GU][NGA];
 #pragma unroll
-            for (int j = 0; j < NG; ++j) xs[j] = xn[j];
-            if (s + 1 < S) {
-                nv = view_row(block_of(s + 1), g, line);
-                nv.active = nv.active && lane;
-                prefetch(nv, qline + seq + (cv.active ? 1 : 0));
+            for (int j = 0; j < GU; ++j) {
+                act[j] = n_act[j];
+                val[j] = n_val[j];
+                stride[j] = n_stride[j];
+                dval[j] = n_dval[j];
+                pat[j] = n_pat[j];
+                ph[j] = n_ph[j];
+                len[j] = n_len[j];
+                ng[j] = n_ng[j];
+                bb[j] = bn[j];
+#pragma unroll
+                for (int k = 0; k < NG; ++k) xs[j][k] = xn[j][k];
             }
-            if (cv.active) {
-                const int64_t q = qline + seq;
-                const int64_t row = UPPER ? P.n - 1 - q : q;
-                // cross-task values: wait until published, then into the own slots
-                if (ng > 0) {
-                    const int32_t* pat = spat + cv.pid * kPatHdr;
+            if (s + 1 < S) {
+                const unsigned blk = block_of(s + 1);
 #pragma unroll
-                    for (int j = 0; j < NG; ++j)
-                        if (j < ng) {
+                for (int j = 0; j < GU; ++j) view(blk, j, qlj[j] + seq[j] + (act[j] ? 1 : 0));
+            }
+#pragma unroll
+            for (int j = 0; j < GU; ++j) {
+                if (!act[j]) continue;
+                const int q = qlj[j] + seq[j];
+                const int row = UPPER ? n - 1 - q : q;
+                // cross-task values: wait until published, then into the own slots
+                if (NG > 0 && ng[j] > 0) {
+#pragma unroll
+                    for (int k = 0; k < NG; ++k)
+                        if (k < ng[j]) {
                             unsigned long long u =
-                                (unsigned long long)__double_as_longlong(xs[j]);
-                            unsigned int ns = 32;
-                            while (u == kPending) {
-                                __nanosleep(ns);
-                                if (ns < 256) ns <<= 1;
-                                u = ld_strong_u64(y + row + pat[2 + j]);
+                                (unsigned long long)__double_as_longlong(xs[j][k]);
+                            if (u == kPending) {
+                                const int go = lds_s32(ph[j] + 8u + 4u * k);
+                                unsigned int ns = 32;
+                                do {
+                                    __nanosleep(ns);
+                                    if (ns < 256) ns <<= 1;
+                                    u = ld_strong_u64(y + row + go);
+                                } while (u == kPending);
                             }
-                            myring[(R + j) * Tp] = __longlong_as_double((long long)u);
+                            sts_f64(ringj[j] + (unsigned)(R + k) * ring_step,
+                                    __longlong_as_double((long long)u));
                         }
                 }
-                double acc = bb;
-                const int16_t* off = soff + ((size_t)cv.pid * R + phase) * pwo;
-                for (int k0 = 0; k0 < len; k0 += kChunk) {
-                    const short4 o = *reinterpret_cast<const short4*>(off + k0);
-                    const int oi[kChunk] = {o.x, o.y, o.z, o.w};
+                double acc = bb[j];
+                const unsigned orow = pat[j] + phase_b[j];
+                unsigned fa = val[j];
+#pragma unroll 1
+                for (int k0 = 0; k0 < len[j]; k0 += kChunk) {
+                    int o0, o1, o2, o3;
+                    lds_v4s16(orow + 2u * (unsigned)k0, o0, o1, o2, o3);
+                    const int oi[kChunk] = {o0, o1, o2, o3};
                     double v[kChunk], f[kChunk];
 #pragma unroll
                     for (int k = 0; k < kChunk; ++k)
-                        if (k0 + k < len) {
-                            v[k] = myring[oi[k]];
-                            f[k] = cv.val[(size_t)(k0 + k) * cv.cnt];
+                        if (k0 + k < len[j]) {
+                            v[k] = lds_f64(ringj[j] + 8u * (unsigned)oi[k]);
+                            f[k] = lds_f64(fa + (unsigned)k * stride[j]);
                         }
 #pragma unroll
                     for (int k = 0; k < kChunk; ++k)
-                        if (k0 + k < len) acc = sub(acc, mul(f[k], v[k]));
+                        if (k0 + k < len[j]) acc = sub(acc, mul(f[k], v[k]));
+                    fa += kChunk * stride[j];
                 }
-                if (UPPER) acc = acc / cv.dval[0];
+                if (UPPER) acc = acc / lds_f64(dval[j]);
                 {
-                    const int sl = (int)(row & 3);
-                    w0 = sl == 0 ? acc : w0;
-                    w1 = sl == 1 ? acc : w1;
-                    w2 = sl == 2 ? acc : w2;
-                    w3 = sl == 3 ? acc : w3;
-                    ++wcnt;
-                    if ((UPPER ? sl == 0 : sl == 3) || seq + 1 == P.npoint) {
-                        const int64_t g0 = row & ~(int64_t)3;
-                        if (wcnt == 4 && y32) {
-                            st_strong4(y + g0, w0, w1, w2, w3);
+                    const int sl = row & 3;
+                    w0[j] = sl == 0 ? acc : w0[j];
+                    w1[j] = sl == 1 ? acc : w1[j];
+                    w2[j] = sl == 2 ? acc : w2[j];
+                    w3[j] = sl == 3 ? acc : w3[j];
+                    ++wcnt[j];
+                    if ((UPPER ? sl == 0 : sl == 3) || seq[j] + 1 == P.npoint) {
+                        double* g0 = y + (row & ~3);
+                        const int wc = wcnt[j];
+                        if (wc == 4 && y32) {
+                            st_strong4(g0, w0[j], w1[j], w2[j], w3[j]);
                         } else {  // partial sector: rows [lo, hi] of this group
-                            const int lo = UPPER ? sl : sl - wcnt + 1;
-                            const int hi = UPPER ? sl + wcnt - 1 : sl;
-                            if (lo <= 0 && 0 <= hi) st_strong(y + g0, w0);
-                            if (lo <= 1 && 1 <= hi) st_strong(y + g0 + 1, w1);
-                            if (lo <= 2 && 2 <= hi) st_strong(y + g0 + 2, w2);
-                            if (lo <= 3 && 3 <= hi) st_strong(y + g0 + 3, w3);
+                            const int lo = UPPER ? sl : sl - wc + 1;
+                            const int hi = UPPER ? sl + wc - 1 : sl;
+                            if (lo <= 0 && 0 <= hi) st_strong(g0, w0[j]);
+                            if (lo <= 1 && 1 <= hi) st_strong(g0 + 1, w1[j]);
+                            if (lo <= 2 && 2 <= hi) st_strong(g0 + 2, w2[j]);
+                            if (lo <= 3 && 3 <= hi) st_strong(g0 + 3, w3[j]);
                         }
-                        wcnt = 0;
+                        wcnt[j] = 0;
                     }
                 }
-                myring[phase * Tp] = acc;
-                ++seq;
-                phase = (phase + 1 == R) ? 0 : phase + 1;
+                sts_f64(ringj[j] + ring_ph[j], acc);
+                ++seq[j];
+                const bool wrap = phase_b[j] + off_row == off_pat;
+                phase_b[j] = wrap ? 0u : phase_b[j] + off_row;
+                ring_ph[j] = wrap ? 0u : ring_ph[j] + ring_step;
             }
             __syncthreads();
         }
@@ -402,8 +488,7 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
                 bool upper, int NG, HostPlan& hp) {
     const int kPatHdr = 2 + NG;
     const int64_t TR = (int64_t)G * nline * npoint, T = (int64_t)G * nline;
-    if (G < 1 || G > kMaxGroups || TR <= 0 || n % TR != 0 || n >= INT_MAX ||
-        T > (NG <= kNgFine ? 768 : 512))
+    if (G < 1 || G > kMaxGroups || TR <= 0 || n % TR != 0 || n >= INT_MAX || T > 4096)
         return plan_fail("1");
     const int64_t ntask = n / TR;
     auto row_of = [&](int64_t q) { return upper ? n - 1 - q : q; };
@@ -534,23 +619,23 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
                 hi[gg] = std::max<int32_t>(hi[gg], ln);
                 W[gg] = std::max(W[gg], nent[q]);
             }
-            int32_t hdr[kHdrInts] = {0};
-            size_t off = kHdrInts * 4;
-            for (int gg = 0; gg < kMaxGroups; ++gg) {
+            // header: per group int4 {lo, cnt, pid_off, val_off}, then dval_off[G]
+            std::vector<int32_t> hdr(hdr_ints(G), 0);
+            size_t off = hdr.size() * 4;
+            for (int gg = 0; gg < G; ++gg) {
                 cnt[gg] = hi[gg] >= lo[gg] ? hi[gg] - lo[gg] + 1 : 0;
-                hdr[gg] = cnt[gg] ? lo[gg] : 0;
-                hdr[kMaxGroups + gg] = cnt[gg];
-                hdr[2 * kMaxGroups + gg] = W[gg];
-                hdr[3 * kMaxGroups + gg] = (int32_t)off;
+                hdr[4 * gg] = cnt[gg] ? lo[gg] : 0;
+                hdr[4 * gg + 1] = cnt[gg];
+                hdr[4 * gg + 2] = (int32_t)off;
                 off += (size_t)cnt[gg] * 2;
             }
             off = align_up(off, 8);
-            for (int gg = 0; gg < kMaxGroups; ++gg) {
-                hdr[4 * kMaxGroups + gg] = (int32_t)off;
+            for (int gg = 0; gg < G; ++gg) {
+                hdr[4 * gg + 3] = (int32_t)off;
                 off += (size_t)cnt[gg] * W[gg] * 8;
             }
-            for (int gg = 0; gg < kMaxGroups; ++gg) {
-                hdr[5 * kMaxGroups + gg] = (int32_t)off;
+            for (int gg = 0; gg < G; ++gg) {
+                hdr[4 * G + gg] = (int32_t)off;
                 if (upper) off += (size_t)cnt[gg] * 8;
             }
             const size_t bytes = align_up(off, 16);
@@ -559,19 +644,19 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
             hp.bofs.push_back((int64_t)base);
             hp.blob.resize(base + bytes, 0);
             unsigned char* blk = hp.blob.data() + base;
-            std::memcpy(blk, hdr, sizeof(hdr));
-            for (int gg = 0; gg < kMaxGroups; ++gg)
+            std::memcpy(blk, hdr.data(), hdr.size() * 4);
+            for (int gg = 0; gg < G; ++gg)
                 for (int i = 0; i < cnt[gg]; ++i)
-                    reinterpret_cast<uint16_t*>(blk + hdr[3 * kMaxGroups + gg])[i] = kIdle;
+                    reinterpret_cast<uint16_t*>(blk + hdr[4 * gg + 2])[i] = kIdle;
             for (int64_t q : at[s]) {
                 const int64_t th = (q % TR) / npoint;
                 const int gg = (int)(th / nline), i = (int)(th % nline) - lo[gg];
-                reinterpret_cast<uint16_t*>(blk + hdr[3 * kMaxGroups + gg])[i] = pid[q];
+                reinterpret_cast<uint16_t*>(blk + hdr[4 * gg + 2])[i] = pid[q];
                 hp.srow.push_back((int32_t)row_of(q));
-                hp.sval.push_back((int64_t)(base + hdr[4 * kMaxGroups + gg]) / 8 + i);
+                hp.sval.push_back((int64_t)(base + hdr[4 * gg + 3]) / 8 + i);
                 hp.sstride.push_back(cnt[gg]);
                 hp.scount.push_back(nent[q]);
-                hp.sdiag.push_back((int64_t)(base + hdr[5 * kMaxGroups + gg]) / 8 + i);
+                hp.sdiag.push_back((int64_t)(base + hdr[4 * G + gg]) / 8 + i);
             }
         }
         hp.bofs.push_back((int64_t)hp.blob.size());
@@ -580,8 +665,8 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
     return true;
 }
 
-template <bool UPPER, int NG>
-bool configure_launch(Ctx& c, WfPlan& p) {
+template <bool UPPER, int NG, int GU>
+bool configure_launch_gu(Ctx& c, WfPlan& p) {
     constexpr int kPatHdr = 2 + NG;
     const size_t smem = kStages * p.stage_bytes +
                         (size_t)((p.T + 31) / 32 * 32) * (p.R + NG) * sizeof(double) +
@@ -590,22 +675,36 @@ bool configure_launch(Ctx& c, WfPlan& p) {
                         align_up((size_t)p.npat * p.R * p.pwo * sizeof(int16_t), 16);
     int dev_max = 0;
     PD_CUDA(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
-    if (smem + 1024 > (size_t)dev_max) return false;
+    const int threads = (p.T / GU + 31) / 32 * 32;
+    const int max_threads = GU == 1 ? (NG <= kNgFine ? 768 : 512) : 256;
+    if (getenv("PD_WF_VERBOSE"))
+        fprintf(stderr, "[wf] %s NG=%d GU=%d T=%d R=%d npat=%d pwo=%d stage=%zu smem=%zu (max %d)\n",
+                UPPER ? "upper" : "lower", NG, GU, p.T, p.R, p.npat, p.pwo, p.stage_bytes, smem,
+                dev_max);
+    if (smem + 1024 > (size_t)dev_max || threads > max_threads) return false;
     p.smem = smem;
     // the attribute is per kernel, shared by every plan: only ever raise it
     static size_t attr_max = 0;
     if (smem > attr_max) {
-        PD_CUDA(cudaFuncSetAttribute(k_wf_sweep<UPPER, NG>,
+        PD_CUDA(cudaFuncSetAttribute(k_wf_sweep<UPPER, NG, GU>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_max = smem;
     }
-    const int threads = (p.T + 31) / 32 * 32;
     int per_sm = 0;
-    PD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wf_sweep<UPPER, NG>, threads,
-                                                          smem));
+    PD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wf_sweep<UPPER, NG, GU>,
+                                                          threads, smem));
     if (per_sm < 1) return false;
     p.blocks = std::min(p.ntask, per_sm * c.sms);
+    p.gu = GU;
+    p.threads = threads;
     return true;
+}
+
+// GU > 1 (a thread running the node grids of its line) measured slower on
+// every C2 level (per-step chains lengthen; round-1 log): one row per thread.
+template <bool UPPER, int NG>
+bool configure_launch(Ctx& c, WfPlan& p) {
+    return configure_launch_gu<UPPER, NG, 1>(c, p);
 }
 
 void upload(WfPlan& p, HostPlan& hp, int64_t n, int G, int64_t nline, int64_t npoint) {
@@ -649,11 +748,14 @@ bool wavefront_disabled() {
 }  // namespace
 
 bool ilu0_set_wavefront(Ctx& c, Ilu0& f, int64_t ngroup, int64_t nline, int64_t npoint,
-                        int ring) {
+                        int64_t ngroup_lower) {
     f.wf_lo.reset();
     f.wf_up.reset();
     if (wavefront_disabled() || f.n == 0) return false;
-    (void)ring;  // ring depth is derived from the schedule (kept for the ABI)
+    // the lower sweep's tasks may span several time steps (in-task time coupling
+    // through the ring instead of cross-CTA polls); the upper factor has no time
+    // coupling, so its tasks stay one step each
+    const int64_t glo = ngroup_lower > 0 ? ngroup_lower : ngroup;
     const Csr& P = f.pat();
     const int64_t n = f.n;
     PD_CUDA(cudaStreamSynchronize(c.stream));
@@ -666,20 +768,22 @@ bool ilu0_set_wavefront(Ctx& c, Ilu0& f, int64_t ngroup, int64_t nline, int64_t 
         if (dg[i] < rp[i] || dg[i] >= rp[i + 1] || ci[dg[i]] != i) return false;
     auto lo = std::make_unique<WfPlan>();
     auto up = std::make_unique<WfPlan>();
-    auto build = [&](int NG) -> bool {
-        {
+    auto build = [&](bool upper, int64_t G, WfPlan& plan) -> bool {
+        for (int NG : {0, kNgFine, kNgWide}) {
             HostPlan hp;
-            if (!build_plan(rp, ci, dg, n, (int)ngroup, nline, npoint, false, NG, hp)) return false;
-            upload(*lo, hp, n, (int)ngroup, nline, npoint);
+            if (!build_plan(rp, ci, dg, n, (int)G, nline, npoint, upper, NG, hp)) continue;
+            upload(plan, hp, n, (int)G, nline, npoint);
+            const bool ok = NG == 0 ? (upper ? configure_launch<true, 0>(c, plan)
+                                             : configure_launch<false, 0>(c, plan))
+                : NG == kNgFine ? (upper ? configure_launch<true, kNgFine>(c, plan)
+                                         : configure_launch<false, kNgFine>(c, plan))
+                                : (upper ? configure_launch<true, kNgWide>(c, plan)
+                                         : configure_launch<false, kNgWide>(c, plan));
+            if (ok) return true;
         }
-        HostPlan hp;
-        if (!build_plan(rp, ci, dg, n, (int)ngroup, nline, npoint, true, NG, hp)) return false;
-        upload(*up, hp, n, (int)ngroup, nline, npoint);
-        if (NG == kNgFine)
-            return configure_launch<false, kNgFine>(c, *lo) && configure_launch<true, kNgFine>(c, *up);
-        return configure_launch<false, kNgWide>(c, *lo) && configure_launch<true, kNgWide>(c, *up);
+        return false;
     };
-    if (!build(kNgFine) && !build(kNgWide)) return false;
+    if (!build(false, glo, *lo) || !build(true, ngroup, *up)) return false;
     f.wf_lo = std::move(lo);
     f.wf_up = std::move(up);
     wf_gather(c, f);
@@ -737,6 +841,24 @@ static void wf_trace_report(Ctx& c, WfPlan& p, const char* name) {
             q(start, 1));
 }
 
+template <bool UPPER, int NG>
+static void launch_sweep_ng(Ctx& c, WfPlan& p, const double* b, double* y,
+                            unsigned long long* ctr, const int* guard, int want) {
+    launch(k_wf_sweep<UPPER, NG, 1>, p.blocks, p.threads, p.smem, c.stream, wf_dev(p), b, y, ctr,
+           guard, want);
+}
+
+template <bool UPPER>
+static void launch_sweep(Ctx& c, WfPlan& p, const double* b, double* y, unsigned long long* ctr,
+                         const int* guard, int want) {
+    if (p.ng == 0)
+        launch_sweep_ng<UPPER, 0>(c, p, b, y, ctr, guard, want);
+    else if (p.ng == kNgFine)
+        launch_sweep_ng<UPPER, kNgFine>(c, p, b, y, ctr, guard, want);
+    else
+        launch_sweep_ng<UPPER, kNgWide>(c, p, b, y, ctr, guard, want);
+}
+
 void wf_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int want) {
     WfPlan& lo = *f.wf_lo;
     WfPlan& up = *f.wf_up;
@@ -745,23 +867,13 @@ void wf_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int
         lo.trace.alloc(2 * (size_t)lo.ntask);
         up.trace.alloc(2 * (size_t)up.ntask);
     }
-    const int threads = (lo.T + 31) / 32 * 32;
-    arm_pending(c, f.scratch.p, f.n, guard, want);
+    // outputs are armed with the pending sentinel only when a sweep polls them
+    if (lo.ng > 0) arm_pending(c, f.scratch.p, f.n, guard, want);
     launch(k_wf_begin, 1, 1, 0, c.stream, f.counter.p, guard, want);
-    if (lo.ng == kNgFine)
-        launch(k_wf_sweep<false, kNgFine>, lo.blocks, threads, lo.smem, c.stream, wf_dev(lo), b,
-               f.scratch.p, f.counter.p, guard, want);
-    else
-        launch(k_wf_sweep<false, kNgWide>, lo.blocks, threads, lo.smem, c.stream, wf_dev(lo), b,
-               f.scratch.p, f.counter.p, guard, want);
-    arm_pending(c, x, f.n, guard, want);
+    launch_sweep<false>(c, lo, b, f.scratch.p, f.counter.p, guard, want);
+    if (up.ng > 0) arm_pending(c, x, f.n, guard, want);
     launch(k_wf_begin, 1, 1, 0, c.stream, f.counter.p, guard, want);
-    if (up.ng == kNgFine)
-        launch(k_wf_sweep<true, kNgFine>, up.blocks, threads, up.smem, c.stream, wf_dev(up),
-               (const double*)f.scratch.p, x, f.counter.p, guard, want);
-    else
-        launch(k_wf_sweep<true, kNgWide>, up.blocks, threads, up.smem, c.stream, wf_dev(up),
-               (const double*)f.scratch.p, x, f.counter.p, guard, want);
+    launch_sweep<true>(c, up, f.scratch.p, x, f.counter.p, guard, want);
     PD_LAUNCH_CHECK();
     if (trace) {
         wf_trace_report(c, lo, "lower");

@@ -139,9 +139,10 @@ class Ilu0:
         N.call("pd_ilu0_levels", self.handle, ctypes.byref(lo), ctypes.byref(up))
         return lo.value, up.value
 
-    def set_wavefront(self, ngroup: int, nline: int, npoint: int, ring: int = 0) -> bool:
-        """Structured wavefront sweeps for rows laid out [task][ngroup][nline][npoint]."""
-        return set_wavefront(self.ctx, self.handle, ngroup, nline, npoint, ring)
+    def set_wavefront(self, ngroup: int, nline: int, npoint: int, ngroup_lower: int = 0) -> bool:
+        """Structured wavefront sweeps for rows laid out [task][ngroup][nline][npoint]
+        (the lower sweep's tasks span `ngroup_lower` grids when > 0)."""
+        return set_wavefront(self.ctx, self.handle, ngroup, nline, npoint, ngroup_lower)
 
     def solve_dev(self, b, out=None):
         self.ctx.sync_stream()
@@ -160,10 +161,11 @@ class Ilu0:
             pass
 
 
-def set_wavefront(ctx, ilu_handle, ngroup: int, nline: int, npoint: int, ring: int = 0) -> bool:
+def set_wavefront(ctx, ilu_handle, ngroup: int, nline: int, npoint: int,
+                  ngroup_lower: int = 0) -> bool:
     applied = ctypes.c_int()
     N.call("pd_ilu0_set_wavefront", ctx.handle, ilu_handle, int(ngroup), int(nline), int(npoint),
-           int(ring), ctypes.byref(applied))
+           int(ngroup_lower), ctypes.byref(applied))
     return bool(applied.value)
 
 

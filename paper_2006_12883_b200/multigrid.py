@@ -12,6 +12,7 @@ V(nu,nu) cycles, the coarsest dense LU and the residual-stopped solve loop.
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from dataclasses import dataclass
 
@@ -154,6 +155,18 @@ def _build_transfers(dims: list[LevelDims], space_pairs) -> list[TransferSet]:
     return out
 
 
+def lower_task_steps(nt: int, m: int, nline: int, partitions: int, max_threads: int = 768):
+    """Time steps per lower-sweep wavefront task, largest first: divisors of a
+    block-Jacobi partition's step count whose thread count (m*k*nline) fits one
+    CTA; env PD_WF_LOWER_STEPS pins it (experiments)."""
+    env = os.environ.get("PD_WF_LOWER_STEPS")
+    if env:
+        return [int(env), 1]
+    per = nt // partitions if partitions > 0 and nt % partitions == 0 else 1
+    ks = [k for k in range(per, 0, -1) if per % k == 0 and m * k * nline <= max_threads]
+    return ks or [1]
+
+
 # ---------------------------------------------------------------- hierarchy
 class MultigridHierarchy:
     """Galerkin hierarchy whose smoothing, cycling and solving run on the GPU."""
@@ -252,7 +265,11 @@ class MultigridHierarchy:
             if g is not None:
                 ilu = ctypes.c_void_p()
                 N.call("pd_mg_level_precond", self._mg, l, ctypes.byref(ilu))
-                ok = set_wavefront(self.ctx, ilu, self.dims[l].m, g[0], g[1])
+                d = self.dims[l]
+                for k in lower_task_steps(d.nt, d.m, g[0], self.partitions):
+                    ok = set_wavefront(self.ctx, ilu, d.m, g[0], g[1], d.m * k)
+                    if ok:
+                        break
             self.wavefront.append(ok)
 
     # ---- device Newton refresh (§8(f)1) --------------------------------------

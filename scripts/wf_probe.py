@@ -16,6 +16,7 @@ from paper_2006_12883_b200 import _native as N
 
 Nt = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 level = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+ksteps = [int(k) for k in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1]
 cfg = pd.baseline_config("C2", Nt=Nt)
 s = pd.assemble_system(pd.make_tableau(3), pd.fd_space(cfg.spec), pd.TimeGrid(cfg.Nt, cfg.T),
                        0.0, cfg.u0())
@@ -47,10 +48,12 @@ def timed(reps=10):
 
 
 t_lvl, x_lvl = timed()
-t0 = time.perf_counter()
-ok = ilu.set_wavefront(3, spec.n, spec.n)
-t_plan = time.perf_counter() - t0
-t_wf, x_wf = timed()
-same = bool(torch.equal(x_lvl, x_wf))
-print(f"level={level} n={A.shape[0]} nnz={A.nnz} levels={ilu.levels()} plan_ok={ok} "
-      f"plan_s={t_plan:.2f} level_ms={t_lvl:.3f} wavefront_ms={t_wf:.3f} bitwise={same}")
+for k in ksteps:
+    t0 = time.perf_counter()
+    ok = ilu.set_wavefront(3, spec.n, spec.n, 3 * k)
+    t_plan = time.perf_counter() - t0
+    t_wf, x_wf = timed()
+    same = bool(torch.equal(x_lvl, x_wf))
+    print(f"level={level} k={k} n={A.shape[0]} nnz={A.nnz} levels={ilu.levels()} plan_ok={ok} "
+          f"plan_s={t_plan:.2f} level_ms={t_lvl:.3f} wavefront_ms={t_wf:.3f} bitwise={same}",
+          flush=True)

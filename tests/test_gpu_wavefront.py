@@ -23,11 +23,11 @@ def _system(name, n, Nt):
                                    pd.TimeGrid(cfg.Nt, cfg.T), 0.0, cfg.u0())
 
 
-def _check(A, ngroup, nline, npoint, parts, seed=0, repeats=2, applies=True):
+def _check(A, ngroup, nline, npoint, parts, seed=0, repeats=2, applies=True, ngroup_lower=0):
     A = pd.linalg.as_csr(A)
     rng = np.random.default_rng(seed)
     dev = pd.BlockJacobiPrecond(A, parts) if parts > 1 else pd.Ilu0(A)
-    assert dev.set_wavefront(ngroup, nline, npoint) == applies
+    assert dev.set_wavefront(ngroup, nline, npoint, ngroup_lower) == applies
     ref = O.OBlockJacobi(A, parts) if parts > 1 else O.OIlu0(A)
     for _ in range(repeats):  # repeated solves exercise the re-arming protocol
         b = rng.standard_normal(A.shape[0])
@@ -70,6 +70,16 @@ def test_wavefront_galerkin_levels_bitwise():
     for l, A in enumerate(h.matrices[:-1]):
         _check(A, cfg.M, spec.n, spec.n, 2, seed=l)
         spec = spec.coarse()
+
+
+@pytest.mark.parametrize("k", [2, 4])
+def test_wavefront_multistep_lower_tasks_bitwise(k):
+    """Lower-sweep tasks spanning k time steps (time coupling through the ring)."""
+    cfg, s = _system("C2", 15, 8)
+    _check(s.global_matrix(), cfg.M, cfg.spec.n, cfg.spec.n, 2, seed=k, ngroup_lower=cfg.M * k)
+    h = pd.build_hierarchy(s, "SMG", 3, 2, partitions=2)
+    spec = cfg.spec.coarse()
+    _check(h.matrices[1], cfg.M, spec.n, spec.n, 2, seed=k + 1, ngroup_lower=cfg.M * k)
 
 
 def test_wavefront_rejects_mismatched_layout():
