@@ -9,6 +9,7 @@ pointers only.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -16,7 +17,7 @@ import numpy as np
 
 from .errors import ConfigurationError, DeviceError, SolverError
 
-LIB_PATH = Path(__file__).resolve().parent / "libparadiff_b200.so"
+LIB_PATH = Path(os.environ.get("PD_LIB") or Path(__file__).resolve().parent / "libparadiff_b200.so")
 
 PD_OK, PD_ERR_CONFIG, PD_ERR_SOLVER, PD_ERR_CUDA = 0, 1, 2, 3
 

@@ -41,7 +41,8 @@ using namespace dev;
 
 namespace {
 
-constexpr int kStages = 3;      // staged step blocks (TMA bulk copies kStages-1 ahead)
+constexpr int kMaxStages = 16;  // staged step blocks (TMA bulk copies stages-1 ahead)
+constexpr int kMinStages = 2, kDefStages = 3;
 constexpr int kMaxGroups = 24;  // node grids per task (M nodes x time steps)
 // cross-task (global) entries per row, prefetched one step ahead: kNgFine for
 // fine-level stencils (Jq couples one point), kNgWide for Galerkin levels
@@ -70,7 +71,7 @@ struct WfDev {
     const unsigned char* blob;
     unsigned long long* trace;
     int64_t n;
-    int ntask, T, nline, npoint, R, pwo, maxS, npat, G;
+    int ntask, T, nline, npoint, R, pwo, maxS, npat, G, stages;
     size_t stage_bytes;
 };
 
@@ -94,6 +95,8 @@ WfDev wf_dev(WfPlan& p) {
     d.maxS = p.maxS;
     d.npat = p.npat;
     d.G = p.T / p.nline;
+    d.stages = p.stages;
+
     d.stage_bytes = p.stage_bytes;
     return d;
 }
@@ -208,13 +211,15 @@ __device__ __forceinline__ void sts_f64(unsigned a, double v) {
 // GU virtual threads (the GU node grids of its line: rows of one step are
 // independent, so their chains interleave and every thread gets the same
 // node mix).  Shared memory is addressed through 32-bit shared-window offsets.
-template <bool UPPER, int NG, int GU>
-__global__ void __launch_bounds__(GU == 1 ? (NG <= kNgFine ? 768 : 512) : 256, 1)
+template <bool UPPER, int NG, bool PAD>
+__global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
     k_wf_sweep(WfDev P, const double* __restrict__ b, double* y, unsigned long long* counter,
                const int* guard, int want) {
+    constexpr int GU = 1;  // virtual threads per thread (GU > 1 measured slower)
     if (guard_off(guard, want)) return;
     extern __shared__ __align__(128) unsigned char sm[];
-    __shared__ unsigned long long bar[kStages];
+    __shared__ unsigned long long bar[kMaxStages];
+    __shared__ unsigned long long bar_tab;
     __shared__ int s_ticket;
     constexpr int kPatHdr = 2 + NG;
     constexpr int NGA = NG > 0 ? NG : 1;
@@ -222,15 +227,16 @@ __global__ void __launch_bounds__(GU == 1 ? (NG <= kNgFine ? 768 : 512) : 256, 1
     const unsigned Tp = (unsigned)(T + 31) & ~31u, RW = (unsigned)(R + NG);
     const unsigned sb = (unsigned)P.stage_bytes;
     // layout (bytes from sm): stages | ring [RW][Tp] f64 | bofs [maxS+1] | patterns | offsets
-    const unsigned o_ring = kStages * sb;
-    const unsigned o_bofs = o_ring + Tp * RW * 8u;
+    const unsigned nst = (unsigned)P.stages;
+    const unsigned o_ring = nst * sb;
+    // PAD plans read an extra all-zero slot row; unpadded plans skip it (every KB
+    // counts: above 196 KB of shared memory the SM keeps no L1 for the b loads)
+    const unsigned o_bofs = o_ring + Tp * (RW + (PAD ? 1u : 0u)) * 8u;
     const unsigned o_pat = (o_bofs + (unsigned)(P.maxS + 1) * 8u + 15u) & ~15u;
-    const unsigned o_off = o_pat + (unsigned)(P.npat * kPatHdr) * 4u;
+    const unsigned pat_bytes = ((unsigned)(P.npat * kPatHdr) * 4u + 15u) & ~15u;
+    const unsigned off_bytes = ((unsigned)(P.npat * R * pwo) * 2u + 15u) & ~15u;
+    const unsigned o_off = o_pat + pat_bytes;
     int64_t* sbofs = reinterpret_cast<int64_t*>(sm + o_bofs);
-    int32_t* spat = reinterpret_cast<int32_t*>(sm + o_pat);
-    int16_t* soff = reinterpret_cast<int16_t*>(sm + o_off);
-    for (int i = t; i < P.npat * kPatHdr; i += blockDim.x) spat[i] = P.pattern[i];
-    for (int i = t; i < P.npat * R * pwo; i += blockDim.x) soff[i] = P.offs[i];
     const unsigned u0 = smem_u32(sm);
     const unsigned u_pat = u0 + o_pat, u_off = u0 + o_off;
     const int nthr = T / GU;  // real threads with work
@@ -247,10 +253,35 @@ __global__ void __launch_bounds__(GU == 1 ? (NG <= kNgFine ? 768 : 512) : 256, 1
     const unsigned ring_step = Tp * 8u;             // bytes between ring slots
     const unsigned off_row = (unsigned)pwo * 2u;    // bytes per (pattern, phase) offset row
     const unsigned off_pat = (unsigned)R * off_row;  // bytes per pattern
+    if (PAD)
+        for (unsigned i = t; i < Tp; i += blockDim.x)  // the zero slot row
+            reinterpret_cast<double*>(sm + o_ring)[RW * Tp + i] = 0.0;
     if (t == 0)
-        for (int k = 0; k < kStages; ++k) mbar_init(&bar[k]);
+        for (unsigned k = 0; k < nst; ++k) mbar_init(&bar[k]);
+    if (t == 0) mbar_init(&bar_tab);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    unsigned uses = 0;  // blocks consumed by this CTA so far (stage = uses % kStages)
+    __syncthreads();
+    // pattern and offset tables: two bulk copies (a per-thread copy loop costs
+    // ~100 us of dependent load->store latency on small CTAs)
+    if (t == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         smem_u32(&bar_tab)),
+                     "r"(pat_bytes + off_bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(u_pat),
+            "l"(P.pattern), "r"(pat_bytes), "r"(smem_u32(&bar_tab))
+            : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+            "[%3];" ::"r"(u_off),
+            "l"(P.offs), "r"(off_bytes), "r"(smem_u32(&bar_tab))
+            : "memory");
+    }
+    mbar_wait(&bar_tab, 0);
+    unsigned ist = 0;             // stage of the next bulk copy (thread 0)
+    unsigned wst = 0, wpar = 0;   // stage and mbarrier parity of the next block consumed
     const int n = (int)P.n;
     const bool y32 = (reinterpret_cast<uintptr_t>(y) & 31) == 0;
     for (;;) {
@@ -264,17 +295,23 @@ __global__ void __launch_bounds__(GU == 1 ? (NG <= kNgFine ? 768 : 512) : 256, 1
         const int64_t bo = P.boff[task];
         for (int s = t; s <= S; s += blockDim.x) sbofs[s] = P.bofs[bo + s];
         __syncthreads();
+        // blocks are issued and consumed in order, once each: running stage
+        // indices (no runtime division by the stage count)
         auto issue = [&](int s) {
-            const unsigned st = (uses + s) % kStages;
-            bulk_load(sm + st * sb, P.blob + sbofs[s], (unsigned)(sbofs[s + 1] - sbofs[s]),
-                      &bar[st]);
+            bulk_load(sm + ist * sb, P.blob + sbofs[s], (unsigned)(sbofs[s + 1] - sbofs[s]),
+                      &bar[ist]);
+            ist = ist + 1 == nst ? 0u : ist + 1;
         };
         if (t == 0)
-            for (int s = 0; s < kStages - 1 && s < S; ++s) issue(s);
-        auto block_of = [&](int s) -> unsigned {
-            const unsigned k = uses + s;
-            mbar_wait(&bar[k % kStages], (k / kStages) & 1u);
-            return u0 + (k % kStages) * sb;
+            for (int s = 0; s < (int)nst - 1 && s < S; ++s) issue(s);
+        auto block_of = [&](int) -> unsigned {
+            mbar_wait(&bar[wst], wpar);
+            const unsigned a = u0 + wst * sb;
+            if (++wst == nst) {
+                wst = 0;
+                wpar ^= 1u;
+            }
+            return a;
         };
         const int q0 = (int)P.q0[task];
         // per virtual thread: rows done on its line, ring phase, pending result sector
@@ -336,7 +373,7 @@ __global__ void __launch_bounds__(GU == 1 ? (NG <= kNgFine ? 768 : 512) : 256, 1
         }
         for (int s = 0; s < S; ++s) {
             // refill the stage freed by step s-1 (everyone passed the barrier)
-            if (t == 0 && s + kStages - 1 < S) issue(s + kStages - 1);
+            if (t == 0 && s + (int)nst - 1 < S) issue(s + (int)nst - 1);
             bool act[GU];
             unsigned val[GU], stride[GU], dval[GU], pat[GU], ph[GU];
             int len[GU], ng[GU];
@@ -388,6 +425,7 @@ __global__ void __launch_bounds__(GU == 1 ? (NG <= kNgFine ? 768 : 512) : 256, 1
                 double acc = bb[j];
                 const unsigned orow = pat[j] + phase_b[j];
                 unsigned fa = val[j];
+                // PAD: len is padded to kChunk with zero entries, no per-entry predicates
 #pragma unroll 1
                 for (int k0 = 0; k0 < len[j]; k0 += kChunk) {
                     int o0, o1, o2, o3;
@@ -396,13 +434,13 @@ __global__ void __launch_bounds__(GU == 1 ? (NG <= kNgFine ? 768 : 512) : 256, 1
                     double v[kChunk], f[kChunk];
 #pragma unroll
                     for (int k = 0; k < kChunk; ++k)
-                        if (k0 + k < len[j]) {
+                        if (PAD || k0 + k < len[j]) {
                             v[k] = lds_f64(ringj[j] + 8u * (unsigned)oi[k]);
                             f[k] = lds_f64(fa + (unsigned)k * stride[j]);
                         }
 #pragma unroll
                     for (int k = 0; k < kChunk; ++k)
-                        if (k0 + k < len[j]) acc = sub(acc, mul(f[k], v[k]));
+                        if (PAD || k0 + k < len[j]) acc = sub(acc, mul(f[k], v[k]));
                     fa += kChunk * stride[j];
                 }
                 if (UPPER) acc = acc / lds_f64(dval[j]);
@@ -437,7 +475,6 @@ __global__ void __launch_bounds__(GU == 1 ? (NG <= kNgFine ? 768 : 512) : 256, 1
             }
             __syncthreads();
         }
-        uses += (unsigned)S;
         if (P.trace && t == 0) P.trace[2 * task + 1] = globaltimer();
     }
 }
@@ -485,7 +522,7 @@ bool plan_fail(const char* why) {
 // builder: task = q / (G*nline*npoint), thread = (group, line), x = point.
 bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
                 const std::vector<int64_t>& dg, int64_t n, int G, int64_t nline, int64_t npoint,
-                bool upper, int NG, HostPlan& hp) {
+                bool upper, int NG, bool pad, HostPlan& hp) {
     const int kPatHdr = 2 + NG;
     const int64_t TR = (int64_t)G * nline * npoint, T = (int64_t)G * nline;
     if (G < 1 || G > kMaxGroups || TR <= 0 || n % TR != 0 || n >= INT_MAX || T > 4096)
@@ -534,7 +571,8 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
     const int64_t RW = R + NG, Tp = (T + 31) / 32 * 32;
     hp.R = (int)R;
     hp.ng = NG;
-    if (RW * Tp + Tp > 32767) return plan_fail("3");  // int16 offsets
+    // ring slots [RW + 1][Tp]: the extra slot row stays +0.0 (padded entries read it)
+    if ((RW + 1) * Tp + Tp > 32767) return plan_fail("3");  // int16 offsets
     // entry-source patterns, deduplicated: key = [len, ng, goff[NG], (dth, dx | global j)...]
     std::unordered_map<std::string, int> pid_of;
     std::vector<std::vector<int32_t>> pats;
@@ -585,16 +623,25 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
     hp.pwo = pwo;
     hp.pattern.assign(pats.size() * kPatHdr, 0);
     hp.offs.assign(pats.size() * R * pwo, 0);
+    // Entry lists are padded to a multiple of kChunk with (zero slot, +0.0 factor)
+    // entries: acc - (+0)*(+0) == acc bitwise for every acc, so the chunk loop
+    // needs no per-entry predication.  The pattern header stores the padded length.
+    const int16_t zero_off = (int16_t)(RW * Tp);
     for (size_t k = 0; k < pats.size(); ++k) {
         const auto& pt = pats[k];
         std::copy(pt.begin(), pt.begin() + kPatHdr, hp.pattern.begin() + k * kPatHdr);
+        const int lenp = pad ? (int)align_up(pt[0], kChunk) : pt[0];
+        hp.pattern[k * kPatHdr] = lenp;
         for (int64_t ph = 0; ph < R; ++ph)
-            for (int e = 0; e < pt[0]; ++e) {
-                const int32_t a = pt[kPatHdr + 2 * e], b2 = pt[kPatHdr + 2 * e + 1];
-                const int64_t off =
-                    a == INT_MIN ? (R + b2) * Tp : ((((ph + b2) % R) + R) % R) * Tp + a;
+            for (int e = 0; e < pwo; ++e) {
+                int64_t off = zero_off;
+                if (e < pt[0]) {
+                    const int32_t a = pt[kPatHdr + 2 * e], b2 = pt[kPatHdr + 2 * e + 1];
+                    off = a == INT_MIN ? (R + b2) * Tp : ((((ph + b2) % R) + R) % R) * Tp + a;
+                }
                 hp.offs[(k * R + ph) * pwo + e] = (int16_t)off;
             }
+        (void)lenp;
     }
     // step blocks: rows of (task, step) grouped per node grid, line-contiguous
     hp.boff.assign(ntask, 0);
@@ -617,7 +664,7 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
                 const int gg = (int)(th / nline), ln = (int)(th % nline);
                 lo[gg] = std::min<int32_t>(lo[gg], ln);
                 hi[gg] = std::max<int32_t>(hi[gg], ln);
-                W[gg] = std::max(W[gg], nent[q]);
+                W[gg] = std::max(W[gg], pad ? (int32_t)align_up(nent[q], kChunk) : nent[q]);
             }
             // header: per group int4 {lo, cnt, pid_off, val_off}, then dval_off[G]
             std::vector<int32_t> hdr(hdr_ints(G), 0);
@@ -665,46 +712,56 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
     return true;
 }
 
-template <bool UPPER, int NG, int GU>
-bool configure_launch_gu(Ctx& c, WfPlan& p) {
+template <bool UPPER, int NG, bool PAD>
+bool configure_launch_pad(Ctx& c, WfPlan& p) {
+    constexpr int GU = 1;
     constexpr int kPatHdr = 2 + NG;
-    const size_t smem = kStages * p.stage_bytes +
-                        (size_t)((p.T + 31) / 32 * 32) * (p.R + NG) * sizeof(double) +
-                        (size_t)(p.maxS + 1) * sizeof(int64_t) + 16 +
-                        (size_t)p.npat * kPatHdr * sizeof(int32_t) +
-                        align_up((size_t)p.npat * p.R * p.pwo * sizeof(int16_t), 16);
+    const size_t fixed = (size_t)((p.T + 31) / 32 * 32) * (p.R + NG + (PAD ? 1 : 0)) * sizeof(double) +
+                         (size_t)(p.maxS + 1) * sizeof(int64_t) + 16 +
+                         align_up((size_t)p.npat * kPatHdr * sizeof(int32_t), 16) +
+                         align_up((size_t)p.npat * p.R * p.pwo * sizeof(int16_t), 16);
     int dev_max = 0;
     PD_CUDA(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+    // kDefStages staged step blocks (a block is requested stages-1 steps before its
+    // use); deeper staging measured no faster on any C2 level (the step is bound by
+    // its own dependency chain, not the copy).  Two when three do not fit.
+    const size_t budget = (size_t)dev_max - 1024;
+    int stages = kDefStages;
+    if (const char* e = getenv("PD_WF_STAGES")) stages = atoi(e);
+    if (budget > fixed)
+        stages = std::min<int>(stages, (int)((budget - fixed) / std::max<size_t>(p.stage_bytes, 1)));
+    stages = std::max(kMinStages, std::min(kMaxStages, stages));
+    const size_t smem = stages * p.stage_bytes + fixed;
+    p.stages = stages;
     const int threads = (p.T / GU + 31) / 32 * 32;
-    const int max_threads = GU == 1 ? (NG <= kNgFine ? 768 : 512) : 256;
+    const int max_threads = NG <= kNgFine ? 768 : 512;
     if (getenv("PD_WF_VERBOSE"))
-        fprintf(stderr, "[wf] %s NG=%d GU=%d T=%d R=%d npat=%d pwo=%d stage=%zu smem=%zu (max %d)\n",
-                UPPER ? "upper" : "lower", NG, GU, p.T, p.R, p.npat, p.pwo, p.stage_bytes, smem,
+        fprintf(stderr, "[wf] %s NG=%d PAD=%d T=%d R=%d npat=%d pwo=%d stage=%zu smem=%zu (max %d)\n",
+                UPPER ? "upper" : "lower", NG, (int)PAD, p.T, p.R, p.npat, p.pwo, p.stage_bytes, smem,
                 dev_max);
     if (smem + 1024 > (size_t)dev_max || threads > max_threads) return false;
     p.smem = smem;
     // the attribute is per kernel, shared by every plan: only ever raise it
     static size_t attr_max = 0;
     if (smem > attr_max) {
-        PD_CUDA(cudaFuncSetAttribute(k_wf_sweep<UPPER, NG, GU>,
+        PD_CUDA(cudaFuncSetAttribute(k_wf_sweep<UPPER, NG, PAD>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_max = smem;
     }
     int per_sm = 0;
-    PD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wf_sweep<UPPER, NG, GU>,
+    PD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_wf_sweep<UPPER, NG, PAD>,
                                                           threads, smem));
     if (per_sm < 1) return false;
     p.blocks = std::min(p.ntask, per_sm * c.sms);
-    p.gu = GU;
+    p.pad = PAD;
     p.threads = threads;
     return true;
 }
 
-// GU > 1 (a thread running the node grids of its line) measured slower on
-// every C2 level (per-step chains lengthen; round-1 log): one row per thread.
 template <bool UPPER, int NG>
-bool configure_launch(Ctx& c, WfPlan& p) {
-    return configure_launch_gu<UPPER, NG, 1>(c, p);
+bool configure_launch(Ctx& c, WfPlan& p, bool pad) {
+    return pad ? configure_launch_pad<UPPER, NG, true>(c, p)
+               : configure_launch_pad<UPPER, NG, false>(c, p);
 }
 
 void upload(WfPlan& p, HostPlan& hp, int64_t n, int G, int64_t nline, int64_t npoint) {
@@ -717,6 +774,9 @@ void upload(WfPlan& p, HostPlan& hp, int64_t n, int G, int64_t nline, int64_t np
     p.pwo = hp.pwo;
     p.ng = hp.ng;
     p.npat = (int)(hp.pattern.size() / (2 + hp.ng));
+    // tables are bulk-copied into shared memory: 16-byte multiples
+    hp.pattern.resize(align_up(hp.pattern.size() * 4, 16) / 4, 0);
+    hp.offs.resize(align_up(hp.offs.size() * 2, 16) / 2, 0);
     p.maxS = hp.maxS;
     p.stage_bytes = hp.stage_bytes;
     auto up = [](auto& dst, auto& src) {
@@ -769,18 +829,28 @@ bool ilu0_set_wavefront(Ctx& c, Ilu0& f, int64_t ngroup, int64_t nline, int64_t 
     auto lo = std::make_unique<WfPlan>();
     auto up = std::make_unique<WfPlan>();
     auto build = [&](bool upper, int64_t G, WfPlan& plan) -> bool {
-        for (int NG : {0, kNgFine, kNgWide}) {
-            HostPlan hp;
-            if (!build_plan(rp, ci, dg, n, (int)G, nline, npoint, upper, NG, hp)) continue;
-            upload(plan, hp, n, (int)G, nline, npoint);
-            const bool ok = NG == 0 ? (upper ? configure_launch<true, 0>(c, plan)
-                                             : configure_launch<false, 0>(c, plan))
-                : NG == kNgFine ? (upper ? configure_launch<true, kNgFine>(c, plan)
-                                         : configure_launch<false, kNgFine>(c, plan))
-                                : (upper ? configure_launch<true, kNgWide>(c, plan)
-                                         : configure_launch<false, kNgWide>(c, plan));
-            if (ok) return true;
-        }
+        // zero-padded entry lists first (no predication); unpadded when the
+        // padded step blocks do not fit three stages
+        // Padding trades issue slots (extra zero entries) for a shorter per-entry
+        // critical path: it pays on latency-bound CTAs (<= 12 warps: C2 127^2..7^2
+        // levels) and costs on the 24-warp fine level (upper sweep 631 -> 770 us).
+        const char* pe = getenv("PD_WF_PAD");  // experiments: 0 = never, 1 = always
+        const bool try_pad = pe && *pe ? *pe == '1' : G * nline <= 384;
+        for (bool pad : {true, false})
+            for (int NG : {0, kNgFine, kNgWide}) {
+                if (pad && !try_pad) continue;
+                HostPlan hp;
+                if (!build_plan(rp, ci, dg, n, (int)G, nline, npoint, upper, NG, pad, hp))
+                    continue;
+                upload(plan, hp, n, (int)G, nline, npoint);
+                const bool ok = NG == 0 ? (upper ? configure_launch<true, 0>(c, plan, pad)
+                                                 : configure_launch<false, 0>(c, plan, pad))
+                    : NG == kNgFine ? (upper ? configure_launch<true, kNgFine>(c, plan, pad)
+                                             : configure_launch<false, kNgFine>(c, plan, pad))
+                                    : (upper ? configure_launch<true, kNgWide>(c, plan, pad)
+                                             : configure_launch<false, kNgWide>(c, plan, pad));
+                if (ok && (plan.stages >= kDefStages || !pad)) return true;
+            }
         return false;
     };
     if (!build(false, glo, *lo) || !build(true, ngroup, *up)) return false;
@@ -834,9 +904,9 @@ static void wf_trace_report(Ctx& c, WfPlan& p, const char* name) {
         return v[(size_t)(f * (v.size() - 1))];
     };
     fprintf(stderr,
-            "[wf %s] tasks=%d blocks=%d T=%d S=%d npat=%d stage=%zuB smem=%zuB span=%.1fus "
+            "[wf %s] tasks=%d blocks=%d T=%d S=%d npat=%d stage=%zuBx%d smem=%zuB span=%.1fus "
             "ns/step min/med/max=%.0f/%.0f/%.0f start(us) med/max=%.1f/%.1f\n",
-            name, p.ntask, p.blocks, p.T, p.maxS, p.npat, p.stage_bytes, p.smem,
+            name, p.ntask, p.blocks, p.T, p.maxS, p.npat, p.stage_bytes, p.stages, p.smem,
             (t1 - t0) * 1e-3, q(per_step, 0), q(per_step, 0.5), q(per_step, 1), q(start, 0.5),
             q(start, 1));
 }
@@ -844,8 +914,12 @@ static void wf_trace_report(Ctx& c, WfPlan& p, const char* name) {
 template <bool UPPER, int NG>
 static void launch_sweep_ng(Ctx& c, WfPlan& p, const double* b, double* y,
                             unsigned long long* ctr, const int* guard, int want) {
-    launch(k_wf_sweep<UPPER, NG, 1>, p.blocks, p.threads, p.smem, c.stream, wf_dev(p), b, y, ctr,
-           guard, want);
+    if (p.pad)
+        launch(k_wf_sweep<UPPER, NG, true>, p.blocks, p.threads, p.smem, c.stream, wf_dev(p), b,
+               y, ctr, guard, want);
+    else
+        launch(k_wf_sweep<UPPER, NG, false>, p.blocks, p.threads, p.smem, c.stream, wf_dev(p),
+               b, y, ctr, guard, want);
 }
 
 template <bool UPPER>

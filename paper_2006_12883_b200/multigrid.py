@@ -155,16 +155,20 @@ def _build_transfers(dims: list[LevelDims], space_pairs) -> list[TransferSet]:
     return out
 
 
-def lower_task_steps(nt: int, m: int, nline: int, partitions: int, max_threads: int = 768):
-    """Time steps per lower-sweep wavefront task, largest first: divisors of a
-    block-Jacobi partition's step count whose thread count (m*k*nline) fits one
-    CTA; env PD_WF_LOWER_STEPS pins it (experiments)."""
+def lower_task_steps(nt: int, m: int, nline: int, partitions: int, whole_max: int = 384,
+                     part_max: int = 192):
+    """Time steps per lower-sweep wavefront task, best first.  A task spanning a
+    whole block-Jacobi partition has no cross-CTA coupling at all (measured best
+    on C2's 15^2/7^2 levels); otherwise tasks of k steps pay off only while the
+    CTA stays small (31^2: k=2 at 186 threads; 63^2: k=2 at 378 is slower than
+    k=1).  Env PD_WF_LOWER_STEPS pins it (experiments)."""
     env = os.environ.get("PD_WF_LOWER_STEPS")
     if env:
         return [int(env), 1]
     per = nt // partitions if partitions > 0 and nt % partitions == 0 else 1
-    ks = [k for k in range(per, 0, -1) if per % k == 0 and m * k * nline <= max_threads]
-    return ks or [1]
+    ks = [per] if per > 1 and m * per * nline <= whole_max else []
+    ks += [k for k in range(per - 1, 1, -1) if per % k == 0 and m * k * nline <= part_max]
+    return ks + [1]
 
 
 # ---------------------------------------------------------------- hierarchy
