@@ -87,6 +87,24 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return s;  // valid in thread 0
 }
 
+// block_sum for multi-dimensional blocks: `tid` is the linear thread index
+template <int BS>
+__device__ __forceinline__ double block_sum_flat(double v, double* sh, int tid) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int lane = tid & 31, w = tid >> 5;
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (w == 0) {
+        s = (lane < BS / 32) ? sh[lane] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    }
+    __syncthreads();
+    return s;  // valid in tid 0
+}
+
 // Grid-wide deterministic sum: each block writes its partial; the last block
 // to arrive sums the partials in index order and stores *out (then resets the
 // counter so the slot can be reused by the next kernel on the stream).

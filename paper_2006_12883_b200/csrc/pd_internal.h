@@ -110,7 +110,8 @@ struct WfPlan {
     int64_t n = 0, nslot = 0;
     int ntask = 0, T = 0, nline = 0, npoint = 0, R = 0, pwo = 0, maxS = 0, blocks = 0, npat = 0,
         ng = 0, threads = 0, stages = 3;
-    bool pad = false;  // entry lists zero-padded to the kernel's chunk
+    bool pad = false;     // entry lists zero-padded to the kernel's chunk
+    bool gfirst = false;  // cross-task entries lead every pattern (no ring slots)
     size_t smem = 0, stage_bytes = 0;
     DevBuf<int32_t> nsteps;
     DevBuf<int64_t> boff, bofs, q0;

@@ -18,7 +18,11 @@
 #include "pd_stencil.h"
 
 #include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <vector>
 
 namespace pd {
 using namespace dev;
@@ -169,6 +173,125 @@ __global__ void __launch_bounds__(SB) k_st_residual(int64_t Nt, int M, int64_t S
         }
     }
 }
+
+// ---- structured-grid K1 (Dirichlet 1D/2D/3D constant-coefficient stencils) ----
+// When Kh is the (2*DIM+1)-point stencil on an n^DIM grid with one value per
+// stencil position and Mh is constant, every coefficient of L depends only on
+// (m, m', position): a table of M*M*(2*DIM+1) values (scipy's rounding, built
+// by k_st_coef on the grid's first interior row) replaces the per-entry coef/ci
+// gathers.  A thread owns one point of one step and produces its M rows from
+// the (2*DIM+1)*M neighbour values (coalesced along x, reused through L1), each
+// row summed in the global CSR's column order (previous step's last node, then
+// per node m' the stencil positions -z,-y,-x,c,+x,+y,+z), missing boundary
+// entries skipped exactly like absent CSR entries: bitwise the CSR SpMV.
+
+template <int DIM, int M, bool REDUCE>
+__global__ void __launch_bounds__(SB, M <= 3 ? 3 : 2) k_st_grid(int64_t Nt, int n, int gy, const double* __restrict__ tab,
+                                                const double* __restrict__ x,
+                                                const double* __restrict__ halo, double* y,
+                                                int mode, const double* b, const int* guard,
+                                                int want, double* partials,
+                                                unsigned int* counter, double* norm2,
+                                                int* nonfinite) {
+    if (guard_off(guard, want)) return;
+    constexpr int NP = 2 * DIM + 1;  // stencil positions, column order
+    __shared__ double c[M * M * NP + M];  // [m][m'][pos], then cprev[m]
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    for (int i = tid; i < M * M * NP + M; i += SB) c[i] = tab[i];
+    __syncthreads();
+    // block (32 x 8) tiles x and y; blockIdx.y = (z, y-tile); blockIdx.z strides the steps
+    const int zi = DIM == 3 ? (int)(blockIdx.y / gy) : 0;
+    const int yt = DIM == 3 ? (int)(blockIdx.y - zi * gy) : (int)blockIdx.y;
+    const int xi = blockIdx.x * 32 + threadIdx.x;
+    const int yi = DIM >= 2 ? yt * 8 + threadIdx.y : 0;
+    const bool inside = xi < n && (DIM < 2 || yi < n);
+    const int64_t S = DIM == 1 ? n : DIM == 2 ? (int64_t)n * n : (int64_t)n * n * n;
+    const int64_t MS = (int64_t)M * S;
+    const int j = (zi * n + yi) * n + xi;  // S < 2^31 (checked at plan time)
+    int off[NP];
+    bool has[NP];
+    {
+        int k = 0;
+        if (DIM == 3) { off[k] = -n * n; has[k++] = zi > 0; }
+        if (DIM >= 2) { off[k] = -n; has[k++] = yi > 0; }
+        off[k] = -1; has[k++] = xi > 0;
+        off[k] = 0; has[k++] = true;
+        off[k] = 1; has[k++] = xi < n - 1;
+        if (DIM >= 2) { off[k] = n; has[k++] = yi < n - 1; }
+        if (DIM == 3) { off[k] = n * n; has[k++] = zi < n - 1; }
+    }
+    const int Si = (int)S;
+    double acc2 = 0.0;
+    bool bad = false;
+    for (int64_t step = blockIdx.z; inside && step < Nt; step += gridDim.z) {
+        const double* xs = x + step * MS + j;
+        double v[M][NP];
+#pragma unroll
+        for (int mp = 0; mp < M; ++mp)
+#pragma unroll
+            for (int k = 0; k < NP; ++k)
+                v[mp][k] = has[k] ? __ldg(xs + (mp * Si + off[k])) : 0.0;
+        const double* xp = step > 0 ? xs - MS + (M - 1) * Si : (halo ? halo + j : nullptr);
+        const double vprev = xp ? __ldg(xp) : 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            double sacc = 0.0;
+            if (xp && c[M * M * NP + m] != 0.0) sacc = add(sacc, mul(c[M * M * NP + m], vprev));
+#pragma unroll
+            for (int mp = 0; mp < M; ++mp)
+#pragma unroll
+                for (int k = 0; k < NP; ++k)
+                    if (has[k]) sacc = add(sacc, mul(c[(m * M + mp) * NP + k], v[mp][k]));
+            const int64_t r = step * MS + j + m * Si;
+            double out = sacc;
+            if (mode == 1) out = sub(b[r], sacc);
+            else if (mode == 2) out = add(b[r], sacc);
+            y[r] = out;
+            if (REDUCE) {
+                acc2 = fma(out, out, acc2);
+                if (nonfinite && !isfinite(v[m][DIM])) bad = true;
+            }
+        }
+    }
+    if (REDUCE) {
+        if (bad) atomicOr(nonfinite, 1);
+        __shared__ double sh[SB / 32];
+        __shared__ bool last;
+        // block_sum needs a flat thread index: reduce over tid order
+        double sblk = block_sum_flat<SB>(acc2, sh, tid);
+        const unsigned int bid = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        const unsigned int nb = gridDim.x * gridDim.y * gridDim.z;
+        if (tid == 0) {
+            partials[bid] = sblk;
+            __threadfence();
+            last = (atomicAdd(counter, 1u) == nb - 1);
+        }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        double t = 0.0;
+        for (unsigned int i = tid; i < nb; i += SB) t += __ldcg(partials + i);
+        t = block_sum_flat<SB>(t, sh, tid);
+        if (tid == 0) {
+            *norm2 = t;
+            *counter = 0u;
+        }
+    }
+}
+
+// the grid table from the coefficient table of one interior row (k_st_coef's
+// rounding) and the step coupling -fl(l0[m]*mh)
+__global__ void k_st_grid_tab(int M, int NP, int64_t nnzK, const int64_t* __restrict__ rp,
+                              int64_t jrow, const double* __restrict__ coef, Tab T,
+                              const double* __restrict__ mh, double* tab) {
+    const int64_t p0 = rp[jrow];
+    for (int i = threadIdx.x; i < M * M * NP; i += blockDim.x) {
+        const int mm = i / NP, k = i - mm * NP;
+        tab[i] = coef[(int64_t)mm * nnzK + p0 + k];
+    }
+    for (int m = threadIdx.x; m < M; m += blockDim.x) tab[M * M * NP + m] = -mul(T.l0[m], mh[jrow]);
+}
+
 }  // namespace
 
 static Tab make_tab_raw(const double* Kq, const double* Mq, const double* l0, int M) {
@@ -200,6 +323,67 @@ StOp::StOp(Ctx& c_, int64_t Nt_, int M_, int64_t S_, const double* Kq_, const do
            Kh->val.p, mh.p, nnzK, coef.p);
     PD_LAUNCH_CHECK();
     PD_CUDA(cudaStreamSynchronize(c.stream));
+    detect_grid(rp, mh_host);
+}
+
+// Structured mode applies when Kh is exactly the Dirichlet (2d+1)-point stencil
+// on an n^d grid (d = 1..3) with one value per stencil position, Mh is
+// constant and a kernel is instantiated for (d, M).  Checked entry by entry.
+void StOp::detect_grid(const std::vector<int64_t>& rp, const double* mh_host) {
+    grid_dim = 0;
+    if (getenv("PD_NO_GRID_K1") || M < 2 || M > 5 || S < 27) return;
+    std::vector<int32_t> ci(std::max<int64_t>(nnzK, 1));
+    std::vector<double> kv(std::max<int64_t>(nnzK, 1));
+    PD_CUDA(cudaMemcpy(ci.data(), Kh->col.p, nnzK * 4, cudaMemcpyDeviceToHost));
+    PD_CUDA(cudaMemcpy(kv.data(), Kh->val.p, nnzK * 8, cudaMemcpyDeviceToHost));
+    for (int64_t j = 1; j < S; ++j)
+        if (mh_host[j] != mh_host[0]) return;
+    for (int d = 2; d <= 3; ++d) {
+        int64_t n = (int64_t)llround(std::pow((double)S, 1.0 / d));
+        int64_t Sd = d == 2 ? n * n : n * n * n;
+        if (Sd != S || n < 3 || S * M >= INT_MAX) continue;
+        const int NP = 2 * d + 1;
+        // template values from the centre row (all positions present)
+        const int64_t mid = n / 2, jc = d == 2 ? mid * n + mid : (mid * n + mid) * n + mid;
+        if (rp[jc + 1] - rp[jc] != NP) continue;
+        double tv[7];
+        for (int k = 0; k < NP; ++k) tv[k] = kv[rp[jc] + k];
+        bool ok = true;
+        for (int64_t j = 0; j < S && ok; ++j) {
+            const int64_t xi = j % n, yi = (j / n) % n, zi = d == 3 ? j / (n * n) : 0;
+            int64_t off[7];
+            bool has[7];
+            int k = 0;
+            if (d == 3) { off[k] = -n * n; has[k++] = zi > 0; }
+            off[k] = -n; has[k++] = yi > 0;
+            off[k] = -1; has[k++] = xi > 0;
+            off[k] = 0; has[k++] = true;
+            off[k] = 1; has[k++] = xi < n - 1;
+            off[k] = n; has[k++] = yi < n - 1;
+            if (d == 3) { off[k] = n * n; has[k++] = zi < n - 1; }
+            int64_t p = rp[j];
+            for (k = 0; k < NP && ok; ++k) {
+                if (!has[k]) continue;
+                if (p >= rp[j + 1] || ci[p] != j + off[k] || kv[p] != tv[k]) ok = false;
+                ++p;
+            }
+            if (p != rp[j + 1]) ok = false;
+        }
+        if (!ok) continue;
+        grid_tab.alloc(kGridMaxTabHost);
+        Tab T = make_tab_raw(Kq, Mq, l0, (int)M);
+        launch(k_st_grid_tab, 1, 128, 0, c.stream, (int)M, NP, nnzK, Kh->rowptr.p, jc, coef.p, T,
+               mh.p, grid_tab.p);
+        PD_LAUNCH_CHECK();
+        PD_CUDA(cudaStreamSynchronize(c.stream));
+        grid_partials.alloc(kGridMaxBlocks);
+        grid_counter.alloc(1);
+        PD_CUDA(cudaMemsetAsync(grid_counter.p, 0, sizeof(unsigned int), c.stream));
+        PD_CUDA(cudaStreamSynchronize(c.stream));
+        grid_dim = d;
+        grid_n = (int)n;
+        return;
+    }
 }
 
 static Tab make_tab(const StOp& op) { return make_tab_raw(op.Kq, op.Mq, op.l0, (int)op.M); }
@@ -213,10 +397,58 @@ static dim3 st_grid(const Ctx& c, int64_t S, int64_t planes, bool reduce) {
     return dim3((unsigned)gx, (unsigned)gy);
 }
 
+template <int DIM, int MM>
+static void launch_grid(const StOp& op, const double* x, double* y, int mode, const double* b,
+                        const int* guard, int want, double* norm2_out, int* nonfinite,
+                        const double* halo) {
+    Ctx& c = op.c;
+    const int n = op.grid_n;
+    const int gx = (n + 31) / 32, gy = DIM >= 2 ? (n + 7) / 8 : 1;
+    const int gyz = DIM == 3 ? gy * n : gy;
+    // steps strided by blockIdx.z: enough blocks to fill the GPU several times,
+    // at most kGridMaxBlocks for the fused norm's per-block partials
+    const int64_t per_step = (int64_t)gx * gyz;
+    int64_t gz = std::max<int64_t>(1, std::min<int64_t>(op.Nt, (int64_t)c.sms * 32 / per_step + 1));
+    if (norm2_out) gz = std::max<int64_t>(1, std::min<int64_t>(gz, kGridMaxBlocks / per_step));
+    const dim3 grid((unsigned)gx, (unsigned)gyz, (unsigned)gz), block(32, SB / 32);
+    if (norm2_out) {
+        if (per_step * gz > kGridMaxBlocks) throw ConfigError("grid K1: too many blocks");
+        launch(k_st_grid<DIM, MM, true>, grid, block, 0, c.stream, op.Nt, n, gy, op.grid_tab.p, x,
+               halo, y, mode, b, guard, want, op.grid_partials.p, op.grid_counter.p, norm2_out,
+               nonfinite);
+    } else {
+        launch(k_st_grid<DIM, MM, false>, grid, block, 0, c.stream, op.Nt, n, gy, op.grid_tab.p,
+               x, halo, y, mode, b, guard, want, (double*)nullptr, (unsigned int*)nullptr,
+               (double*)nullptr, (int*)nullptr);
+    }
+}
+
+template <int DIM>
+static bool launch_grid_m(const StOp& op, const double* x, double* y, int mode, const double* b,
+                          const int* guard, int want, double* norm2_out, int* nonfinite,
+                          const double* halo) {
+    switch (op.M) {
+        case 2: launch_grid<DIM, 2>(op, x, y, mode, b, guard, want, norm2_out, nonfinite, halo); return true;
+        case 3: launch_grid<DIM, 3>(op, x, y, mode, b, guard, want, norm2_out, nonfinite, halo); return true;
+        case 4: launch_grid<DIM, 4>(op, x, y, mode, b, guard, want, norm2_out, nonfinite, halo); return true;
+        case 5: launch_grid<DIM, 5>(op, x, y, mode, b, guard, want, norm2_out, nonfinite, halo); return true;
+        default: return false;
+    }
+}
+
 void StOp::apply(const double* x, double* y, int mode, const double* b, const int* guard,
                  int want, double* norm2_out, int* nonfinite, const double* halo) const {
     const int64_t N = size();
     if (N <= 0) return;
+    if (grid_dim == 2 || grid_dim == 3) {
+        const bool done = grid_dim == 2
+            ? launch_grid_m<2>(*this, x, y, mode, b, guard, want, norm2_out, nonfinite, halo)
+            : launch_grid_m<3>(*this, x, y, mode, b, guard, want, norm2_out, nonfinite, halo);
+        if (done) {
+            PD_LAUNCH_CHECK();
+            return;
+        }
+    }
     const Tab T = make_tab(*this);
     if (norm2_out) {
         launch(k_st_apply<true>, st_grid(c, S, Nt * M, true), SB, 0, c.stream, Nt, (int)M, S, T,

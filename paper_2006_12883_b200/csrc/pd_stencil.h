@@ -1,11 +1,15 @@
 // K1 matrix-free space-time operator (see pd_stencil.cu).
 #pragma once
 
+#include <vector>
+
 #include "pd_internal.h"
 
 namespace pd {
 
 constexpr int kStMaxM = 9;
+constexpr int kGridMaxTabHost = kStMaxM * kStMaxM * 7 + kStMaxM;
+constexpr int kGridMaxBlocks = 65536;
 
 struct StOp {
     Ctx& c;
@@ -16,6 +20,11 @@ struct StOp {
     DevBuf<double> mh;
     DevBuf<double> coef;  // one time block of Aqh values, [m][m'][p of Kh] (L2-resident)
     int64_t nnzK = 0;
+    // structured-grid mode (Dirichlet constant-coefficient stencil on n^dim)
+    int grid_dim = 0, grid_n = 0;
+    DevBuf<double> grid_tab;  // [m][m'][position] + step coupling per m
+    DevBuf<double> grid_partials;  // fused-norm per-block partials (kGridMaxBlocks)
+    DevBuf<unsigned int> grid_counter;
     StOp(Ctx& c, int64_t Nt, int M, int64_t S, const double* Kq, const double* Mq,
          const double* l0, double dt, const Csr& Kh, const double* mh_host);
     int64_t size() const { return Nt * M * S; }
@@ -24,6 +33,7 @@ struct StOp {
                int want = 0, double* norm2_out = nullptr, int* nonfinite = nullptr,
                const double* halo = nullptr) const;
     void residual(const double* u, const double* rhs, double* out, double gamma, int kind) const;
+    void detect_grid(const std::vector<int64_t>& rp, const double* mh_host);
 };
 
 // y = A x through the structured operator when present, else the CSR

@@ -71,7 +71,7 @@ struct WfDev {
     const unsigned char* blob;
     unsigned long long* trace;
     int64_t n;
-    int ntask, T, nline, npoint, R, pwo, maxS, npat, G, stages;
+    int ntask, T, nline, npoint, R, pwo, maxS, npat, G, stages, gfirst;
     size_t stage_bytes;
 };
 
@@ -96,6 +96,7 @@ WfDev wf_dev(WfPlan& p) {
     d.npat = p.npat;
     d.G = p.T / p.nline;
     d.stages = p.stages;
+    d.gfirst = p.gfirst ? 1 : 0;
 
     d.stage_bytes = p.stage_bytes;
     return d;
@@ -112,6 +113,16 @@ __device__ __forceinline__ unsigned long long ld_strong_if(bool pred, const doub
                                                            unsigned long long v) {
     asm volatile(
         "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q ld.relaxed.gpu.global.b64 %0, [%1];\n}\n"
+        : "+l"(v)
+        : "l"(p), "r"((unsigned)pred)
+        : "memory");
+    return v;
+}
+// weak (L1-cacheable) load issued only when `pred`
+__device__ __forceinline__ unsigned long long ld_weak_if(bool pred, const double* p,
+                                                         unsigned long long v) {
+    asm volatile(
+        "{\n.reg .pred q;\nsetp.ne.u32 q, %2, 0;\n@q ld.global.b64 %0, [%1];\n}\n"
         : "+l"(v)
         : "l"(p), "r"((unsigned)pred)
         : "memory");
@@ -224,7 +235,8 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
     constexpr int kPatHdr = 2 + NG;
     constexpr int NGA = NG > 0 ? NG : 1;
     const int T = P.T, R = P.R, pwo = P.pwo, G = P.G, t = threadIdx.x;
-    const unsigned Tp = (unsigned)(T + 31) & ~31u, RW = (unsigned)(R + NG);
+    const bool gf = P.gfirst != 0;  // polled values folded from registers, no ring slots
+    const unsigned Tp = (unsigned)(T + 31) & ~31u, RW = (unsigned)(R + (gf ? 0 : NG));
     const unsigned sb = (unsigned)P.stage_bytes;
     // layout (bytes from sm): stages | ring [RW][Tp] f64 | bofs [maxS+1] | patterns | offsets
     const unsigned nst = (unsigned)P.stages;
@@ -362,8 +374,12 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
             for (int k = 0; k < NG; ++k) {
                 const bool pk = k < n_ng[j];
                 const int go = pk ? lds_s32(pat + 8u + 4u * k) : 0;
+                // first look with a weak (L1-cacheable) load: each word goes from the
+                // sentinel to its final value exactly once per launch (L1 starts clean),
+                // so a weak load sees one or the other; pending values are re-polled
+                // with strong loads below
                 xn[j][k] = __longlong_as_double(
-                    (long long)ld_strong_if(pk, y + row + go, (unsigned long long)kPending));
+                    (long long)ld_weak_if(pk, y + row + go, (unsigned long long)kPending));
             }
         };
         {
@@ -403,28 +419,49 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
                 const int q = qlj[j] + seq[j];
                 const int row = UPPER ? n - 1 - q : q;
                 // cross-task values: wait until published, then into the own slots
+                double acc = bb[j];
+                unsigned fa = val[j];
                 if (NG > 0 && ng[j] > 0) {
+                    // cross-task values: resolve the (rare) pending ones by strong polls
+                    unsigned long long u[NGA];
 #pragma unroll
-                    for (int k = 0; k < NG; ++k)
+                    for (int k = 0; k < NG; ++k) {
+                        u[k] = (unsigned long long)__double_as_longlong(xs[j][k]);
                         if (k < ng[j]) {
-                            unsigned long long u =
-                                (unsigned long long)__double_as_longlong(xs[j][k]);
-                            if (u == kPending) {
+                            if (P.trace) {  // diagnostics: polls, and polls found pending
+                                atomicAdd(P.trace + 2 * P.ntask + 1, 1ull);
+                                if (u[k] == kPending) atomicAdd(P.trace + 2 * P.ntask, 1ull);
+                            }
+                            if (u[k] == kPending) {
                                 const int go = lds_s32(ph[j] + 8u + 4u * k);
                                 unsigned int ns = 32;
                                 do {
                                     __nanosleep(ns);
                                     if (ns < 256) ns <<= 1;
-                                    u = ld_strong_u64(y + row + go);
-                                } while (u == kPending);
+                                    u[k] = ld_strong_u64(y + row + go);
+                                } while (u[k] == kPending);
                             }
-                            sts_f64(ringj[j] + (unsigned)(R + k) * ring_step,
-                                    __longlong_as_double((long long)u));
                         }
+                    }
+                    if (gf) {  // CSR order: the previous-step entries come first
+                        double fg[NGA];
+#pragma unroll
+                        for (int k = 0; k < NG; ++k)
+                            if (k < ng[j]) fg[k] = lds_f64(fa + (unsigned)k * stride[j]);
+#pragma unroll
+                        for (int k = 0; k < NG; ++k)
+                            if (k < ng[j])
+                                acc = sub(acc, mul(fg[k], __longlong_as_double((long long)u[k])));
+                        fa += (unsigned)ng[j] * stride[j];
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < NG; ++k)
+                            if (k < ng[j])
+                                sts_f64(ringj[j] + (unsigned)(R + k) * ring_step,
+                                        __longlong_as_double((long long)u[k]));
+                    }
                 }
-                double acc = bb[j];
                 const unsigned orow = pat[j] + phase_b[j];
-                unsigned fa = val[j];
                 // PAD: len is padded to kChunk with zero entries, no per-entry predicates
 #pragma unroll 1
                 for (int k0 = 0; k0 < len[j]; k0 += kChunk) {
@@ -503,6 +540,7 @@ struct HostPlan {
     std::vector<int32_t> pattern;
     std::vector<int16_t> offs;
     int R = 0, pwo = 0, ng = 0;
+    bool gfirst = false;
     std::vector<unsigned char> blob;
     std::vector<int32_t> srow, sstride, scount;
     std::vector<int64_t> sval, sdiag;
@@ -568,11 +606,10 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
             if (r <= kRmax) R = std::max(R, r);
         }
     }
-    const int64_t RW = R + NG, Tp = (T + 31) / 32 * 32;
+    const int64_t Tp = (T + 31) / 32 * 32;
     hp.R = (int)R;
     hp.ng = NG;
-    // ring slots [RW + 1][Tp]: the extra slot row stays +0.0 (padded entries read it)
-    if ((RW + 1) * Tp + Tp > 32767) return plan_fail("3");  // int16 offsets
+    if ((R + NG + 1) * Tp + Tp > 32767) return plan_fail("3");  // int16 offsets
     // entry-source patterns, deduplicated: key = [len, ng, goff[NG], (dth, dx | global j)...]
     std::unordered_map<std::string, int> pid_of;
     std::vector<std::vector<int32_t>> pats;
@@ -617,8 +654,18 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
         }
         pid[q] = (uint16_t)id;
     }
+    // globals first: every pattern's cross-task entries precede its ring entries
+    // (the lower sweep's previous-step columns come first in CSR order).  Then the
+    // kernel folds polled values straight from registers and the ring needs no
+    // global slots; otherwise they go through slots R + j.
+    bool gfirst = true;
+    for (auto& pt : pats)
+        for (int e = pt[1]; e < pt[0]; ++e)
+            if (pt[kPatHdr + 2 * e] == INT_MIN) gfirst = false;
+    hp.gfirst = gfirst;
+    const int64_t RW = R + (gfirst ? 0 : NG);
     int maxlen = 1;
-    for (auto& pt : pats) maxlen = std::max(maxlen, pt[0]);
+    for (auto& pt : pats) maxlen = std::max(maxlen, pt[0] - (gfirst ? pt[1] : 0));
     const int pwo = (int)align_up(std::max(maxlen, kOffPad), 8);
     hp.pwo = pwo;
     hp.pattern.assign(pats.size() * kPatHdr, 0);
@@ -630,13 +677,15 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
     for (size_t k = 0; k < pats.size(); ++k) {
         const auto& pt = pats[k];
         std::copy(pt.begin(), pt.begin() + kPatHdr, hp.pattern.begin() + k * kPatHdr);
-        const int lenp = pad ? (int)align_up(pt[0], kChunk) : pt[0];
+        const int e0 = gfirst ? pt[1] : 0;  // first entry taken from the ring
+        const int nr = pt[0] - e0;
+        const int lenp = pad ? (int)align_up(nr, kChunk) : nr;
         hp.pattern[k * kPatHdr] = lenp;
         for (int64_t ph = 0; ph < R; ++ph)
             for (int e = 0; e < pwo; ++e) {
                 int64_t off = zero_off;
-                if (e < pt[0]) {
-                    const int32_t a = pt[kPatHdr + 2 * e], b2 = pt[kPatHdr + 2 * e + 1];
+                if (e < nr) {
+                    const int32_t a = pt[kPatHdr + 2 * (e0 + e)], b2 = pt[kPatHdr + 2 * (e0 + e) + 1];
                     off = a == INT_MIN ? (R + b2) * Tp : ((((ph + b2) % R) + R) % R) * Tp + a;
                 }
                 hp.offs[(k * R + ph) * pwo + e] = (int16_t)off;
@@ -664,7 +713,9 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
                 const int gg = (int)(th / nline), ln = (int)(th % nline);
                 lo[gg] = std::min<int32_t>(lo[gg], ln);
                 hi[gg] = std::max<int32_t>(hi[gg], ln);
-                W[gg] = std::max(W[gg], pad ? (int32_t)align_up(nent[q], kChunk) : nent[q]);
+                const int32_t ngq = gfirst ? pats[pid[q]][1] : 0;
+                W[gg] = std::max(W[gg], pad ? ngq + (int32_t)align_up(nent[q] - ngq, kChunk)
+                                            : nent[q]);
             }
             // header: per group int4 {lo, cnt, pid_off, val_off}, then dval_off[G]
             std::vector<int32_t> hdr(hdr_ints(G), 0);
@@ -716,7 +767,8 @@ template <bool UPPER, int NG, bool PAD>
 bool configure_launch_pad(Ctx& c, WfPlan& p) {
     constexpr int GU = 1;
     constexpr int kPatHdr = 2 + NG;
-    const size_t fixed = (size_t)((p.T + 31) / 32 * 32) * (p.R + NG + (PAD ? 1 : 0)) * sizeof(double) +
+    const size_t fixed = (size_t)((p.T + 31) / 32 * 32) *
+                             (p.R + (p.gfirst ? 0 : NG) + (PAD ? 1 : 0)) * sizeof(double) +
                          (size_t)(p.maxS + 1) * sizeof(int64_t) + 16 +
                          align_up((size_t)p.npat * kPatHdr * sizeof(int32_t), 16) +
                          align_up((size_t)p.npat * p.R * p.pwo * sizeof(int16_t), 16);
@@ -774,6 +826,7 @@ void upload(WfPlan& p, HostPlan& hp, int64_t n, int G, int64_t nline, int64_t np
     p.pwo = hp.pwo;
     p.ng = hp.ng;
     p.npat = (int)(hp.pattern.size() / (2 + hp.ng));
+    p.gfirst = hp.gfirst;
     // tables are bulk-copied into shared memory: 16-byte multiples
     hp.pattern.resize(align_up(hp.pattern.size() * 4, 16) / 4, 0);
     hp.offs.resize(align_up(hp.offs.size() * 2, 16) / 2, 0);
@@ -885,9 +938,12 @@ __global__ void k_wf_begin(unsigned long long* c, const int* guard, int want) {
 
 static void wf_trace_report(Ctx& c, WfPlan& p, const char* name) {
     PD_CUDA(cudaStreamSynchronize(c.stream));
-    std::vector<unsigned long long> tr(2 * (size_t)p.ntask);
+    std::vector<unsigned long long> tr(2 * (size_t)p.ntask + 2);
     std::vector<int32_t> S(p.ntask);
     PD_CUDA(cudaMemcpy(tr.data(), p.trace.p, tr.size() * 8, cudaMemcpyDeviceToHost));
+    PD_CUDA(cudaMemset(p.trace.p + 2 * (size_t)p.ntask, 0, 16));
+    fprintf(stderr, "[wf %s] polls=%llu pending=%llu\n", name, tr[2 * (size_t)p.ntask + 1],
+            tr[2 * (size_t)p.ntask]);
     PD_CUDA(cudaMemcpy(S.data(), p.nsteps.p, S.size() * 4, cudaMemcpyDeviceToHost));
     unsigned long long t0 = ~0ull, t1 = 0;
     std::vector<double> per_step, start;
@@ -938,8 +994,8 @@ void wf_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int
     WfPlan& up = *f.wf_up;
     static const bool trace = getenv("PD_WF_TRACE") != nullptr;
     if (trace && !lo.trace.p) {
-        lo.trace.alloc(2 * (size_t)lo.ntask);
-        up.trace.alloc(2 * (size_t)up.ntask);
+        lo.trace.alloc(2 * (size_t)lo.ntask + 2);
+        up.trace.alloc(2 * (size_t)up.ntask + 2);
     }
     // outputs are armed with the pending sentinel only when a sweep polls them
     if (lo.ng > 0) arm_pending(c, f.scratch.p, f.n, guard, want);

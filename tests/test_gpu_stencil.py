@@ -30,6 +30,12 @@ def _systems():
     spec3 = pd.StencilSpec(3, 7, "dirichlet", 0.7)
     yield "fd3d_dir", pd.assemble_system(pd.make_tableau(2), pd.fd_space(spec3),
                                          pd.TimeGrid(3, 0.1), 0.0, np.cos(np.arange(343.0)))
+    # structured-grid kernel instantiations (2D/3D x M = 2..5)
+    yield "fd2d_dir_M4", pd.assemble_system(pd.make_tableau(4), pd.fd_space(spec2),
+                                            pd.TimeGrid(3, 0.1), 0.0, np.sin(np.arange(225.0)))
+    spec3b = pd.StencilSpec(3, 9, "dirichlet", 1.0)
+    yield "fd3d_dir_M5", pd.assemble_system(pd.make_tableau(5), pd.fd_space(spec3b),
+                                            pd.TimeGrid(2, 0.1), 0.0, np.cos(np.arange(729.0)))
     specp = pd.StencilSpec(2, 16, "periodic", 1.0)
     yield "fd2d_per", pd.assemble_system(pd.make_tableau(3), pd.fd_space(specp),
                                          pd.TimeGrid(4, 0.04), 1.0, np.sin(np.arange(256.0)),
