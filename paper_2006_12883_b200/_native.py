@@ -254,8 +254,14 @@ def is_tensor(x) -> bool:
     return isinstance(x, torch.Tensor)
 
 
-def like_input(result, template):
-    """Return a CUDA tensor if the caller passed one, numpy otherwise."""
+def like_input(result, template, out=None):
+    """Hand a device result back in the caller's form: into `out` when given
+    (e.g. a pinned host tensor: one DMA, no allocation); a tensor on the
+    template's device for tensor inputs (host tensors come back on the host);
+    numpy for numpy inputs."""
+    if out is not None:
+        out.copy_(result.view_as(out) if out.shape != result.shape else result)
+        return out
     if is_tensor(template):
-        return result
+        return result if template.is_cuda else result.cpu()
     return result.cpu().numpy()

@@ -353,12 +353,16 @@ class MultigridHierarchy:
         return x, report
 
     def solve(self, b, x0=None, tol_rel: float = 1e-9, tol_abs: float = 1e-9,
-              max_cycles: int = 1000):
-        """V-cycle until ||b - Ax|| <= max(tol_abs, tol_rel*||b - Ax0||) (multigrid.py:275-305)."""
+              max_cycles: int = 1000, out=None):
+        """V-cycle until ||b - Ax|| <= max(tol_abs, tol_rel*||b - Ax0||) (multigrid.py:275-305).
+
+        numpy in -> numpy out (the reference's contract); torch tensors come back
+        on their own device; `out` (e.g. a pinned host tensor) receives x in place.
+        """
         bd = N.to_device(b, self.ctx)
         xd = N.zeros(bd.numel(), self.ctx) if x0 is None else N.to_device(x0, self.ctx).clone()
         x, rep = self.solve_dev(bd, xd, tol_rel, tol_abs, max_cycles)
-        return N.like_input(x, b), rep
+        return N.like_input(x, b, out), rep
 
 
 # ---------------------------------------------------------------- builders
