@@ -12,6 +12,6 @@ PD_NCU_REGION=1 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control
 echo "launch list rc=$?"
 python scripts/ilu_probe.py 64 > gpurun_out/probe_plain.log 2>&1 && \
 timeout 900 ncu --set full --clock-control none --import-source on --profile-from-start off \
-    -k regex:"k_trsv|k_wf_sweep|k_spmv|k_st_apply" -c 4 -o gpurun_out/top_kernels \
+    -k regex:"k_trsv|k_wf_sweep|k_spmv|k_st_apply|k_st_grid" -c 4 -o gpurun_out/top_kernels \
     python scripts/ilu_probe.py 64 > gpurun_out/ncu_full.log 2>&1
 echo "full capture rc=$?"
