@@ -90,9 +90,18 @@ struct Ctx {
     DevBuf<unsigned int> red_counter; // 4 counters
     DevBuf<double> scalars;           // small result slots
     DevBuf<int> flags;                // misc device flags
+    void* blas = nullptr;             // cuBLAS handle (plain DGEMMs only), lazily created
     explicit Ctx(int dev, cudaStream_t s);
+    ~Ctx();
+    Ctx(const Ctx&) = delete;
+    Ctx& operator=(const Ctx&) = delete;
     int grid_for(int64_t n, int bs, int per_sm = 8) const;
 };
+
+// out = mode-`stride` product of W stacked grids with the n x n matrix phi
+// (row-major; transpose=1: Phi^T, 0: Phi) as cuBLAS DGEMMs (pd_sdc.cu)
+void mode_product(Ctx& c, const double* in, double* out, int64_t total, int64_t n,
+                  int64_t stride, const double* phi, int transpose);
 
 // CSR on device: int64 row pointers (nnz may exceed 2^31 at C3/C5 sizes),
 // int32 column indices, fp64 values.  Column indices sorted per row.

@@ -20,7 +20,12 @@
 // guess with the reference's thresholds, growth test and iteration cap.
 #include "../../include/paradiff_b200.h"
 #include "pd_device.cuh"
+#include <cublas_v2.h>
+
+#include <array>
+
 #include "pd_internal.h"
+#include "pd_stencil.h"
 #include "pd_krylov.h"
 
 #include <algorithm>
@@ -80,6 +85,72 @@ void bspmv(Ctx& c, const Csr& A, const double* x, int64_t xs, double* y, int64_t
     if (nvec <= 0 || A.nrows <= 0) return;
     launch(k_bspmv, c.grid_for(A.nrows * nvec, TB, 16), TB, 0, c.stream, A.nrows, A.rowptr.p,
            A.col.p, A.val.p, x, xs, y, ys, nvec, mode, mh, b, bs);
+}
+
+// k_bspmv for a Kh that is a Dirichlet constant-coefficient (2*DIM+1)-point
+// stencil (detected at level creation): same per-row CSR column order and the
+// same modes, with the column indices and values replaced by grid offsets and
+// the per-position table, so the result is bitwise k_bspmv's.
+struct StTab {
+    double v[7];
+};
+template <int DIM>
+__global__ void __launch_bounds__(256) k_bstencil(int n, int gy, StTab tv, const double* __restrict__ x,
+                                                  int64_t xs, double* y, int64_t ys, int nvec,
+                                                  int mode, const double* __restrict__ mh,
+                                                  const double* b, int64_t bs) {
+    constexpr int NP = 2 * DIM + 1;
+    const int zi = DIM == 3 ? (int)(blockIdx.y / gy) : 0;
+    const int yt = DIM == 3 ? (int)(blockIdx.y - zi * gy) : (int)blockIdx.y;
+    const int xi = blockIdx.x * 32 + threadIdx.x, yi = yt * 8 + threadIdx.y;
+    if (xi >= n || yi >= n) return;
+    const int j = (zi * n + yi) * n + xi;
+    int off[NP];
+    bool has[NP];
+    {
+        int k = 0;
+        if (DIM == 3) { off[k] = -n * n; has[k++] = zi > 0; }
+        off[k] = -n; has[k++] = yi > 0;
+        off[k] = -1; has[k++] = xi > 0;
+        off[k] = 0; has[k++] = true;
+        off[k] = 1; has[k++] = xi < n - 1;
+        off[k] = n; has[k++] = yi < n - 1;
+        if (DIM == 3) { off[k] = n * n; has[k++] = zi < n - 1; }
+    }
+    const double mj = mode == 1 ? mh[j] : 1.0;
+    for (int v = blockIdx.z; v < nvec; v += gridDim.z) {
+        const double* xv = x + v * xs + j;
+        double xk[NP];
+#pragma unroll
+        for (int k = 0; k < NP; ++k) xk[k] = has[k] ? __ldg(xv + off[k]) : 0.0;
+        double s = 0.0;
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+            if (has[k]) s = add(s, mul(tv.v[k], xk[k]));
+        double* yv = y + v * ys + j;
+        if (mode == 0) *yv = s;
+        else if (mode == 1) *yv = (-s) / mj;
+        else if (mode == 2) *yv = sub(b[v * bs + j], s);
+        else *yv = add(*yv, s);
+    }
+}
+
+static void bstencil(Ctx& c, int dim, int n, const double* tv, const double* x, int64_t xs,
+                     double* y, int64_t ys, int nvec, int mode, const double* mh, const double* b,
+                     int64_t bs) {
+    StTab t;
+    for (int k = 0; k < 7; ++k) t.v[k] = tv[k];
+    const int gx = (n + 31) / 32, gy = (n + 7) / 8;
+    const int gyz = dim == 3 ? gy * n : gy;
+    const int gz = (int)std::max<int64_t>(1, std::min<int64_t>(nvec, std::max<int64_t>(
+        1, (int64_t)c.sms * 16 / ((int64_t)gx * gyz))));
+    const dim3 grid(gx, gyz, gz), block(32, 8);
+    if (dim == 3)
+        launch(k_bstencil<3>, grid, block, 0, c.stream, n, gy, t, x, xs, y, ys, nvec, mode, mh,
+               b, bs);
+    else
+        launch(k_bstencil<2>, grid, block, 0, c.stream, n, gy, t, x, xs, y, ys, nvec, mode, mh,
+               b, bs);
 }
 
 // out = -gamma * r(U)  (zeros when gamma == 0, pfasst.py:98-101)
@@ -195,6 +266,10 @@ struct SdcLevelDev {
     double dt, gamma;
     Small Q, QDI, QDE, A_imp, A_exp;  // A_imp = Q-QDI, A_exp = Q-QDE
     std::unique_ptr<Csr> Kh;
+    int kh_dim = 0, kh_n = 0;  // Kh a Dirichlet constant-coefficient grid stencil
+    double kh_tv[7] = {0};
+    std::vector<std::array<double, 7>> am_tv;  // node operators' stencils (when kh_dim)
+    bool am_grid = false;
     DevBuf<double> mh;
     // node operators A_m = diag(mh) + dt*qdi[m][m]*Kh
     std::vector<std::unique_ptr<Csr>> Am;
@@ -484,25 +559,6 @@ __global__ void k_node_newton_tri(const int64_t* __restrict__ rp, const int32_t*
     node_newton_tri_worker(rp, ci, kv, mh, S, q, gamma, kind, b, x, gbuf, lbuf, ubuf, w, err);
 }
 
-// Mode product along one axis of W stacked n^dim grids (C order, last axis
-// fastest): out[.., a, ..] = sum_i Mat(a, i) in[.., i, ..] with Mat = Phi^T
-// (transpose=1: forward transform) or Phi (transpose=0: back transform).
-__global__ void k_mode_apply(const double* __restrict__ in, double* __restrict__ out,
-                             int64_t total, int64_t n, int64_t stride,
-                             const double* __restrict__ phi, int transpose) {
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t a = (t / stride) % n;
-        const double* base = in + (t - a * stride);
-        double acc = 0.0;
-        for (int64_t i = 0; i < n; ++i) {
-            const double mv = transpose ? phi[i * n + a] : phi[a * n + i];
-            acc = fma(mv, base[i * stride], acc);
-        }
-        out[t] = acc;
-    }
-}
-
 // z /= (mh + q*s*sum_axes mu_{i_axis})  (eigenvalues of the node operator)
 __global__ void k_spec_scale(double* z, int64_t total, int64_t n, int dim,
                              const double* __restrict__ mu, double mh, double qs) {
@@ -518,6 +574,17 @@ __global__ void k_spec_scale(double* z, int64_t total, int64_t n, int dim,
     }
 }
 
+cublasHandle_t blas_of(Ctx& c) {
+    if (!c.blas) {
+        cublasHandle_t h;
+        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate failed");
+        c.blas = h;
+    }
+    auto h = static_cast<cublasHandle_t>(c.blas);
+    cublasSetStream(h, c.stream);
+    return h;
+}
+
 Small small_from(const double* h, int r, int cols) {
     Small s;
     std::memset(&s, 0, sizeof(s));
@@ -527,6 +594,30 @@ Small small_from(const double* h, int r, int cols) {
 }  // namespace
 
 // ---------------------------------------------------------------- host API
+// Mode product as DGEMMs (column-major views of the C-order [outer][n][stride]
+// array).  phi's raw row-major storage is Phi^T in column-major terms.
+//   stride == 1: out(a, o) = sum_i Mat(a, i) in(i, o): one GEMM, m=n, n=outer;
+//   stride  > 1: per outer block C_o(r, a) = sum_i B_o(r, i) Mat(a, i): strided
+//                batched GEMMs m=stride, n=n, k=n (B_o = in block, ld = stride).
+// Mat = Phi^T (transpose=1, forward) or Phi (back).
+void mode_product(Ctx& c, const double* in, double* out, int64_t total, int64_t n,
+                  int64_t stride, const double* phi, int transpose) {
+    const double one = 1.0, zero = 0.0;
+    cublasHandle_t h = blas_of(c);
+    const int64_t outer = total / (n * stride);
+    cublasStatus_t st;
+    if (stride == 1) {
+        st = cublasDgemm(h, transpose ? CUBLAS_OP_N : CUBLAS_OP_T, CUBLAS_OP_N, (int)n,
+                         (int)outer, (int)n, &one, phi, (int)n, in, (int)n, &zero, out, (int)n);
+    } else {
+        st = cublasDgemmStridedBatched(h, CUBLAS_OP_N, transpose ? CUBLAS_OP_T : CUBLAS_OP_N,
+                                       (int)stride, (int)n, (int)n, &one, in, (int)stride,
+                                       (long long)(n * stride), phi, (int)n, 0LL, &zero, out,
+                                       (int)stride, (long long)(n * stride), (int)outer);
+    }
+    if (st != CUBLAS_STATUS_SUCCESS) throw CudaError("cublas DGEMM failed in mode_product");
+}
+
 static void bnorm(SdcLevelDev& L, const double* x, int64_t n, int64_t stride, int W, double* out,
                   bool take_sqrt) {
     Ctx& c = L.c;
@@ -549,8 +640,7 @@ static void node_apply_inverse(SdcLevelDev& L, int m, const double* r, double* z
         int64_t stride = 1;
         for (int d = 0; d < L.spec_dim; ++d, stride *= L.spec_n) {
             double* dst = (src == T1) ? T2 : T1;
-            launch(k_mode_apply, c.grid_for(total, TB), TB, 0, c.stream, src, dst, total,
-                   L.spec_n, stride, (const double*)L.phi.p, 1);
+            mode_product(c, src, dst, total, L.spec_n, stride, L.phi.p, 1);
             src = dst;
         }
         launch(k_spec_scale, c.grid_for(total, TB), TB, 0, c.stream, const_cast<double*>(src),
@@ -559,8 +649,7 @@ static void node_apply_inverse(SdcLevelDev& L, int m, const double* r, double* z
         stride = 1;
         for (int d = 0; d < L.spec_dim; ++d, stride *= L.spec_n) {
             double* dst = (src == T1) ? T2 : T1;
-            launch(k_mode_apply, c.grid_for(total, TB), TB, 0, c.stream, src, dst, total,
-                   L.spec_n, stride, (const double*)L.phi.p, 0);
+            mode_product(c, src, dst, total, L.spec_n, stride, L.phi.p, 0);
             src = dst;
         }
         if (src != z) vec_copy(c, z, src, total);
@@ -596,9 +685,16 @@ static void node_solve(SdcLevelDev& L, int m, const double* b, double* x, int W,
     }
     const int64_t S = L.S;
     const Csr& A = *L.Am[m];
+    // r = b - A x (the grid stencil kernel when A_m is one: bitwise the same)
+    auto residual = [&] {
+        if (L.am_grid)
+            bstencil(c, L.kh_dim, L.kh_n, L.am_tv[m].data(), x, S, L.r.p, S, W, 2, nullptr, b, S);
+        else
+            bspmv(c, A, x, S, L.r.p, S, W, 2, nullptr, b, S);
+    };
     double* bn = L.tmp.p;  // W norms
     bnorm(L, b, S, S, W, bn, true);
-    bspmv(c, A, x, S, L.r.p, S, W, 2, nullptr, b, S);  // r = b - A x
+    residual();
     bnorm(L, L.r.p, S, S, W, L.beta.p, true);
     launch(k_refine_check, (W + 127) / 128, 128, 0, c.stream, L.beta.p, bn, L.beta0.p, L.thr.p,
            L.lowest.p, L.done.p, L.err.p, W, 0, 1e-13);
@@ -606,7 +702,7 @@ static void node_solve(SdcLevelDev& L, int m, const double* b, double* x, int W,
         node_apply_inverse(L, m, L.r.p, L.rhs.p + 0, W);  // rhs buffer reused as z
         launch(k_refine_update, c.grid_for(W * S, TB), TB, 0, c.stream, x, L.rhs.p, W, S,
                L.done.p);
-        bspmv(c, A, x, S, L.r.p, S, W, 2, nullptr, b, S);
+        residual();
         bnorm(L, L.r.p, S, S, W, L.beta.p, true);
         launch(k_refine_check, (W + 127) / 128, 128, 0, c.stream, L.beta.p, bn, L.beta0.p,
                L.thr.p, L.lowest.p, L.done.p, L.err.p, W, 1, 1e-13);
@@ -842,7 +938,10 @@ static void feval(SdcLevelDev& L, const double* U, double* fi, double* fe, int W
     Ctx& c = L.c;
     const int64_t S = L.S;
     (void)stride_w;
-    bspmv(c, *L.Kh, U, S, fi, S, W * nodes, 1, L.mh.p);
+    if (L.kh_dim)
+        bstencil(c, L.kh_dim, L.kh_n, L.kh_tv, U, S, fi, S, W * nodes, 1, L.mh.p, nullptr, 0);
+    else
+        bspmv(c, *L.Kh, U, S, fi, S, W * nodes, 1, L.mh.p);
     launch(k_freact, c.grid_for((int64_t)W * nodes * S, TB), TB, 0, c.stream, U, fe,
            (int64_t)W * nodes * S, L.gamma, L.kind);
 }
@@ -892,7 +991,11 @@ void sdc_sweep(SdcLevelDev& L, double* U, const double* U0, const double* tau, i
         launch(k_scatter_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.x.p, U, W, M, S,
                m);
         // f of the new node value (stored in the node-m slot of fi_new/fe_new)
-        bspmv(c, *L.Kh, L.x.p, S, L.fi_old.p, S, W, 1, L.mh.p);  // reuse fi_old as W x S scratch
+        if (L.kh_dim)  // reuse fi_old as W x S scratch
+            bstencil(c, L.kh_dim, L.kh_n, L.kh_tv, L.x.p, S, L.fi_old.p, S, W, 1, L.mh.p,
+                     nullptr, 0);
+        else
+            bspmv(c, *L.Kh, L.x.p, S, L.fi_old.p, S, W, 1, L.mh.p);
         launch(k_scatter_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.fi_old.p,
                L.fi_new.p, W, M, S, m);
         launch(k_freact, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.x.p, L.fe_old.p,
@@ -984,6 +1087,11 @@ int pd_sdc_level_create(void* ctx, void* Kh, const double* mh_host, int M, const
         PD_CUDA(cudaMemcpy(rp.data(), K->rowptr.p, (S + 1) * sizeof(int64_t),
                            cudaMemcpyDeviceToHost));
         L->Kh = pd::csr_upload(c, S, S, K->nnz, K->rowptr.p, K->col.p, K->val.p, true);
+        {
+            int64_t jc = 0;
+            if (!pd::detect_dirichlet_stencil(*L->Kh, L->kh_dim, L->kh_n, L->kh_tv, jc))
+                L->kh_dim = 0;
+        }
         L->mh.alloc(S);
         PD_CUDA(cudaMemcpy(L->mh.p, mh_host, S * sizeof(double), cudaMemcpyHostToDevice));
         // node operators A_m = diag(mh) + dt*qdi[m][m]*Kh (host assembly of values on Kh's
@@ -1030,6 +1138,18 @@ int pd_sdc_level_create(void* ctx, void* Kh, const double* mh_host, int M, const
                 for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
                     av[p] = (ci[p] == i ? mh_host[i] : 0.0) + q * kv[p];
             L->Am.push_back(pd::csr_upload(c, S, S, K->nnz, rp.data(), ci.data(), av.data(), false));
+        }
+        if (L->kh_dim) {  // node operators share Kh's structure: grid residuals too
+            L->am_grid = true;
+            for (int m = 0; m < M && L->am_grid; ++m) {
+                int d = 0, nn = 0;
+                int64_t jc = 0;
+                std::array<double, 7> tv{};
+                if (!pd::detect_dirichlet_stencil(*L->Am[m], d, nn, tv.data(), jc) ||
+                    d != L->kh_dim || nn != L->kh_n)
+                    L->am_grid = false;
+                L->am_tv.push_back(tv);
+            }
         }
         L->Aval.alloc((int64_t)M * std::max<int64_t>(K->nnz, 1));
         for (int m = 0; m < M; ++m)

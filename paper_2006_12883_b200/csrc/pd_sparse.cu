@@ -15,6 +15,8 @@
 // by a thread that is already running: no deadlock for any grid size.  Each
 // row's arithmetic follows the reference's sequential order exactly.
 #include "pd_device.cuh"
+#include <cublas_v2.h>
+
 #include "pd_internal.h"
 
 #include <cub/device/device_radix_sort.cuh>
@@ -40,6 +42,10 @@ Ctx::Ctx(int dev_, cudaStream_t s) : device(dev_), stream(s) {
     scalars.alloc(64);
     flags.alloc(64);
     PD_CUDA(cudaMemset(flags.p, 0, 64 * sizeof(int)));
+}
+
+Ctx::~Ctx() {
+    if (blas) cublasDestroy(static_cast<cublasHandle_t>(blas));
 }
 
 int Ctx::grid_for(int64_t n, int bs, int per_sm) const {

@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -326,27 +327,27 @@ StOp::StOp(Ctx& c_, int64_t Nt_, int M_, int64_t S_, const double* Kq_, const do
     detect_grid(rp, mh_host);
 }
 
-// Structured mode applies when Kh is exactly the Dirichlet (2d+1)-point stencil
-// on an n^d grid (d = 1..3) with one value per stencil position, Mh is
-// constant and a kernel is instantiated for (d, M).  Checked entry by entry.
-void StOp::detect_grid(const std::vector<int64_t>& rp, const double* mh_host) {
-    grid_dim = 0;
-    if (getenv("PD_NO_GRID_K1") || M < 2 || M > 5 || S < 27) return;
-    std::vector<int32_t> ci(std::max<int64_t>(nnzK, 1));
-    std::vector<double> kv(std::max<int64_t>(nnzK, 1));
-    PD_CUDA(cudaMemcpy(ci.data(), Kh->col.p, nnzK * 4, cudaMemcpyDeviceToHost));
-    PD_CUDA(cudaMemcpy(kv.data(), Kh->val.p, nnzK * 8, cudaMemcpyDeviceToHost));
-    for (int64_t j = 1; j < S; ++j)
-        if (mh_host[j] != mh_host[0]) return;
+// Kh is exactly the Dirichlet (2d+1)-point stencil on an n^d grid (d = 2, 3)
+// with one value per stencil position (positions in CSR column order: -z, -y,
+// -x, centre, +x, +y, +z; boundary rows simply lack the outside neighbours).
+// Checked entry by entry on a host copy.  jc = a centre row with every entry.
+bool detect_dirichlet_stencil(const Csr& K, int& dim, int& n_out, double tv[7], int64_t& jc_out) {
+    const int64_t S = K.nrows;
+    dim = 0;
+    if (S < 27 || K.ncols != S || getenv("PD_NO_GRID_STENCIL")) return false;
+    std::vector<int64_t> rp(S + 1);
+    std::vector<int32_t> ci(std::max<int64_t>(K.nnz, 1));
+    std::vector<double> kv(std::max<int64_t>(K.nnz, 1));
+    PD_CUDA(cudaMemcpy(rp.data(), K.rowptr.p, (S + 1) * 8, cudaMemcpyDeviceToHost));
+    PD_CUDA(cudaMemcpy(ci.data(), K.col.p, K.nnz * 4, cudaMemcpyDeviceToHost));
+    PD_CUDA(cudaMemcpy(kv.data(), K.val.p, K.nnz * 8, cudaMemcpyDeviceToHost));
     for (int d = 2; d <= 3; ++d) {
-        int64_t n = (int64_t)llround(std::pow((double)S, 1.0 / d));
-        int64_t Sd = d == 2 ? n * n : n * n * n;
-        if (Sd != S || n < 3 || S * M >= INT_MAX) continue;
+        const int64_t n = (int64_t)llround(std::pow((double)S, 1.0 / d));
+        const int64_t Sd = d == 2 ? n * n : n * n * n;
+        if (Sd != S || n < 3 || S >= INT_MAX / 8) continue;
         const int NP = 2 * d + 1;
-        // template values from the centre row (all positions present)
         const int64_t mid = n / 2, jc = d == 2 ? mid * n + mid : (mid * n + mid) * n + mid;
         if (rp[jc + 1] - rp[jc] != NP) continue;
-        double tv[7];
         for (int k = 0; k < NP; ++k) tv[k] = kv[rp[jc] + k];
         bool ok = true;
         for (int64_t j = 0; j < S && ok; ++j) {
@@ -369,21 +370,41 @@ void StOp::detect_grid(const std::vector<int64_t>& rp, const double* mh_host) {
             }
             if (p != rp[j + 1]) ok = false;
         }
+        if (getenv("PD_STENCIL_VERBOSE"))
+            fprintf(stderr, "[stencil] S=%lld d=%d n=%lld %s\n", (long long)S, d, (long long)n,
+                    ok ? "structured" : "not constant-coefficient");
         if (!ok) continue;
-        grid_tab.alloc(kGridMaxTabHost);
-        Tab T = make_tab_raw(Kq, Mq, l0, (int)M);
-        launch(k_st_grid_tab, 1, 128, 0, c.stream, (int)M, NP, nnzK, Kh->rowptr.p, jc, coef.p, T,
-               mh.p, grid_tab.p);
-        PD_LAUNCH_CHECK();
-        PD_CUDA(cudaStreamSynchronize(c.stream));
-        grid_partials.alloc(kGridMaxBlocks);
-        grid_counter.alloc(1);
-        PD_CUDA(cudaMemsetAsync(grid_counter.p, 0, sizeof(unsigned int), c.stream));
-        PD_CUDA(cudaStreamSynchronize(c.stream));
-        grid_dim = d;
-        grid_n = (int)n;
-        return;
+        dim = d;
+        n_out = (int)n;
+        jc_out = jc;
+        return true;
     }
+    return false;
+}
+
+// Structured K1 mode: Kh a Dirichlet constant-coefficient stencil, Mh constant,
+// and a kernel instantiated for M.
+void StOp::detect_grid(const std::vector<int64_t>& rp, const double* mh_host) {
+    (void)rp;
+    grid_dim = 0;
+    if (getenv("PD_NO_GRID_K1") || M < 2 || M > 5) return;
+    for (int64_t j = 1; j < S; ++j)
+        if (mh_host[j] != mh_host[0]) return;
+    int d = 0, n = 0;
+    double tv[7];
+    int64_t jc = 0;
+    if (!detect_dirichlet_stencil(*Kh, d, n, tv, jc) || S * M >= INT_MAX) return;
+    grid_tab.alloc(kGridMaxTabHost);
+    Tab T = make_tab_raw(Kq, Mq, l0, (int)M);
+    launch(k_st_grid_tab, 1, 128, 0, c.stream, (int)M, 2 * d + 1, nnzK, Kh->rowptr.p, jc, coef.p,
+           T, mh.p, grid_tab.p);
+    PD_LAUNCH_CHECK();
+    grid_partials.alloc(kGridMaxBlocks);
+    grid_counter.alloc(1);
+    PD_CUDA(cudaMemsetAsync(grid_counter.p, 0, sizeof(unsigned int), c.stream));
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    grid_dim = d;
+    grid_n = n;
 }
 
 static Tab make_tab(const StOp& op) { return make_tab_raw(op.Kq, op.Mq, op.l0, (int)op.M); }

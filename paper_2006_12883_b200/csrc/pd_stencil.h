@@ -36,6 +36,10 @@ struct StOp {
     void detect_grid(const std::vector<int64_t>& rp, const double* mh_host);
 };
 
+// Kh a Dirichlet constant-coefficient (2d+1)-point stencil on n^d (d = 2, 3)?
+// tv = the value per stencil position in CSR column order; jc = a full row.
+bool detect_dirichlet_stencil(const Csr& K, int& dim, int& n, double tv[7], int64_t& jc);
+
 // y = A x through the structured operator when present, else the CSR
 inline void apply_A(Ctx& c, const Csr& A, const StOp* op, const double* x, double* y, int mode,
                     const double* b, const int* guard = nullptr, int want = 0,

@@ -174,3 +174,23 @@ def test_reduced_baseline_configs_on_device(golden):
     assert rep.iterations == int(g["c5_newton_its"])
     assert rep.inner_iterations == g["c5_newton_inner"].tolist()
     assert per_node_rel(x, g["c5_newton_x"], (4, 3, 512)) < 1e-10
+
+
+@pytest.mark.parametrize("name,n", [("C2", 15), ("C4", 7)])
+def test_structured_stencil_f_evaluations_bitwise(monkeypatch, name, n):
+    """Grid-stencil f(U) = -Kh U / mh (k_bstencil) is bitwise the CSR k_bspmv path:
+    whole PFASST runs agree to the last bit with the structured kernel disabled."""
+    cfg = pd.baseline_config(name, n=n, Nt=4)
+    ops = pd.fd_space(cfg.spec)
+    out = []
+    for disable in (True, False):
+        if disable:
+            monkeypatch.setenv("PD_NO_GRID_STENCIL", "1")
+        else:
+            monkeypatch.delenv("PD_NO_GRID_STENCIL", raising=False)
+        hier = PF.build_pfasst_hierarchy(cfg.M, ops.mesh, pd.TimeGrid(cfg.Nt, cfg.T), 0.0, L=2,
+                                         nu=1, space=ops, M_coarse=cfg.M_coarse)
+        out.append(PF.pfasst_run(hier, cfg.u0(), cfg.Nt, 4, 1e-10, 1e-10))
+    (x1, r1), (x2, r2) = out
+    assert r1.iterations == r2.iterations and r1.converged
+    np.testing.assert_array_equal(x1, x2)
