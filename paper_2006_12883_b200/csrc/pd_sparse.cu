@@ -182,10 +182,19 @@ __global__ void __launch_bounds__(BS) k_spmv(int64_t n, const int64_t* __restric
                 sc[spad(k)] = __ldcs(ci + c0 + k);
             }
             __syncthreads();
-            const int64_t lo = max(a, c0), hi = min(bnd, c0 + cnt);
-            for (int64_t p = lo; p < hi; ++p) {
-                const int k = spad((int)(p - c0));
-                s = add(s, mul(sv[k], __ldg(x + sc[k])));
+            // four gathers in flight before their multiply/add chain (same order)
+            const int klo = (int)(max(a, c0) - c0), khi = (int)(min(bnd, c0 + cnt) - c0);
+            for (int k0 = klo; k0 < khi; k0 += 4) {
+                double xv[4], fv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int k = spad(min(k0 + u, khi - 1));
+                    fv[u] = sv[k];
+                    xv[u] = __ldg(x + sc[k]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (k0 + u < khi) s = add(s, mul(fv[u], xv[u]));
             }
         }
         if (i < n) {
