@@ -23,6 +23,10 @@ single-GPU PFASST path used by pfasst_run.
 
 from __future__ import annotations
 
+import sys
+
+import os
+
 import time
 
 import numpy as np
@@ -138,8 +142,11 @@ def run_windows(engine, comm, Nt: int, P: int, tol_rel: float, tol_abs: float,
                         return None
                     try:
                         return fn(*a)
-                    except SolverError:
+                    except SolverError as e:
                         state["failed"] = True
+                        if os.environ.get("PD_PFASST_VERBOSE"):
+                            print(f"[pfasst] window iteration {k}: {fn.__name__}: {e}",
+                                  file=sys.stderr, flush=True)
                         return None
 
                 if k > 1:
