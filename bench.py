@@ -12,10 +12,12 @@ this config (measured, 300 cycles), see DESIGN.md.
 
 One "step" = one full solve to tolerance from x=0 (inputs resident in HBM).
 value = N * (2*nu*cycles) / t  (space-time GDOF/s per fine smoother sweep,
-SURVEY §8(d)), summed over ranks / max-over-ranks time for N>1 (replicas of
-the workload per GPU in round 1; weak scaling).
-`e2e` = the same metric through the public API (`MultigridHierarchy.solve`
-with host numpy in, host numpy out: H2D + D2H inside the timed region).
+SURVEY §8(d)), N = the C2 system's unknowns.  With --gpus N > 1 (torchrun)
+the one solve is sharded over the ranks by time slabs (mg_sharded: each rank
+owns P/N block-Jacobi partitions of every level; halo send/recv and GMRES
+allreduces over NCCL); time = max over ranks; strong scaling.
+`e2e` = the same metric through the public API (`MultigridHierarchy.solve(b,
+out=x)` with pinned host tensors: H2D + D2H inside the timed region).
 `--impl reference` times the reference algorithm's CPU restatement (oracle/,
 a port: the reference itself is not present on the GPU box) on host cores.
 """
@@ -149,7 +151,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(8) | {"sample": sample},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
@@ -183,13 +185,29 @@ def run_b200(args):
                                 pd.TimeGrid(cfg.Nt, cfg.T), 0.0, cfg.u0())
     h = pd.build_hierarchy(system, "SMG", LEVELS, NU, partitions=PARTS)
     b_host = system.rhs()
-    b = N.to_device(b_host)
+    b = b_glob = N.to_device(b_host)
     x = N.zeros(system.size)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t_setup
     lib = N.load_library()
 
+    smg = None
+    if world > 1:
+        # N GPUs: the time-slab sharded V-cycle (mg_sharded: halo send/recv of the
+        # previous step's rows, allreduced GMRES dots, replicated coarsest solve);
+        # strong scaling of the one C2 solve
+        from paper_2006_12883_b200.mg_sharded import Comm, build_sharded_hierarchy
+
+        smg = build_sharded_hierarchy(h, Comm(device=torch.device("cuda", local)))
+        r0, r1 = smg.shards[0].r0, smg.shards[0].r1
+        b = N.to_device(b_host[r0:r1])
+        b_host = np.ascontiguousarray(b_host[r0:r1])
+        torch.cuda.synchronize()
+        setup_s = time.perf_counter() - t_setup
+
     def one_solve():
+        if smg is not None:
+            return smg.solve(b, tol_rel=TOL, tol_abs=TOL, max_cycles=1000)[1]
         N.call("pd_scale", h.ctx.handle, N.ptr(x), N.ptr(x), 0.0, system.size)  # x = 0
         return h.solve_dev(b, x, TOL, TOL, 1000)[1]
 
@@ -222,24 +240,36 @@ def run_b200(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_dev = float(tt.item())
     sweeps = 2 * NU * cycles
-    value = world * system.size * sweeps / t_dev / 1e9
+    # one C2 solve in total: the replicated/sharded unit count is system.size per solve
+    value = system.size * sweeps / t_dev / 1e9
 
     # e2e: public API from pinned host memory (H2D of b and D2H of x inside the
     # timed region, every step; MultigridHierarchy.solve(b, out=x))
     b_pin = torch.from_numpy(b_host).pin_memory()
     x_pin = torch.empty_like(b_pin).pin_memory()
-    xh, rep_e = h.solve(b_pin, tol_rel=TOL, tol_abs=TOL, max_cycles=1000, out=x_pin)
+
+    def e2e_solve(bh, out=None):
+        if smg is not None:
+            xd, r = smg.solve(bh, tol_rel=TOL, tol_abs=TOL, max_cycles=1000)
+            if out is not None:
+                out.copy_(xd)
+            else:
+                xd.cpu()
+            return out, r
+        return h.solve(bh, tol_rel=TOL, tol_abs=TOL, max_cycles=1000, out=out)
+
+    xh, rep_e = e2e_solve(b_pin, x_pin)
     e2e_times = []
     for _ in range(max(1, min(args.steps, 3))):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        xh, rep_e = h.solve(b_pin, tol_rel=TOL, tol_abs=TOL, max_cycles=1000, out=x_pin)
+        xh, rep_e = e2e_solve(b_pin, x_pin)
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
     # the numpy drop-in path (pageable host arrays) for reference
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    h.solve(b_host, tol_rel=TOL, tol_abs=TOL, max_cycles=1000)
+    e2e_solve(b_host)
     torch.cuda.synchronize()
     t_e2e_numpy = time.perf_counter() - t0
     t_e2e = float(np.mean(e2e_times))
@@ -247,7 +277,7 @@ def run_b200(args):
         tt = torch.tensor([t_e2e], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_e2e = float(tt.item())
-    e2e_value = world * system.size * 2 * NU * rep_e.iterations / t_e2e / 1e9
+    e2e_value = system.size * 2 * NU * rep_e.iterations / t_e2e / 1e9
 
     # roofline: dominant kernel = fine-level ILU(0) triangular sweeps (both), timed
     # live with CUDA events on the library's stream (torch's current stream)
@@ -257,11 +287,11 @@ def run_b200(args):
     N.call("pd_mg_level_precond", h._mg, 0, ctypes.byref(ilu))
     y = N.empty(system.size)
     for _ in range(2):
-        N.call("pd_ilu0_solve", h.ctx.handle, ilu, N.ptr(b), N.ptr(y))
+        N.call("pd_ilu0_solve", h.ctx.handle, ilu, N.ptr(b_glob), N.ptr(y))
     reps = 10
     ev0.record()
     for _ in range(reps):
-        N.call("pd_ilu0_solve", h.ctx.handle, ilu, N.ptr(b), N.ptr(y))
+        N.call("pd_ilu0_solve", h.ctx.handle, ilu, N.ptr(b_glob), N.ptr(y))
     ev1.record()
     torch.cuda.synchronize()
     t_ilu = ev0.elapsed_time(ev1) / 1e3 / reps
@@ -288,9 +318,10 @@ def run_b200(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config() | {"parallelism": f"replicas x{world}" if world > 1
-                                           else "1 GPU"},
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config() | {"parallelism": (
+                f"time-slab sharded MG over {world} GPUs (block-Jacobi partitions "
+                f"{PARTS // world}/rank, NCCL halo + allreduce)") if world > 1 else "1 GPU"},
             "solve_time_s": t_dev / args.steps, "cycles_per_solve": cycles / max(args.steps, 1),
             "setup_s": setup_s,
             "clocks": clk.summary(),

@@ -191,3 +191,21 @@ def test_device_galerkin_refresh_bitwise_equals_scipy():
         dev = pd.DeviceCsr.borrowed(hnd, M.shape, M.nnz, h.ctx)
         x = np.random.default_rng(l).standard_normal(M.shape[1])
         np.testing.assert_array_equal(dev.dot(x), M @ x)
+
+
+def test_sharded_mg_device_engine_one_rank_matches_serial():
+    """mg_sharded on the GPU engine (G=1: no communication) reproduces the serial
+    device multigrid: equal cycle counts, rel L2 <= 1e-10 (host-side GMRES scalars)."""
+    from paper_2006_12883_b200.mg_sharded import build_sharded_hierarchy
+
+    cfg = pd.baseline_config("C2", n=31, Nt=8)
+    system = pd.assemble_system(pd.make_tableau(cfg.M), pd.fd_space(cfg.spec),
+                                pd.TimeGrid(cfg.Nt, cfg.T), 0.0, cfg.u0())
+    h = pd.build_hierarchy(system, "SMG", 3, 3, partitions=4)
+    b = system.rhs()
+    x1, r1 = h.solve(b, tol_rel=1e-10, tol_abs=1e-10)
+    smg = build_sharded_hierarchy(h)
+    x2, r2 = smg.solve(b, tol_rel=1e-10, tol_abs=1e-10)
+    x2 = x2.cpu().numpy()
+    assert r1.converged and r2.converged and r1.iterations == r2.iterations
+    assert np.linalg.norm(x2 - x1) <= 1e-10 * np.linalg.norm(x1)
