@@ -58,7 +58,7 @@ constexpr int kChunk = 4;       // entries loaded together before their multiply
 // dthread for in-task results, (R + j)*Tp for the thread's polled cross-task
 // slots.  Every entry is then one conflict-free shared load.
 constexpr int kRmax = 16;
-constexpr int kOffPad = 16;     // offset rows: at least this many entries, multiple of 8
+constexpr int kOffPad = 4;      // offset rows: a multiple of 4 entries (8-byte loads)
 constexpr unsigned kBulkPieces = 8;  // bulk copy requests per step block     // entry offsets of the next row held in registers
 
 struct WfDev {
@@ -66,6 +66,7 @@ struct WfDev {
     const int64_t* boff;     // per task: first index into bofs
     const int64_t* bofs;     // byte offset of every step block (+1 sentinel per task)
     const int64_t* q0;       // per task: sweep position of its first row
+    const int64_t* gate;     // per task: predecessor row to await before starting (-1: none)
     const int32_t* pattern;  // [npat][2 + NG]
     const int16_t* offs;     // [npat][R][pwo]
     const unsigned char* blob;
@@ -81,6 +82,7 @@ WfDev wf_dev(WfPlan& p) {
     d.boff = p.boff.p;
     d.bofs = p.bofs.p;
     d.q0 = p.q0.p;
+    d.gate = p.gate.p;
     d.pattern = p.pattern.p;
     d.offs = p.offs.p;
     d.blob = p.blob.p;
@@ -244,11 +246,11 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
     // PAD plans read an extra all-zero slot row; unpadded plans skip it (every KB
     // counts: above 196 KB of shared memory the SM keeps no L1 for the b loads)
     const unsigned o_bofs = o_ring + Tp * (RW + (PAD ? 1u : 0u)) * 8u;
-    const unsigned o_pat = (o_bofs + (unsigned)(P.maxS + 1) * 8u + 15u) & ~15u;
+    const unsigned o_pat = (o_bofs + (unsigned)(P.maxS + 1) * 4u + 15u) & ~15u;
     const unsigned pat_bytes = ((unsigned)(P.npat * kPatHdr) * 4u + 15u) & ~15u;
     const unsigned off_bytes = ((unsigned)(P.npat * R * pwo) * 2u + 15u) & ~15u;
     const unsigned o_off = o_pat + pat_bytes;
-    int64_t* sbofs = reinterpret_cast<int64_t*>(sm + o_bofs);
+    int32_t* sbofs = reinterpret_cast<int32_t*>(sm + o_bofs);  // block offsets in the task
     const unsigned u0 = smem_u32(sm);
     const unsigned u_pat = u0 + o_pat, u_off = u0 + o_off;
     const int nthr = T / GU;  // real threads with work
@@ -305,12 +307,18 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
         if (P.trace && t == 0) P.trace[2 * task] = globaltimer();
         const int S = P.nsteps[task];
         const int64_t bo = P.boff[task];
-        for (int s = t; s <= S; s += blockDim.x) sbofs[s] = P.bofs[bo + s];
+        const int64_t base = P.bofs[bo];
+        for (int s = t; s <= S; s += blockDim.x) sbofs[s] = (int32_t)(P.bofs[bo + s] - base);
+        if (t == 0) {  // start gate (see build_plan)
+            const int64_t gr = P.gate[task];
+            if (gr >= 0)
+                while (ld_strong_u64(y + gr) == kPending) __nanosleep(128);
+        }
         __syncthreads();
         // blocks are issued and consumed in order, once each: running stage
         // indices (no runtime division by the stage count)
         auto issue = [&](int s) {
-            bulk_load(sm + ist * sb, P.blob + sbofs[s], (unsigned)(sbofs[s + 1] - sbofs[s]),
+            bulk_load(sm + ist * sb, P.blob + base + sbofs[s], (unsigned)(sbofs[s + 1] - sbofs[s]),
                       &bar[ist]);
             ist = ist + 1 == nst ? 0u : ist + 1;
         };
@@ -536,7 +544,7 @@ __global__ void k_wf_gather(int64_t nslot, const int32_t* srow, const int64_t* s
 
 struct HostPlan {
     std::vector<int32_t> S;
-    std::vector<int64_t> boff, bofs, q0;
+    std::vector<int64_t> boff, bofs, q0, gate;
     std::vector<int32_t> pattern;
     std::vector<int16_t> offs;
     int R = 0, pwo = 0, ng = 0;
@@ -666,7 +674,7 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
     const int64_t RW = R + (gfirst ? 0 : NG);
     int maxlen = 1;
     for (auto& pt : pats) maxlen = std::max(maxlen, pt[0] - (gfirst ? pt[1] : 0));
-    const int pwo = (int)align_up(std::max(maxlen, kOffPad), 8);
+    const int pwo = (int)align_up(std::max(maxlen, kOffPad), kOffPad);
     hp.pwo = pwo;
     hp.pattern.assign(pats.size() * kPatHdr, 0);
     hp.offs.assign(pats.size() * R * pwo, 0);
@@ -691,6 +699,28 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
                 hp.offs[(k * R + ph) * pwo + e] = (int16_t)off;
             }
         (void)lenp;
+    }
+    // Start gates: a task that polls its predecessor begins only once the
+    // predecessor has published its row of step `gate_steps`.  Without the gate
+    // the consumer settles right behind its producer and finds a pending value
+    // on most steps (each wait costs a sleep + L2 round trip for the whole CTA);
+    // with it the lag carries that many steps of slack.
+    hp.gate.assign(ntask, -1);
+    {
+        static const int gate_steps = getenv("PD_WF_GATE") ? atoi(getenv("PD_WF_GATE")) : 8;
+        if (gate_steps > 0)
+            for (int64_t task = 1; task < ntask; ++task) {
+                bool polls = false;
+                for (int64_t q = task * TR; q < (task + 1) * TR && !polls; ++q)
+                    polls = pats[pid[q]][1] > 0;
+                if (!polls) continue;
+                const int target = std::min(gate_steps, hp.S[task - 1] - 1);
+                for (int64_t q = (task - 1) * TR; q < task * TR; ++q)
+                    if (step[q] == target) {
+                        hp.gate[task] = row_of(q);
+                        break;
+                    }
+            }
     }
     // step blocks: rows of (task, step) grouped per node grid, line-contiguous
     hp.boff.assign(ntask, 0);
@@ -769,7 +799,7 @@ bool configure_launch_pad(Ctx& c, WfPlan& p) {
     constexpr int kPatHdr = 2 + NG;
     const size_t fixed = (size_t)((p.T + 31) / 32 * 32) *
                              (p.R + (p.gfirst ? 0 : NG) + (PAD ? 1 : 0)) * sizeof(double) +
-                         (size_t)(p.maxS + 1) * sizeof(int64_t) + 16 +
+                         (size_t)(p.maxS + 1) * sizeof(int32_t) + 16 +
                          align_up((size_t)p.npat * kPatHdr * sizeof(int32_t), 16) +
                          align_up((size_t)p.npat * p.R * p.pwo * sizeof(int16_t), 16);
     int dev_max = 0;
@@ -842,6 +872,7 @@ void upload(WfPlan& p, HostPlan& hp, int64_t n, int G, int64_t nline, int64_t np
     up(p.boff, hp.boff);
     up(p.bofs, hp.bofs);
     up(p.q0, hp.q0);
+    up(p.gate, hp.gate);
     up(p.pattern, hp.pattern);
     up(p.offs, hp.offs);
     up(p.blob, hp.blob);
