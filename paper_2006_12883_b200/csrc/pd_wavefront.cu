@@ -219,16 +219,15 @@ __device__ __forceinline__ void sts_f64(unsigned a, double v) {
 
 // One CTA per task (up to kMaxGroups node grids: the M nodes of one or more
 // time steps), tickets in topological order so a CTA only waits on tasks
-// already claimed by running CTAs.  Virtual thread v = g*nline + line walks
-// points x = 0.. of line `line` of grid g (in sweep order); a real thread runs
-// GU virtual threads (the GU node grids of its line: rows of one step are
-// independent, so their chains interleave and every thread gets the same
-// node mix).  Shared memory is addressed through 32-bit shared-window offsets.
+// already claimed by running CTAs.  Thread t = g*nline + line walks points
+// x = 0.. of line `line` of grid g (in sweep order), one row per wavefront step.
+// (A thread running the M node rows of its line measured slower on every C2
+// level: the per-step chain lengthens.)  Shared memory is addressed through
+// 32-bit shared-window offsets.
 template <bool UPPER, int NG, bool PAD>
 __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
     k_wf_sweep(WfDev P, const double* __restrict__ b, double* y, unsigned long long* counter,
                const int* guard, int want) {
-    constexpr int GU = 1;  // virtual threads per thread (GU > 1 measured slower)
     if (guard_off(guard, want)) return;
     extern __shared__ __align__(128) unsigned char sm[];
     __shared__ unsigned long long bar[kMaxStages];
@@ -240,7 +239,7 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
     const bool gf = P.gfirst != 0;  // polled values folded from registers, no ring slots
     const unsigned Tp = (unsigned)(T + 31) & ~31u, RW = (unsigned)(R + (gf ? 0 : NG));
     const unsigned sb = (unsigned)P.stage_bytes;
-    // layout (bytes from sm): stages | ring [RW][Tp] f64 | bofs [maxS+1] | patterns | offsets
+    // layout (bytes from sm): stages | ring [RW(+1)][Tp] f64 | block offsets | patterns | offsets
     const unsigned nst = (unsigned)P.stages;
     const unsigned o_ring = nst * sb;
     // PAD plans read an extra all-zero slot row; unpadded plans skip it (every KB
@@ -253,26 +252,19 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
     int32_t* sbofs = reinterpret_cast<int32_t*>(sm + o_bofs);  // block offsets in the task
     const unsigned u0 = smem_u32(sm);
     const unsigned u_pat = u0 + o_pat, u_off = u0 + o_off;
-    const int nthr = T / GU;  // real threads with work
-    const bool lane = t < nthr;
-    const int line = lane ? t % P.nline : 0, tsub = lane ? t / P.nline : 0;
-    int gj[GU];
-    unsigned ringj[GU];
-    int qlj[GU];
-#pragma unroll
-    for (int j = 0; j < GU; ++j) {
-        gj[j] = tsub * GU + j;
-        ringj[j] = u0 + o_ring + (unsigned)(gj[j] * P.nline + line) * 8u;
-    }
+    const bool lane = t < T;
+    const int g = lane ? t / P.nline : 0, line = lane ? t % P.nline : 0;
+    const unsigned my_ring = u0 + o_ring + (lane ? (unsigned)t : 0u) * 8u;
     const unsigned ring_step = Tp * 8u;             // bytes between ring slots
     const unsigned off_row = (unsigned)pwo * 2u;    // bytes per (pattern, phase) offset row
     const unsigned off_pat = (unsigned)R * off_row;  // bytes per pattern
     if (PAD)
         for (unsigned i = t; i < Tp; i += blockDim.x)  // the zero slot row
             reinterpret_cast<double*>(sm + o_ring)[RW * Tp + i] = 0.0;
-    if (t == 0)
+    if (t == 0) {
         for (unsigned k = 0; k < nst; ++k) mbar_init(&bar[k]);
-    if (t == 0) mbar_init(&bar_tab);
+        mbar_init(&bar_tab);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     __syncthreads();
     // pattern and offset tables: two bulk copies (a per-thread copy loop costs
@@ -324,7 +316,7 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
         };
         if (t == 0)
             for (int s = 0; s < (int)nst - 1 && s < S; ++s) issue(s);
-        auto block_of = [&](int) -> unsigned {
+        auto next_block = [&]() -> unsigned {
             mbar_wait(&bar[wst], wpar);
             const unsigned a = u0 + wst * sb;
             if (++wst == nst) {
@@ -333,115 +325,85 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
             }
             return a;
         };
-        const int q0 = (int)P.q0[task];
-        // per virtual thread: rows done on its line, ring phase, pending result sector
-        int seq[GU];
-        unsigned phase_b[GU], ring_ph[GU];
-        double w0[GU], w1[GU], w2[GU], w3[GU];
-        int wcnt[GU];
-        // the next row of each virtual thread, prepared one step ahead: descriptor,
-        // right-hand side and cross-task values (loads land while this step computes)
-        bool n_act[GU];
-        unsigned n_val[GU], n_stride[GU], n_dval[GU], n_pat[GU], n_ph[GU];
-        int n_len[GU], n_ng[GU];
-        double bn[GU], xn[GU][NGA];
-#pragma unroll
-        for (int j = 0; j < GU; ++j) {
-            qlj[j] = q0 + (gj[j] * P.nline + line) * P.npoint;  // sweep position of x = 0
-            seq[j] = 0;
-            phase_b[j] = ring_ph[j] = 0;
-            w0[j] = w1[j] = w2[j] = w3[j] = 0.0;
-            wcnt[j] = 0;
-        }
-        auto view = [&](unsigned blk, int j, int q) {
-            const int4 h = lds_v4s32(blk + 16u * (unsigned)gj[j]);  // lo, cnt, pid_off, val_off
+        const int qline = (int)P.q0[task] + t * P.npoint;  // sweep position of x = 0
+        int seq = 0;                  // rows done on this line
+        unsigned phase_b = 0, ring_ph = 0;  // ring phase: offset-row and slot byte offsets
+        // results are published per aligned 4-row sector (one 32-byte store instead
+        // of four scattered 8-byte ones); a line's last rows are flushed at its end
+        double w0 = 0.0, w1 = 0.0, w2 = 0.0, w3 = 0.0;
+        int wcnt = 0;
+        // the thread's next row, prepared one step ahead: descriptor, right-hand
+        // side and cross-task values (loads land while this step computes)
+        bool n_act = false;
+        unsigned n_val = 0, n_stride = 0, n_dval = 0, n_pat = 0, n_ph = 0;
+        int n_len = 0, n_ng = 0;
+        double bn = 0.0, xn[NGA];
+        auto view = [&](unsigned blk, int q) {
+            const int4 h = lds_v4s32(blk + 16u * (unsigned)g);  // lo, cnt, pid_off, val_off
             const int i = line - h.x;
             bool act = lane && (unsigned)i < (unsigned)h.y;
             unsigned pid = kIdle;
             if (act) pid = lds_u16(blk + (unsigned)h.z + 2u * (unsigned)i);
             act = act && pid != kIdle;
-            n_act[j] = act;
-            n_val[j] = blk + (unsigned)h.w + 8u * (unsigned)i;
-            n_stride[j] = 8u * (unsigned)h.y;
-            if (UPPER)
-                n_dval[j] = blk + (unsigned)lds_s32(blk + 16u * G + 4u * gj[j]) + 8u * (unsigned)i;
-            n_len[j] = 0;
-            n_ng[j] = 0;
+            n_act = act;
+            n_val = blk + (unsigned)h.w + 8u * (unsigned)i;
+            n_stride = 8u * (unsigned)h.y;
+            if (UPPER) n_dval = blk + (unsigned)lds_s32(blk + 16u * G + 4u * g) + 8u * (unsigned)i;
+            n_len = 0;
+            n_ng = 0;
             int row = 0;
             const unsigned pat = u_pat + pid * (unsigned)(kPatHdr * 4);
-            n_ph[j] = pat;
-            n_pat[j] = u_off + pid * off_pat;
+            n_ph = pat;
+            n_pat = u_off + pid * off_pat;
             if (act) {
                 const int2 lg = lds_v2s32(pat);
-                n_len[j] = lg.x;
-                n_ng[j] = lg.y;
+                n_len = lg.x;
+                n_ng = lg.y;
                 row = UPPER ? n - 1 - q : q;
             }
-            bn[j] = __ldg(b + row);
+            bn = __ldg(b + row);
 #pragma unroll
             for (int k = 0; k < NG; ++k) {
-                const bool pk = k < n_ng[j];
+                const bool pk = k < n_ng;
                 const int go = pk ? lds_s32(pat + 8u + 4u * k) : 0;
                 // first look with a weak (L1-cacheable) load: each word goes from the
                 // sentinel to its final value exactly once per launch (L1 starts clean),
                 // so a weak load sees one or the other; pending values are re-polled
                 // with strong loads below
-                xn[j][k] = __longlong_as_double(
+                xn[k] = __longlong_as_double(
                     (long long)ld_weak_if(pk, y + row + go, (unsigned long long)kPending));
             }
         };
-        {
-            const unsigned blk = block_of(0);
-#pragma unroll
-            for (int j = 0; j < GU; ++j) view(blk, j, qlj[j]);
-        }
+        view(next_block(), qline);
         for (int s = 0; s < S; ++s) {
             // refill the stage freed by step s-1 (everyone passed the barrier)
             if (t == 0 && s + (int)nst - 1 < S) issue(s + (int)nst - 1);
-            bool act[GU];
-            unsigned val[GU], stride[GU], dval[GU], pat[GU], ph[GU];
-            int len[GU], ng[GU];
-            double bb[GU], xs[GU][NGA];
+            const bool act = n_act;
+            const unsigned val = n_val, stride = n_stride, dval = n_dval, pat = n_pat, ph = n_ph;
+            const int len = n_len, ng = n_ng;
+            const double bb = bn;
+            double xs[NGA];
 #pragma unroll
-            for (int j = 0; j < GU; ++j) {
-                act[j] = n_act[j];
-                val[j] = n_val[j];
-                stride[j] = n_stride[j];
-                dval[j] = n_dval[j];
-                pat[j] = n_pat[j];
-                ph[j] = n_ph[j];
-                len[j] = n_len[j];
-                ng[j] = n_ng[j];
-                bb[j] = bn[j];
-#pragma unroll
-                for (int k = 0; k < NG; ++k) xs[j][k] = xn[j][k];
-            }
-            if (s + 1 < S) {
-                const unsigned blk = block_of(s + 1);
-#pragma unroll
-                for (int j = 0; j < GU; ++j) view(blk, j, qlj[j] + seq[j] + (act[j] ? 1 : 0));
-            }
-#pragma unroll
-            for (int j = 0; j < GU; ++j) {
-                if (!act[j]) continue;
-                const int q = qlj[j] + seq[j];
+            for (int k = 0; k < NG; ++k) xs[k] = xn[k];
+            if (s + 1 < S) view(next_block(), qline + seq + (act ? 1 : 0));
+            if (act) {
+                const int q = qline + seq;
                 const int row = UPPER ? n - 1 - q : q;
-                // cross-task values: wait until published, then into the own slots
-                double acc = bb[j];
-                unsigned fa = val[j];
-                if (NG > 0 && ng[j] > 0) {
+                double acc = bb;
+                unsigned fa = val;
+                if (NG > 0 && ng > 0) {
                     // cross-task values: resolve the (rare) pending ones by strong polls
                     unsigned long long u[NGA];
 #pragma unroll
                     for (int k = 0; k < NG; ++k) {
-                        u[k] = (unsigned long long)__double_as_longlong(xs[j][k]);
-                        if (k < ng[j]) {
+                        u[k] = (unsigned long long)__double_as_longlong(xs[k]);
+                        if (k < ng) {
                             if (P.trace) {  // diagnostics: polls, and polls found pending
                                 atomicAdd(P.trace + 2 * P.ntask + 1, 1ull);
                                 if (u[k] == kPending) atomicAdd(P.trace + 2 * P.ntask, 1ull);
                             }
                             if (u[k] == kPending) {
-                                const int go = lds_s32(ph[j] + 8u + 4u * k);
+                                const int go = lds_s32(ph + 8u + 4u * k);
                                 unsigned int ns = 32;
                                 do {
                                     __nanosleep(ns);
@@ -455,68 +417,67 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
                         double fg[NGA];
 #pragma unroll
                         for (int k = 0; k < NG; ++k)
-                            if (k < ng[j]) fg[k] = lds_f64(fa + (unsigned)k * stride[j]);
+                            if (k < ng) fg[k] = lds_f64(fa + (unsigned)k * stride);
 #pragma unroll
                         for (int k = 0; k < NG; ++k)
-                            if (k < ng[j])
+                            if (k < ng)
                                 acc = sub(acc, mul(fg[k], __longlong_as_double((long long)u[k])));
-                        fa += (unsigned)ng[j] * stride[j];
+                        fa += (unsigned)ng * stride;
                     } else {
 #pragma unroll
                         for (int k = 0; k < NG; ++k)
-                            if (k < ng[j])
-                                sts_f64(ringj[j] + (unsigned)(R + k) * ring_step,
+                            if (k < ng)
+                                sts_f64(my_ring + (unsigned)(R + k) * ring_step,
                                         __longlong_as_double((long long)u[k]));
                     }
                 }
-                const unsigned orow = pat[j] + phase_b[j];
+                const unsigned orow = pat + phase_b;
                 // PAD: len is padded to kChunk with zero entries, no per-entry predicates
 #pragma unroll 1
-                for (int k0 = 0; k0 < len[j]; k0 += kChunk) {
+                for (int k0 = 0; k0 < len; k0 += kChunk) {
                     int o0, o1, o2, o3;
                     lds_v4s16(orow + 2u * (unsigned)k0, o0, o1, o2, o3);
                     const int oi[kChunk] = {o0, o1, o2, o3};
                     double v[kChunk], f[kChunk];
 #pragma unroll
                     for (int k = 0; k < kChunk; ++k)
-                        if (PAD || k0 + k < len[j]) {
-                            v[k] = lds_f64(ringj[j] + 8u * (unsigned)oi[k]);
-                            f[k] = lds_f64(fa + (unsigned)k * stride[j]);
+                        if (PAD || k0 + k < len) {
+                            v[k] = lds_f64(my_ring + 8u * (unsigned)oi[k]);
+                            f[k] = lds_f64(fa + (unsigned)k * stride);
                         }
 #pragma unroll
                     for (int k = 0; k < kChunk; ++k)
-                        if (PAD || k0 + k < len[j]) acc = sub(acc, mul(f[k], v[k]));
-                    fa += kChunk * stride[j];
+                        if (PAD || k0 + k < len) acc = sub(acc, mul(f[k], v[k]));
+                    fa += kChunk * stride;
                 }
-                if (UPPER) acc = acc / lds_f64(dval[j]);
+                if (UPPER) acc = acc / lds_f64(dval);
                 {
                     const int sl = row & 3;
-                    w0[j] = sl == 0 ? acc : w0[j];
-                    w1[j] = sl == 1 ? acc : w1[j];
-                    w2[j] = sl == 2 ? acc : w2[j];
-                    w3[j] = sl == 3 ? acc : w3[j];
-                    ++wcnt[j];
-                    if ((UPPER ? sl == 0 : sl == 3) || seq[j] + 1 == P.npoint) {
+                    w0 = sl == 0 ? acc : w0;
+                    w1 = sl == 1 ? acc : w1;
+                    w2 = sl == 2 ? acc : w2;
+                    w3 = sl == 3 ? acc : w3;
+                    ++wcnt;
+                    if ((UPPER ? sl == 0 : sl == 3) || seq + 1 == P.npoint) {
                         double* g0 = y + (row & ~3);
-                        const int wc = wcnt[j];
-                        if (wc == 4 && y32) {
-                            st_strong4(g0, w0[j], w1[j], w2[j], w3[j]);
+                        if (wcnt == 4 && y32) {
+                            st_strong4(g0, w0, w1, w2, w3);
                         } else {  // partial sector: rows [lo, hi] of this group
-                            const int lo = UPPER ? sl : sl - wc + 1;
-                            const int hi = UPPER ? sl + wc - 1 : sl;
-                            if (lo <= 0 && 0 <= hi) st_strong(g0, w0[j]);
-                            if (lo <= 1 && 1 <= hi) st_strong(g0 + 1, w1[j]);
-                            if (lo <= 2 && 2 <= hi) st_strong(g0 + 2, w2[j]);
-                            if (lo <= 3 && 3 <= hi) st_strong(g0 + 3, w3[j]);
+                            const int lo = UPPER ? sl : sl - wcnt + 1;
+                            const int hi = UPPER ? sl + wcnt - 1 : sl;
+                            if (lo <= 0 && 0 <= hi) st_strong(g0, w0);
+                            if (lo <= 1 && 1 <= hi) st_strong(g0 + 1, w1);
+                            if (lo <= 2 && 2 <= hi) st_strong(g0 + 2, w2);
+                            if (lo <= 3 && 3 <= hi) st_strong(g0 + 3, w3);
                         }
-                        wcnt[j] = 0;
+                        wcnt = 0;
                     }
                 }
-                sts_f64(ringj[j] + ring_ph[j], acc);
-                ++seq[j];
-                const bool wrap = phase_b[j] + off_row == off_pat;
-                phase_b[j] = wrap ? 0u : phase_b[j] + off_row;
-                ring_ph[j] = wrap ? 0u : ring_ph[j] + ring_step;
+                sts_f64(my_ring + ring_ph, acc);
+                ++seq;
+                const bool wrap = phase_b + off_row == off_pat;
+                phase_b = wrap ? 0u : phase_b + off_row;
+                ring_ph = wrap ? 0u : ring_ph + ring_step;
             }
             __syncthreads();
         }
@@ -795,7 +756,6 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
 
 template <bool UPPER, int NG, bool PAD>
 bool configure_launch_pad(Ctx& c, WfPlan& p) {
-    constexpr int GU = 1;
     constexpr int kPatHdr = 2 + NG;
     const size_t fixed = (size_t)((p.T + 31) / 32 * 32) *
                              (p.R + (p.gfirst ? 0 : NG) + (PAD ? 1 : 0)) * sizeof(double) +
@@ -815,7 +775,7 @@ bool configure_launch_pad(Ctx& c, WfPlan& p) {
     stages = std::max(kMinStages, std::min(kMaxStages, stages));
     const size_t smem = stages * p.stage_bytes + fixed;
     p.stages = stages;
-    const int threads = (p.T / GU + 31) / 32 * 32;
+    const int threads = (p.T + 31) / 32 * 32;
     const int max_threads = NG <= kNgFine ? 768 : 512;
     if (getenv("PD_WF_VERBOSE"))
         fprintf(stderr, "[wf] %s NG=%d PAD=%d T=%d R=%d npat=%d pwo=%d stage=%zu smem=%zu (max %d)\n",
