@@ -280,6 +280,9 @@ struct SdcLevelDev {
     std::vector<std::unique_ptr<DenseLU>> dlu;
     // ILU(0) of each node operator (solver 2: the reference's GMRES path)
     std::vector<std::unique_ptr<Ilu0>> ilu;
+    std::unique_ptr<Csr> Jn;      // implicit-mode Newton Jacobian (Kh's pattern), lazily built
+    std::unique_ptr<Ilu0> Jilu;   // its ILU(0), refactored per Newton step
+    DevBuf<double> nw_g, nw_d;    // Newton residual and step (S each)
     // spectral inverse (solver 3): Kh = s * sum_axes T_axis, T = Phi diag(mu) Phi^T
     int spec_dim = 0;
     int64_t spec_n = 0;
@@ -559,6 +562,32 @@ __global__ void k_node_newton_tri(const int64_t* __restrict__ rp, const int32_t*
     node_newton_tri_worker(rp, ci, kv, mh, S, q, gamma, kind, b, x, gbuf, lbuf, ubuf, w, err);
 }
 
+// Implicit-mode Newton node solve, general Kh (pfasst.py:134-152), one worker:
+// -g, g = mh*u + q*(Kh u + gamma*mh*r(u)) - b  (numpy's left-to-right order;
+// Ku = Kh u; negation is exact, and |-g| = |g| for the stopping test)
+__global__ void k_newton_negg(const double* __restrict__ u, const double* __restrict__ Ku,
+                              const double* __restrict__ mh, double q, double gamma, int kind,
+                              const double* __restrict__ b, double* neg_g, int64_t S) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < S;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const double inner = add(Ku[j], mul(mul(gamma, mh[j]), react(kind, u[j])));
+        neg_g[j] = -sub(add(mul(mh[j], u[j]), mul(q, inner)), b[j]);
+    }
+}
+// J = Mh + q*(Kh + gamma*diag(mh*r'(u))) on Kh's pattern (which holds the diagonal):
+// off-diagonal q*k, diagonal mh + q*(k + gamma*(mh*r'(u)))  (scipy sparse sums)
+__global__ void k_newton_jvals(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                               const double* __restrict__ kv, const double* __restrict__ mh,
+                               const double* __restrict__ u, double q, double gamma, int kind,
+                               double* jv, int64_t S) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < S;
+         j += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t p = rp[j]; p < rp[j + 1]; ++p)
+            jv[p] = ci[p] == j
+                ? add(mh[j], mul(q, add(kv[p], mul(gamma, mul(mh[j], react_d(kind, u[j]))))))
+                : mul(q, kv[p]);
+}
+
 // z /= (mh + q*s*sum_axes mu_{i_axis})  (eigenvalues of the node operator)
 __global__ void k_spec_scale(double* z, int64_t total, int64_t n, int dim,
                              const double* __restrict__ mu, double mh, double qs) {
@@ -666,6 +695,51 @@ static void node_apply_inverse(SdcLevelDev& L, int m, const double* r, double* z
 }
 
 // x (in: guess, out: solution) for W workers; b = mh*rhs (W x S contiguous)
+// pfasst.py:134-152 for a general Kh, worker by worker: Newton (<= 50 steps,
+// stop at |g| <= 1e-12*max(1,|b|)) with J delta = -g solved by the reference's
+// GMRES(30, max 200) + ILU(0) of J (tol 1e-13 rel, 1e-13*scale abs)
+static void node_newton_general(SdcLevelDev& L, int m, const double* b, double* x, int W) {
+    Ctx& c = L.c;
+    const int64_t S = L.S;
+    const double q = L.dt * L.QDI.a[m * L.M + m];
+    if (!L.Jn) {
+        const Csr& K = *L.Kh;
+        L.Jn = csr_upload(c, S, S, K.nnz, K.rowptr.p, K.col.p, K.val.p, true);
+        L.Jilu = ilu0_create(c, *L.Jn, 1);
+        L.nw_g.alloc(S);
+        L.nw_d.alloc(S);
+    }
+    const int gb = c.grid_for(S, TB);
+    for (int w = 0; w < W; ++w) {
+        const double* bw = b + (int64_t)w * S;
+        double* u = x + (int64_t)w * S;
+        const double scale = std::max(1.0, vec_norm_host(c, bw, S));
+        bool done = false;
+        for (int it = 0; it < 50 && !done; ++it) {
+            bspmv(c, *L.Kh, u, S, L.nw_d.p, S, 1, 0);  // Kh u
+            launch(k_newton_negg, gb, TB, 0, c.stream, u, (const double*)L.nw_d.p, L.mh.p, q,
+                   L.gamma, L.kind, bw, L.nw_g.p, S);
+            const double gn = vec_norm_host(c, L.nw_g.p, S);
+            if (!std::isfinite(gn)) throw SolverError("node Newton solve failed at node " +
+                                                      std::to_string(m), m);
+            if (gn <= 1e-12 * scale) {
+                done = true;
+                break;
+            }
+            launch(k_newton_jvals, gb, TB, 0, c.stream, L.Kh->rowptr.p, L.Kh->col.p,
+                   L.Kh->val.p, L.mh.p, (const double*)u, q, L.gamma, L.kind, L.Jn->val.p, S);
+            ilu0_refactor(c, *L.Jilu);
+            auto r = gmres_run(c, *L.Jn, L.Jilu.get(), L.nw_g.p, nullptr, L.nw_d.p, 1e-13,
+                               1e-13 * scale, 30, 200);
+            if (r.diverged)
+                throw SolverError("node Newton solve failed at node " + std::to_string(m), m);
+            vec_axpy_inplace(c, u, L.nw_d.p, S);
+        }
+        if (!done)
+            throw SolverError("node Newton iteration stalled at node " + std::to_string(m), m);
+    }
+}
+
 static void node_solve(SdcLevelDev& L, int m, const double* b, double* x, int W, int rounds) {
     Ctx& c = L.c;
     if (L.solver == 2) {
@@ -953,9 +1027,6 @@ void sdc_sweep(SdcLevelDev& L, double* U, const double* U0, const double* tau, i
     const int64_t n = (int64_t)W * M * S;
     const bool imex = L.imex && L.gamma != 0.0;
     if (W > L.maxW) throw ConfigError("too many workers for this SDC level");
-    if (L.gamma != 0.0 && !imex && L.solver != 0)
-        throw ConfigError("implicit-mode nonlinear node solves need a tridiagonal Kh on the "
-                          "device (use mode='imex', the reference default for gamma > 0)");
     if (fused_ok(L)) {
         launch(k_fused_sweep, (unsigned)((W * 32 + 127) / 128), 128, 0, c.stream, fused_params(L),
                U, U0, tau, W);
@@ -979,7 +1050,9 @@ void sdc_sweep(SdcLevelDev& L, double* U, const double* U0, const double* tau, i
                L.QDI, L.QDE, imex ? 1 : 0);
         launch(k_gather_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, U, L.x.p, W, M, S,
                m);
-        if (L.gamma != 0.0 && !imex) {
+        if (L.gamma != 0.0 && !imex && L.solver != 0) {
+            node_newton_general(L, m, L.bvec.p, L.x.p, W);  // x holds the guess U[m]
+        } else if (L.gamma != 0.0 && !imex) {
             // the back sweep updates u in place: x holds the guess U[m]
             launch(k_node_newton_tri, (W + 31) / 32, 32, 0, c.stream, L.Kh->rowptr.p,
                    L.Kh->col.p, L.Kh->val.p, L.mh.p, S, L.dt * L.QDI.a[m * M + m], L.gamma,
