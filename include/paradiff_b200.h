@@ -71,6 +71,13 @@ int pd_ilu0_levels(void *ilu, int32_t *lower_levels, int32_t *upper_levels); /* 
 int pd_ilu0_set_wavefront(void *ctx, void *ilu, int64_t ngroup, int64_t nline, int64_t npoint,
                           int64_t ngroup_lower, int *applied);                    /* synchronising */
 int pd_ilu0_destroy(void *ilu);
+/* Structured SpMV for a 2D-grid space-time operator (SMG Galerkin levels: every
+ * row couples to the previous step's last node and to each node of its own
+ * step through a 3x3 neighbourhood; nt steps, M nodes, n x n points).  When the
+ * CSR has exactly that pattern its values are copied as [position][row] and
+ * pd_csr_spmv uses them (bitwise the CSR product: same per-row order); value
+ * updates of the CSR refresh the copy.  *applied = 0: pattern differs. */
+int pd_csr_set_grid(void *ctx, void *csr, int64_t nt, int M, int64_t n, int *applied);
 
 /* ---- dense LU of the coarsest level (linalg.py:196-209 DenseLU) ---------- */
 int pd_dense_lu_create(void *ctx, void *csr, void **lu_out); /* synchronising */

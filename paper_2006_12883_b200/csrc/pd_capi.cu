@@ -128,6 +128,12 @@ int pd_ilu0_set_wavefront(void* ctx, void* ilu, int64_t ngroup, int64_t nline, i
         if (applied) *applied = ok ? 1 : 0;
     });
 }
+int pd_csr_set_grid(void* ctx, void* csr, int64_t nt, int M, int64_t n, int* applied) {
+    return guarded([&] {
+        const bool ok = pd::csr_attach_grid(*C(ctx), *H<pd::Csr>(csr, "csr"), nt, M, n);
+        if (applied) *applied = ok ? 1 : 0;
+    });
+}
 int pd_ilu0_destroy(void* ilu) {
     return guarded([&] { delete static_cast<pd::Ilu0*>(ilu); });
 }

@@ -103,6 +103,8 @@ struct Ctx {
 void mode_product(Ctx& c, const double* in, double* out, int64_t total, int64_t n,
                   int64_t stride, const double* phi, int transpose);
 
+struct GridSpmv;  // structured copy of a 2D space-time grid operator (pd_gspmv.cu)
+
 // CSR on device: int64 row pointers (nnz may exceed 2^31 at C3/C5 sizes),
 // int32 column indices, fp64 values.  Column indices sorted per row.
 struct Csr {
@@ -110,6 +112,10 @@ struct Csr {
     DevBuf<int64_t> rowptr;
     DevBuf<int32_t> col;
     DevBuf<double> val;
+    // optional structured copy used by csr_spmv; writers of `val` set grid_stale
+    mutable std::shared_ptr<GridSpmv> grid;
+    mutable bool grid_stale = false;
+    void values_changed() const { grid_stale = grid != nullptr; }
 };
 
 // Structured wavefront schedule of one ILU(0) triangular sweep (pd_wavefront.cu):
@@ -181,6 +187,13 @@ std::unique_ptr<Csr> csr_upload(Ctx& c, int64_t nrows, int64_t ncols, int64_t nn
                                 const int64_t* rowptr, const int32_t* col, const double* val,
                                 bool device_src);
 void csr_update_values(Ctx& c, Csr& A, const double* val, bool device_src);
+
+// structured Galerkin SpMV (pd_gspmv.cu): attach when A has the 2D grid
+// space-time pattern (nt steps, M nodes, n x n points); grid_spmv = false when
+// A has no structured copy
+bool csr_attach_grid(Ctx& c, Csr& A, int64_t nt, int M, int64_t n);
+bool grid_spmv(Ctx& c, const Csr& A, const double* x, double* y, int mode, const double* b,
+               const int* guard, int want, double* norm2, int* nonfinite);
 
 // ILU(0)
 std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks);

@@ -454,6 +454,7 @@ void Multigrid::set_fine_values(const double* vals) {
     Csr& A0 = *lv[0].A;
     PD_CUDA(cudaMemcpyAsync(A0.val.p, vals, A0.nnz * sizeof(double), cudaMemcpyDeviceToDevice,
                             c.stream));
+    A0.values_changed();
     for (size_t l = 0; l + 1 < lv.size(); ++l) {
         spgemm_values(c, *lv[l].R, *lv[l].A, *galerkin_T[l]);
         spgemm_values(c, *galerkin_T[l], *lv[l].P, *lv[l + 1].A);

@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(BS) k_spmv(int64_t n, const int64_t* __restric
 void csr_spmv(Ctx& c, const Csr& A, const double* x, double* y, int mode, const double* b,
               const int* guard, int want, double* norm2_out, int* nonfinite_flag) {
     if (A.nrows <= 0) return;
+    if (A.grid && grid_spmv(c, A, x, y, mode, b, guard, want, norm2_out, nonfinite_flag)) return;
     if (norm2_out) {
         int g = std::min(c.grid_for(A.nrows, BS, 8), kReduceMaxBlocks);
         launch(k_spmv<true>, g, BS, 0, c.stream, A.nrows, A.rowptr.p, A.col.p, A.val.p, x, y,
@@ -256,6 +257,7 @@ void csr_update_values(Ctx& c, Csr& A, const double* val, bool device_src) {
     PD_CUDA(cudaMemcpyAsync(A.val.p, val, A.nnz * sizeof(double),
                             device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                             c.stream));
+    A.values_changed();
 }
 
 // ------------------------------------------------------------------ block-Jacobi masking
@@ -1005,6 +1007,7 @@ void spgemm_values(Ctx& c, const Csr& A, const Csr& B, Csr& C) {
     launch(k_spgemm_values, c.grid_for(C.nrows, BS, 8), BS, 0, c.stream, C.nrows, A.rowptr.p,
            A.col.p, A.val.p, B.rowptr.p, B.col.p, B.val.p, C.rowptr.p, C.col.p, C.val.p);
     PD_LAUNCH_CHECK();
+    C.values_changed();
 }
 
 // ------------------------------------------------------------------ Newton Jacobian values

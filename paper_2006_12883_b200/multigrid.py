@@ -262,6 +262,18 @@ class MultigridHierarchy:
     def _enable_wavefront(self) -> None:
         from .linalg import set_wavefront
 
+        # structured SpMV for the Galerkin levels of 2D grids (level 0 runs K1)
+        self.grid_spmv = [False] * len(self.dims)
+        for l in range(1, len(self.dims)):
+            g = self.grids[l] if l < len(self.grids) else None
+            if g is None or g[0] != g[1]:
+                continue
+            A = ctypes.c_void_p()
+            N.call("pd_mg_level_matrix", self._mg, l, ctypes.byref(A))
+            applied = ctypes.c_int()
+            d = self.dims[l]
+            N.call("pd_csr_set_grid", self.ctx.handle, A, d.nt, d.m, g[0], ctypes.byref(applied))
+            self.grid_spmv[l] = bool(applied.value)
         self.wavefront = []
         for l in range(len(self.dims) - 1):
             g = self.grids[l] if l < len(self.grids) else None

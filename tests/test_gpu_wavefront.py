@@ -115,3 +115,29 @@ def test_wavefront_mg_bitwise_vs_level_sweeps(monkeypatch, strategy):
     (x1, r1), (x2, r2) = out["level"], out["wavefront"]
     assert r1.iterations == r2.iterations and r1.converged
     np.testing.assert_array_equal(x1, x2)
+
+
+def test_grid_spmv_galerkin_levels_bitwise(monkeypatch):
+    """Structured SpMV (pd_csr_set_grid) on SMG Galerkin levels: every level's product
+    is bitwise scipy's; whole solves match the CSR path with equal cycle counts (the
+    fused residual norms reduce over a different block tree, so GMRES scalars may
+    differ in the last bit: rel 1e-12)."""
+    from paper_2006_12883_b200 import _native as N
+
+    cfg, s = _system("C2", 31, 8)
+    h = pd.build_hierarchy(s, "SMG", 4, 2, partitions=2)
+    assert h.grid_spmv[1:3] == [True, True]
+    rng = np.random.default_rng(5)
+    for l in range(1, 4):
+        A = h.matrices[l]
+        x = rng.standard_normal(A.shape[1])
+        got = h._dev_mats[l].matvec_dev(N.to_device(x)).cpu().numpy()
+        np.testing.assert_array_equal(got, pd.linalg.as_csr(A) @ x)
+    b = s.rhs()
+    x1, r1 = h.solve(b, tol_rel=1e-10, tol_abs=1e-10)
+    monkeypatch.setenv("PD_NO_GRID_SPMV", "1")
+    h2 = pd.build_hierarchy(s, "SMG", 4, 2, partitions=2)
+    assert not any(h2.grid_spmv)
+    x2, r2 = h2.solve(b, tol_rel=1e-10, tol_abs=1e-10)
+    assert r1.iterations == r2.iterations and r1.converged
+    assert np.linalg.norm(x1 - x2) <= 1e-12 * np.linalg.norm(x2)
