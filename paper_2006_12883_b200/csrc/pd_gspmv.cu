@@ -52,7 +52,7 @@ __global__ void k_gspmv_gather(int64_t N, int M, int n, const int64_t* __restric
 }
 
 template <int M, bool REDUCE>
-__global__ void __launch_bounds__(GB) k_gspmv(int64_t nt, int n, int gy, int64_t N,
+__global__ void __launch_bounds__(GB, 5) k_gspmv(int64_t nt, int n, int gy, int64_t N,
                                               const double* __restrict__ vals,
                                               const double* __restrict__ xv, double* y, int mode,
                                               const double* b, const int* guard, int want,
