@@ -129,7 +129,7 @@ struct WfPlan {
     bool gfirst = false;  // cross-task entries lead every pattern (no ring slots)
     size_t smem = 0, stage_bytes = 0;
     DevBuf<int32_t> nsteps;
-    DevBuf<int64_t> boff, bofs, q0, gate;
+    DevBuf<int64_t> boff, bofs, q0;
     DevBuf<int32_t> pattern;         // per pattern: len, ng, global offsets
     DevBuf<int16_t> offs;            // per pattern and ring phase: source offsets
     DevBuf<unsigned char> blob;      // step blocks

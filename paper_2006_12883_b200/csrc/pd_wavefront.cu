@@ -66,7 +66,6 @@ struct WfDev {
     const int64_t* boff;     // per task: first index into bofs
     const int64_t* bofs;     // byte offset of every step block (+1 sentinel per task)
     const int64_t* q0;       // per task: sweep position of its first row
-    const int64_t* gate;     // per task: predecessor row to await before starting (-1: none)
     const int32_t* pattern;  // [npat][2 + NG]
     const int16_t* offs;     // [npat][R][pwo]
     const unsigned char* blob;
@@ -82,7 +81,6 @@ WfDev wf_dev(WfPlan& p) {
     d.boff = p.boff.p;
     d.bofs = p.bofs.p;
     d.q0 = p.q0.p;
-    d.gate = p.gate.p;
     d.pattern = p.pattern.p;
     d.offs = p.offs.p;
     d.blob = p.blob.p;
@@ -301,11 +299,6 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
         const int64_t bo = P.boff[task];
         const int64_t base = P.bofs[bo];
         for (int s = t; s <= S; s += blockDim.x) sbofs[s] = (int32_t)(P.bofs[bo + s] - base);
-        if (t == 0) {  // start gate (see build_plan)
-            const int64_t gr = P.gate[task];
-            if (gr >= 0)
-                while (ld_strong_u64(y + gr) == kPending) __nanosleep(128);
-        }
         __syncthreads();
         // blocks are issued and consumed in order, once each: running stage
         // indices (no runtime division by the stage count)
@@ -505,7 +498,7 @@ __global__ void k_wf_gather(int64_t nslot, const int32_t* srow, const int64_t* s
 
 struct HostPlan {
     std::vector<int32_t> S;
-    std::vector<int64_t> boff, bofs, q0, gate;
+    std::vector<int64_t> boff, bofs, q0;
     std::vector<int32_t> pattern;
     std::vector<int16_t> offs;
     int R = 0, pwo = 0, ng = 0;
@@ -661,28 +654,6 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
             }
         (void)lenp;
     }
-    // Start gates: a task that polls its predecessor begins only once the
-    // predecessor has published its row of step `gate_steps`.  Without the gate
-    // the consumer settles right behind its producer and finds a pending value
-    // on most steps (each wait costs a sleep + L2 round trip for the whole CTA);
-    // with it the lag carries that many steps of slack.
-    hp.gate.assign(ntask, -1);
-    {
-        static const int gate_steps = getenv("PD_WF_GATE") ? atoi(getenv("PD_WF_GATE")) : 8;
-        if (gate_steps > 0)
-            for (int64_t task = 1; task < ntask; ++task) {
-                bool polls = false;
-                for (int64_t q = task * TR; q < (task + 1) * TR && !polls; ++q)
-                    polls = pats[pid[q]][1] > 0;
-                if (!polls) continue;
-                const int target = std::min(gate_steps, hp.S[task - 1] - 1);
-                for (int64_t q = (task - 1) * TR; q < task * TR; ++q)
-                    if (step[q] == target) {
-                        hp.gate[task] = row_of(q);
-                        break;
-                    }
-            }
-    }
     // step blocks: rows of (task, step) grouped per node grid, line-contiguous
     hp.boff.assign(ntask, 0);
     hp.q0.assign(ntask, 0);
@@ -832,7 +803,6 @@ void upload(WfPlan& p, HostPlan& hp, int64_t n, int G, int64_t nline, int64_t np
     up(p.boff, hp.boff);
     up(p.bofs, hp.bofs);
     up(p.q0, hp.q0);
-    up(p.gate, hp.gate);
     up(p.pattern, hp.pattern);
     up(p.offs, hp.offs);
     up(p.blob, hp.blob);
