@@ -280,6 +280,7 @@ struct SdcLevelDev {
     std::vector<std::unique_ptr<DenseLU>> dlu;
     // ILU(0) of each node operator (solver 2: the reference's GMRES path)
     std::vector<std::unique_ptr<Ilu0>> ilu;
+    DevBuf<int> open_count;       // refinement: workers still open (host early exit)
     std::unique_ptr<Csr> Jn;      // implicit-mode Newton Jacobian (Kh's pattern), lazily built
     std::unique_ptr<Ilu0> Jilu;   // its ILU(0), refactored per Newton step
     DevBuf<double> nw_g, nw_d;    // Newton residual and step (S each)
@@ -415,6 +416,11 @@ __global__ void k_refine_update(double* x, const double* z, int W, int64_t S, co
         const int64_t w = t / S;
         if (!done[w]) x[t] = add(x[t], z[t]);
     }
+}
+
+__global__ void k_count_open(const int* done, int W, int* count) {
+    const int w = blockIdx.x * blockDim.x + threadIdx.x;
+    if (w < W && !done[w]) atomicAdd(count, 1);
 }
 
 __global__ void k_any_open(const int* done, int W, int* err) {
@@ -772,7 +778,21 @@ static void node_solve(SdcLevelDev& L, int m, const double* b, double* x, int W,
     bnorm(L, L.r.p, S, S, W, L.beta.p, true);
     launch(k_refine_check, (W + 127) / 128, 128, 0, c.stream, L.beta.p, bn, L.beta0.p, L.thr.p,
            L.lowest.p, L.done.p, L.err.p, W, 0, 1e-13);
+    // An exact (spectral) inverse usually meets the threshold after one round;
+    // a further round would only be masked out worker by worker, so for large
+    // batches a one-int host check skips it (same result, no wasted GEMMs).
+    const bool probe = L.solver == 3 && (int64_t)W * S >= (int64_t)1 << 20;
     for (int k = 0; k < rounds; ++k) {
+        if (probe) {
+            PD_CUDA(cudaMemsetAsync(L.open_count.p, 0, sizeof(int), c.stream));
+            launch(k_count_open, (W + 127) / 128, 128, 0, c.stream, (const int*)L.done.p, W,
+                   L.open_count.p);
+            int open = 0;
+            PD_CUDA(cudaMemcpyAsync(&open, L.open_count.p, sizeof(int), cudaMemcpyDeviceToHost,
+                                    c.stream));
+            PD_CUDA(cudaStreamSynchronize(c.stream));
+            if (open == 0) break;
+        }
         node_apply_inverse(L, m, L.r.p, L.rhs.p + 0, W);  // rhs buffer reused as z
         launch(k_refine_update, c.grid_for(W * S, TB), TB, 0, c.stream, x, L.rhs.p, W, S,
                L.done.p);
@@ -1230,6 +1250,7 @@ int pd_sdc_level_create(void* ctx, void* Kh, const double* mh_host, int M, const
                                K->nnz * sizeof(double), cudaMemcpyDeviceToDevice));
         L->err.alloc(1);
         PD_CUDA(cudaMemset(L->err.p, 0, sizeof(int)));
+        L->open_count.alloc(1);
         if (tri) {
             L->tl.alloc(M * S);
             L->tu.alloc(M * S);

@@ -102,6 +102,14 @@ class TorchComm:
         return t
 
 
+_PROFILE = {} if os.environ.get("PD_PFASST_PROFILE") else None
+
+
+def phase_profile() -> dict:
+    """Seconds per driver phase accumulated under PD_PFASST_PROFILE (diagnostics)."""
+    return dict(_PROFILE or {})
+
+
 def worker_range(P: int, rank: int, size: int) -> tuple[int, int]:
     if P % size != 0:
         raise ConfigurationError(f"workers per window ({P}) must be a multiple of ranks ({size})")
@@ -141,6 +149,16 @@ def run_windows(engine, comm, Nt: int, P: int, tol_rel: float, tol_abs: float,
                     if state["failed"]:
                         return None
                     try:
+                        if _PROFILE is not None:  # PD_PFASST_PROFILE: device time per phase
+                            import torch
+
+                            torch.cuda.synchronize()
+                            t_0 = time.perf_counter()
+                            out = fn(*a)
+                            torch.cuda.synchronize()
+                            _PROFILE[fn.__name__] = _PROFILE.get(fn.__name__, 0.0) + (
+                                time.perf_counter() - t_0)
+                            return out
                         return fn(*a)
                     except SolverError as e:
                         state["failed"] = True

@@ -4,6 +4,7 @@ usage: python scripts/pfasst_full.py [C4] [workers] [max_windows]
 Prints per-window iterations, device time and GDOF/s per fine SDC sweep
 (N_local = P*M*S per window, sweeps = nu * iterations).
 """
+import os
 import sys
 import time
 from pathlib import Path
@@ -41,3 +42,7 @@ for rep in range(2):
     print(f"  run {rep}: iterations max {r.iterations} per window {list(r.inner_iterations)} "
           f"converged={r.converged} {t:.2f} s, {dofs * sweeps / t / 1e9:.3f} GDOF/s per fine "
           f"sweep, {Nt * cfg.M * cfg.spec.ndof / t / 1e9:.3f} GDOF/s solved", flush=True)
+if os.environ.get("PD_PFASST_PROFILE"):
+    from paper_2006_12883_b200.timeslab import phase_profile
+
+    print("phase seconds (both runs):", {k: round(v, 3) for k, v in phase_profile().items()})
