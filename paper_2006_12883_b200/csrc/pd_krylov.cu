@@ -11,6 +11,8 @@
 // kernels on the device; vector kernels read the phase word and exit early
 // when their stage is inactive.  The host only enqueues.
 #include "pd_device.cuh"
+#include <cstddef>
+
 #include "pd_krylov.h"
 
 #include <algorithm>
@@ -327,11 +329,13 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
     PD_LAUNCH_CHECK();
 }
 
-GmDev Gmres::read_state() {
-    GmDev h;
-    PD_CUDA(cudaMemcpyAsync(&h, st.p, sizeof(GmDev), cudaMemcpyDeviceToHost, c.stream));
+const GmDev& Gmres::read_state() {
+    // the host mirrors only the scalar header (phase, j, counters, flags)
+    if (!host_st) host_st = std::make_unique<GmDev>();
+    PD_CUDA(cudaMemcpyAsync(host_st.get(), st.p, offsetof(GmDev, H), cudaMemcpyDeviceToHost,
+                            c.stream));
     PD_CUDA(cudaStreamSynchronize(c.stream));
-    return h;
+    return *host_st;
 }
 
 std::vector<double> Gmres::history(int total) {
@@ -372,13 +376,13 @@ GmresResult gmres_run(Ctx& c, const Csr& A, Ilu0* M, const double* b, const doub
     }
     csr_spmv(c, A, xs, r0.p, SPMV_RESID, b, nullptr, 0, c.scalars.p + 16, nullptr);
     g.enqueue_init(r0.p, c.scalars.p + 16, tol_rel, tol_abs, x0);
-    GmDev s = g.read_state();
+    const GmDev& s = g.read_state();  // refreshed in place by every read_state()
     // the host mirrors (phase, j) after every Arnoldi step; guards cover the rest
     int slot = 0;
     while (s.phase != GM_DONE && s.total < std::max(max_it, 1)) {
         const int j_eff = (s.phase == GM_START) ? 0 : s.j;
         g.enqueue_slot(slot++, j_eff + 2, b);
-        s = g.read_state();
+        g.read_state();
     }
     if (s.err == 1) throw SolverError("non-finite initial residual in GMRES");
     if (s.err == 2) throw SolverError("non-finite residual in GMRES iteration");

@@ -9,7 +9,7 @@
 
 namespace pd {
 
-constexpr int kGmMaxRestart = 64;
+constexpr int kGmMaxRestart = 256;  // restart lengths the reference tests use (up to 100)
 enum GmPhase { GM_START = 0, GM_RUN = 1, GM_FINISH = 2, GM_DONE = 3 };
 
 struct GmDev {
@@ -34,7 +34,7 @@ class Gmres {
     // one Arnoldi step slot (mgs_passes = max j + 2 this slot can need) plus
     // the guarded cycle-finish block; `b` = the GMRES right-hand side
     void enqueue_slot(int slot, int mgs_passes, const double* b);
-    GmDev read_state();  // synchronising
+    const GmDev& read_state();  // synchronising; scalar header only (host mirror)
     double* x() { return xg.p; }
     int64_t size() const { return n; }
     GmDev* dev() { return st.p; }
@@ -49,6 +49,7 @@ class Gmres {
     int64_t n;
     int restart, max_it;
     DevBuf<GmDev> st;
+    std::unique_ptr<GmDev> host_st;  // host mirror (the struct is ~0.5 MB: kept off the stack)
     bool store_z = false;
     DevBuf<double> V, w, z, u, rg, xg, vcur, norm2, hist, Z;
     const double* r0 = nullptr;
