@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
                 n_ng = lg.y;
                 row = UPPER ? n - 1 - q : q;
             }
-            bn = __ldg(b + row);
+            const double* yrow = y + row;
 #pragma unroll
             for (int k = 0; k < NG; ++k) {
                 const bool pk = k < n_ng;
@@ -364,8 +364,9 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
                 // so a weak load sees one or the other; pending values are re-polled
                 // with strong loads below
                 xn[k] = __longlong_as_double(
-                    (long long)ld_weak_if(pk, y + row + go, (unsigned long long)kPending));
+                    (long long)ld_weak_if(pk, yrow + go, (unsigned long long)kPending));
             }
+            bn = __ldg(b + row);
         };
         view(next_block(), qline);
         for (int s = 0; s < S; ++s) {
