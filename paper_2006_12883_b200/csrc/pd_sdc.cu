@@ -281,6 +281,18 @@ struct SdcLevelDev {
     // ILU(0) of each node operator (solver 2: the reference's GMRES path)
     std::vector<std::unique_ptr<Ilu0>> ilu;
     DevBuf<int> open_count;       // refinement: workers still open (host early exit)
+    bool capturing = false;       // inside a CUDA-graph capture (no host synchronisation)
+    struct ChainGraph {
+        const void *U, *U0, *tau, *u0c;
+        int W, nu;
+        cudaGraphExec_t exec;
+    };
+    std::vector<ChainGraph> chain_graphs;  // captured serial coarse chains (pd_sdc_chain)
+    cudaStream_t capture_stream = nullptr;
+    ~SdcLevelDev() {
+        for (auto& g : chain_graphs) cudaGraphExecDestroy(g.exec);
+        if (capture_stream) cudaStreamDestroy(capture_stream);
+    }
     std::unique_ptr<Csr> Jn;      // implicit-mode Newton Jacobian (Kh's pattern), lazily built
     std::unique_ptr<Ilu0> Jilu;   // its ILU(0), refactored per Newton step
     DevBuf<double> nw_g, nw_d;    // Newton residual and step (S each)
@@ -613,6 +625,10 @@ cublasHandle_t blas_of(Ctx& c) {
     if (!c.blas) {
         cublasHandle_t h;
         if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate failed");
+        // a fixed workspace: no allocation inside a captured CUDA graph
+        static thread_local DevBuf<unsigned char> ws;
+        if (!ws.p) ws.alloc((size_t)32 << 20);
+        cublasSetWorkspace(h, ws.p, (size_t)32 << 20);
         c.blas = h;
     }
     auto h = static_cast<cublasHandle_t>(c.blas);
@@ -781,7 +797,7 @@ static void node_solve(SdcLevelDev& L, int m, const double* b, double* x, int W,
     // An exact (spectral) inverse usually meets the threshold after one round;
     // a further round would only be masked out worker by worker, so for large
     // batches a one-int host check skips it (same result, no wasted GEMMs).
-    const bool probe = L.solver == 3 && (int64_t)W * S >= (int64_t)1 << 20;
+    const bool probe = L.solver == 3 && !L.capturing && (int64_t)W * S >= (int64_t)1 << 20;
     for (int k = 0; k < rounds; ++k) {
         if (probe) {
             PD_CUDA(cudaMemsetAsync(L.open_count.p, 0, sizeof(int), c.stream));
@@ -1311,13 +1327,66 @@ int pd_sdc_chain(void* lvl, double* U, double* U0, const double* tau, int W, con
             PD_LAUNCH_CHECK();
             return;
         }
-        for (int w = 0; w < W; ++w) {
-            const double* src = w == 0 ? u0c : U + (int64_t)(w - 1) * MS + (L.M - 1) * S;
-            PD_CUDA(cudaMemcpyAsync(U0 + (int64_t)w * S, src, S * sizeof(double),
-                                    cudaMemcpyDeviceToDevice, c.stream));
-            for (int k = 0; k < nu; ++k)
-                pd::sdc_sweep(L, U + w * MS, U0 + (int64_t)w * S, tau ? tau + w * MS : nullptr, 1);
+        auto chain = [&] {
+            for (int w = 0; w < W; ++w) {
+                const double* src = w == 0 ? u0c : U + (int64_t)(w - 1) * MS + (L.M - 1) * S;
+                PD_CUDA(cudaMemcpyAsync(U0 + (int64_t)w * S, src, S * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, c.stream));
+                for (int k = 0; k < nu; ++k)
+                    pd::sdc_sweep(L, U + w * MS, U0 + (int64_t)w * S,
+                                  tau ? tau + w * MS : nullptr, 1);
+            }
+        };
+        // The chain is W sequential one-worker sweeps of ~100 small launches each:
+        // launch-bound.  Without host synchronisation inside (spectral / dense /
+        // tridiagonal node solves, no general implicit Newton) it is captured once
+        // per buffer set as a CUDA graph and replayed.
+        const bool graphable = (L.solver == 1 || L.solver == 3) &&
+                               !(L.gamma != 0.0 && !(L.imex && L.gamma != 0.0)) &&
+                               !getenv("PD_NO_SDC_GRAPH");
+        if (!graphable) {
+            chain();
+            return;
         }
+        for (auto& g : L.chain_graphs)
+            if (g.U == U && g.U0 == U0 && g.tau == tau && g.u0c == u0c && g.W == W && g.nu == nu) {
+                PD_CUDA(cudaGraphLaunch(g.exec, c.stream));
+                return;
+            }
+        // capture on a private stream (the context's stream may be the legacy
+        // default stream, which cannot be captured); replay on the context's
+        cudaGraph_t graph = nullptr;
+        if (!L.capture_stream)
+            PD_CUDA(cudaStreamCreateWithFlags(&L.capture_stream, cudaStreamNonBlocking));
+        const cudaStream_t orig = c.stream;
+        c.stream = L.capture_stream;
+        L.capturing = true;
+        auto restore = [&] {
+            c.stream = orig;
+            L.capturing = false;
+            if (c.blas) cublasSetStream(static_cast<cublasHandle_t>(c.blas), orig);
+        };
+        PD_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));
+        try {
+            chain();
+        } catch (...) {
+            cudaStreamEndCapture(c.stream, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            restore();
+            throw;
+        }
+        const cudaError_t ce = cudaStreamEndCapture(c.stream, &graph);
+        restore();
+        PD_CUDA(ce);
+        pd::SdcLevelDev::ChainGraph g{U, U0, tau, u0c, W, nu, nullptr};
+        PD_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
+        cudaGraphDestroy(graph);
+        if (L.chain_graphs.size() >= 4) {
+            cudaGraphExecDestroy(L.chain_graphs.front().exec);
+            L.chain_graphs.erase(L.chain_graphs.begin());
+        }
+        L.chain_graphs.push_back(g);
+        PD_CUDA(cudaGraphLaunch(g.exec, c.stream));
     });
 }
 
