@@ -92,23 +92,33 @@ class Comm:
             return float(value)
         import torch
 
-        t = torch.tensor([float(value)], dtype=torch.float64, device=self.device)
+        dev = "cpu" if self._host_staged() else self.device
+        t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
         self.dist.all_reduce(t, group=self.group)
         return float(t.item())
+
+    def _host_staged(self) -> bool:
+        """gloo moves host tensors only: CUDA vectors are staged through the host."""
+        return self.dist.get_backend(self.group) == "gloo"
 
     def shift_next(self, send_t, recv_t):
         """send_t to rank+1, recv_t from rank-1 (either may be None)."""
         if self.size == 1:
             return
         dist = self.dist
+        stage = self._host_staged()
+        s_t = send_t.cpu() if (stage and send_t is not None and send_t.is_cuda) else send_t
+        r_t = recv_t.cpu() if (stage and recv_t is not None and recv_t.is_cuda) else recv_t
         ops = []
-        if send_t is not None and self.rank + 1 < self.size:
-            ops.append(dist.P2POp(dist.isend, send_t, self._g(self.rank + 1), self.group))
-        if recv_t is not None and self.rank > 0:
-            ops.append(dist.P2POp(dist.irecv, recv_t, self._g(self.rank - 1), self.group))
+        if s_t is not None and self.rank + 1 < self.size:
+            ops.append(dist.P2POp(dist.isend, s_t, self._g(self.rank + 1), self.group))
+        if r_t is not None and self.rank > 0:
+            ops.append(dist.P2POp(dist.irecv, r_t, self._g(self.rank - 1), self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if r_t is not recv_t and recv_t is not None and self.rank > 0:
+            recv_t.copy_(r_t)
 
     def allgather(self, t, counts):
         """Concatenate every rank's 1D piece (sizes `counts`, same on all ranks)."""
@@ -117,11 +127,12 @@ class Comm:
         import torch
 
         m = max(counts)
-        pad = torch.zeros(m, dtype=t.dtype, device=t.device)
+        dev = "cpu" if self._host_staged() else t.device
+        pad = torch.zeros(m, dtype=t.dtype, device=dev)
         pad[: t.numel()] = t
         parts = [torch.empty_like(pad) for _ in range(self.size)]
         self.dist.all_gather(parts, pad, group=self.group)
-        return torch.cat([p[:c] for p, c in zip(parts, counts)])
+        return torch.cat([p[:c] for p, c in zip(parts, counts)]).to(t.device)
 
 
 # ---------------------------------------------------------------- engines
