@@ -80,9 +80,52 @@ __global__ void k_bspmv(int64_t nrows, const int64_t* __restrict__ rp,
     }
 }
 
+// The same products, kVB vectors per thread: a row's entries are read once per
+// vector group instead of once per vector (the transfers apply one small CSR to
+// W*M vectors), each vector's sum keeps the row's CSR order (bitwise k_bspmv).
+constexpr int kVB = 8;
+__global__ void k_bspmv_multi(int nrows, const int64_t* __restrict__ rp,
+                              const int32_t* __restrict__ ci, const double* __restrict__ val,
+                              const double* __restrict__ x, int64_t xs, double* y, int64_t ys,
+                              int nvec, int mode, const double* __restrict__ mh, const double* b,
+                              int64_t bs) {
+    const int v0 = blockIdx.y * kVB;
+    const int nv = min(kVB, nvec - v0);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows; i += gridDim.x * blockDim.x) {
+        double s[kVB];
+#pragma unroll
+        for (int v = 0; v < kVB; ++v) s[v] = 0.0;
+        const int64_t p1 = rp[i + 1];
+        for (int64_t p = rp[i]; p < p1; ++p) {
+            const double a = val[p];
+            const int col = ci[p];
+#pragma unroll
+            for (int v = 0; v < kVB; ++v)
+                if (v < nv) s[v] = add(s[v], mul(a, __ldg(x + (int64_t)(v0 + v) * xs + col)));
+        }
+#pragma unroll
+        for (int v = 0; v < kVB; ++v) {
+            if (v >= nv) break;
+            double* yv = y + (int64_t)(v0 + v) * ys + i;
+            if (mode == 0) *yv = s[v];
+            else if (mode == 1) *yv = (-s[v]) / mh[i];
+            else if (mode == 2) *yv = sub(b[(int64_t)(v0 + v) * bs + i], s[v]);
+            else *yv = add(*yv, s[v]);
+        }
+    }
+}
+
 void bspmv(Ctx& c, const Csr& A, const double* x, int64_t xs, double* y, int64_t ys, int nvec,
            int mode, const double* mh = nullptr, const double* b = nullptr, int64_t bs = 0) {
     if (nvec <= 0 || A.nrows <= 0) return;
+    if (nvec >= 4 && A.nrows < INT32_MAX) {
+        const int groups = (nvec + kVB - 1) / kVB;
+        const int gx = (int)std::max<int64_t>(
+            1, std::min<int64_t>((A.nrows + TB - 1) / TB, (int64_t)c.sms * 16 / groups + 1));
+        launch(k_bspmv_multi, dim3(gx, groups), TB, 0, c.stream, (int)A.nrows, A.rowptr.p,
+               A.col.p, A.val.p, x, xs, y, ys, nvec, mode, mh, b, bs);
+        return;
+    }
     launch(k_bspmv, c.grid_for(A.nrows * nvec, TB, 16), TB, 0, c.stream, A.nrows, A.rowptr.p,
            A.col.p, A.val.p, x, xs, y, ys, nvec, mode, mh, b, bs);
 }
@@ -441,22 +484,27 @@ __global__ void k_any_open(const int* done, int W, int* err) {
 }
 
 // collocation residual / C(u):  R = U - U0 - dt*Q*F - tau ;  C = U - dt*Q*F
+// a thread owns point s of worker w (blockIdx.y) and produces all M nodes from
+// one read of F[w][:][s] (same per-node arithmetic order as before)
 __global__ void k_coll(const double* U, const double* U0, const double* F, const double* tau,
                        double* out, int W, int M, int64_t S, double dt, Small Q, int with_u0) {
-    const int64_t tot = (int64_t)W * M * S;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = t % S, wm = t / S;
-        const int m = (int)(wm % M);
-        const int64_t w = wm / M;
-        const double* Fw = F + w * M * S + s;
-        double acc = 0.0;
-        for (int j = 0; j < M; ++j) acc = add(acc, mul(Q.a[m * M + j], Fw[j * S]));
-        double v = U[t];
-        if (with_u0) v = sub(v, U0[w * S + s]);
-        v = sub(v, mul(dt, acc));
-        if (tau) v = sub(v, tau[t]);
-        out[t] = v;
+    const int64_t w = blockIdx.y;
+    const double* Fw = F + w * M * S;
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < S;
+         s += (int64_t)gridDim.x * blockDim.x) {
+        double f[kMaxNodes];
+        for (int j = 0; j < M; ++j) f[j] = Fw[j * S + s];
+        const double u0 = with_u0 ? U0[w * S + s] : 0.0;
+        for (int m = 0; m < M; ++m) {
+            double acc = 0.0;
+            for (int j = 0; j < M; ++j) acc = add(acc, mul(Q.a[m * M + j], f[j]));
+            const int64_t t = (w * M + m) * S + s;
+            double v = U[t];
+            if (with_u0) v = sub(v, u0);
+            v = sub(v, mul(dt, acc));
+            if (tau) v = sub(v, tau[t]);
+            out[t] = v;
+        }
     }
 }
 
@@ -1133,8 +1181,10 @@ void sdc_coll(SdcLevelDev& L, const double* U, const double* U0, const double* t
     const int64_t n = (int64_t)W * M * S;
     feval(L, U, L.fi_old.p, L.fe_old.p, W, M, 0);
     launch(k_add_to, c.grid_for(n, TB), TB, 0, c.stream, L.f_tot.p, L.fi_old.p, L.fe_old.p, n);
-    launch(k_coll, c.grid_for(n, TB), TB, 0, c.stream, U, U0, L.f_tot.p, tau, out, W, M, S, L.dt,
-           L.Q, with_u0 ? 1 : 0);
+    const int gx = (int)std::max<int64_t>(
+        1, std::min<int64_t>((S + TB - 1) / TB, (int64_t)c.sms * 8 / std::max(W, 1) + 1));
+    launch(k_coll, dim3(gx, W), TB, 0, c.stream, U, U0, L.f_tot.p, tau, out, W, M, S, L.dt, L.Q,
+           with_u0 ? 1 : 0);
 }
 
 }  // namespace pd
