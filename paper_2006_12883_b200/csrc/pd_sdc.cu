@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(256) k_bstencil(int n, int gy, StTab tv, const
         off[k] = n; has[k++] = yi < n - 1;
         if (DIM == 3) { off[k] = n * n; has[k++] = zi < n - 1; }
     }
-    const double mj = mode == 1 ? mh[j] : 1.0;
+    const double mj = (mode == 1 || mode == 4) ? mh[j] : 1.0;
     for (int v = blockIdx.z; v < nvec; v += gridDim.z) {
         const double* xv = x + v * xs + j;
         double xk[NP];
@@ -174,6 +174,7 @@ __global__ void __launch_bounds__(256) k_bstencil(int n, int gy, StTab tv, const
         if (mode == 0) *yv = s;
         else if (mode == 1) *yv = (-s) / mj;
         else if (mode == 2) *yv = sub(b[v * bs + j], s);
+        else if (mode == 4) *yv = add((-s) / mj, 0.0);  // f_total with a zero reaction
         else *yv = add(*yv, s);
     }
 }
@@ -201,6 +202,17 @@ __global__ void k_freact(const double* U, double* out, int64_t n, double gamma, 
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         out[i] = gamma == 0.0 ? 0.0 : mul(-gamma, react(kind, U[i]));
+}
+
+// fe of one node for W workers: out[w * ostride + s] = -gamma r(x[w * S + s])
+__global__ void k_freact_node(const double* x, double* out, int W, int64_t S, int64_t ostride,
+                              double gamma, int kind) {
+    const int64_t n = (int64_t)W * S;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = i / S, s = i - w * S;
+        out[w * ostride + s] = gamma == 0.0 ? 0.0 : mul(-gamma, react(kind, x[i]));
+    }
 }
 
 // f = fi + fe  (f_total, pfasst.py:103-104)
@@ -1148,6 +1160,18 @@ void sdc_sweep(SdcLevelDev& L, double* U, const double* U0, const double* tau, i
         launch(k_scatter_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream, L.x.p, U, W, M, S,
                m);
         // f of the new node value (stored in the node-m slot of fi_new/fe_new)
+        if (L.kh_dim && (imex || L.gamma == 0.0)) {
+            // written straight into the node-m slots (worker stride M*S): no scratch
+            // vectors, no scatter passes
+            // implicit mode keeps f_total = f_diff + f_react in fi (f_react = +0 here:
+            // the +0.0 reproduces its rounding of -0)
+            bstencil(c, L.kh_dim, L.kh_n, L.kh_tv, L.x.p, S, L.fi_new.p + (int64_t)m * S,
+                     (int64_t)M * S, W, imex ? 1 : 4, L.mh.p, nullptr, 0);
+            launch(k_freact_node, c.grid_for((int64_t)W * S, TB), TB, 0, c.stream,
+                   (const double*)L.x.p, L.fe_new.p + (int64_t)m * S, W, S, (int64_t)M * S,
+                   L.gamma, L.kind);
+            continue;
+        }
         if (L.kh_dim)  // reuse fi_old as W x S scratch
             bstencil(c, L.kh_dim, L.kh_n, L.kh_tv, L.x.p, S, L.fi_old.p, S, W, 1, L.mh.p,
                      nullptr, 0);
