@@ -127,6 +127,7 @@ struct WfPlan {
         ng = 0, threads = 0, stages = 3;
     bool pad = false;     // entry lists zero-padded to the kernel's chunk
     bool gfirst = false;  // cross-task entries lead every pattern (no ring slots)
+    bool win = false;     // ... and are the previous step's 3x3 neighbourhood (register window)
     size_t smem = 0, stage_bytes = 0;
     DevBuf<int32_t> nsteps;
     DevBuf<int64_t> boff, bofs, q0;

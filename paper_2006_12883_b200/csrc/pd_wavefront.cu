@@ -71,7 +71,7 @@ struct WfDev {
     const unsigned char* blob;
     unsigned long long* trace;
     int64_t n;
-    int ntask, T, nline, npoint, R, pwo, maxS, npat, G, stages, gfirst;
+    int ntask, T, nline, npoint, R, pwo, maxS, npat, G, stages, gfirst, win;
     size_t stage_bytes;
 };
 
@@ -97,6 +97,7 @@ WfDev wf_dev(WfPlan& p) {
     d.G = p.T / p.nline;
     d.stages = p.stages;
     d.gfirst = p.gfirst ? 1 : 0;
+    d.win = p.win ? 1 : 0;
 
     d.stage_bytes = p.stage_bytes;
     return d;
@@ -222,7 +223,7 @@ __device__ __forceinline__ void sts_f64(unsigned a, double v) {
 // (A thread running the M node rows of its line measured slower on every C2
 // level: the per-step chain lengthens.)  Shared memory is addressed through
 // 32-bit shared-window offsets.
-template <bool UPPER, int NG, bool PAD>
+template <bool UPPER, int NG, bool PAD, bool WIN = false>
 __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
     k_wf_sweep(WfDev P, const double* __restrict__ b, double* y, unsigned long long* counter,
                const int* guard, int want) {
@@ -331,6 +332,37 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
         unsigned n_val = 0, n_stride = 0, n_dval = 0, n_pat = 0, n_ph = 0;
         int n_len = 0, n_ng = 0;
         double bn = 0.0, xn[NGA];
+        // WIN: sliding 3x3 window of the previous step's last node grid around
+        // (line, x): wv[dy+1][dx+1]; nc / nc0 = next column(s) loaded ahead
+        double wv[3][3], nc[3], nc0[3], cnc[3], cnc0[3];
+        const int Sg = P.nline * P.npoint;
+        const double* prevp = y + ((int64_t)qline - (int64_t)(g + 1) * Sg);  // (line, x=0)
+        auto wload = [&](int dy, int col) -> double {
+            const bool ok = lane && line + dy >= 0 && line + dy < P.nline && col >= 0 &&
+                            col < P.npoint;
+            return __longlong_as_double((long long)ld_weak_if(
+                ok, prevp + (int64_t)dy * P.npoint + (ok ? col : 0), (unsigned long long)kPending));
+        };
+        auto wresolve = [&](double v, int dy, int col) -> double {
+            unsigned long long u = (unsigned long long)__double_as_longlong(v);
+            if (u == kPending && line + dy >= 0 && line + dy < P.nline && col >= 0 &&
+                col < P.npoint) {
+                unsigned int ns = 32;
+                do {
+                    __nanosleep(ns);
+                    if (ns < 256) ns <<= 1;
+                    u = ld_strong_u64(prevp + (int64_t)dy * P.npoint + col);
+                } while (u == kPending);
+            }
+            return __longlong_as_double((long long)u);
+        };
+        if (WIN) {
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                nc[d] = nc0[d] = cnc[d] = cnc0[d] = 0.0;
+                wv[d][0] = wv[d][1] = wv[d][2] = 0.0;
+            }
+        }
         auto view = [&](unsigned blk, int q) {
             const int4 h = lds_v4s32(blk + 16u * (unsigned)g);  // lo, cnt, pid_off, val_off
             const int i = line - h.x;
@@ -355,6 +387,23 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
                 row = UPPER ? n - 1 - q : q;
             }
             const double* yrow = y + row;
+            if (WIN) {
+                if (act && n_ng > 0) {
+                    const int xq = q - qline;  // the next row's point on this line
+                    if (xq == 0) {
+#pragma unroll
+                        for (int d = 0; d < 3; ++d) {
+                            nc0[d] = wload(d - 1, 0);
+                            nc[d] = wload(d - 1, 1);
+                        }
+                    } else {
+#pragma unroll
+                        for (int d = 0; d < 3; ++d) nc[d] = wload(d - 1, xq + 1);
+                    }
+                }
+                bn = __ldg(b + row);
+                return;
+            }
 #pragma unroll
             for (int k = 0; k < NG; ++k) {
                 const bool pk = k < n_ng;
@@ -379,13 +428,48 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
             double xs[NGA];
 #pragma unroll
             for (int k = 0; k < NG; ++k) xs[k] = xn[k];
+            if (WIN) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    cnc[d] = nc[d];
+                    cnc0[d] = nc0[d];
+                }
+            }
             if (s + 1 < S) view(next_block(), qline + seq + (act ? 1 : 0));
             if (act) {
                 const int q = qline + seq;
                 const int row = UPPER ? n - 1 - q : q;
                 double acc = bb;
                 unsigned fa = val;
-                if (NG > 0 && ng > 0) {
+                if (WIN && ng > 0) {
+                    // slide the window to x = seq and fold the present 3x3 entries in
+                    // CSR order ((dy, dx) lexicographic = column order)
+                    const int xq = seq;
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        if (xq == 0) {
+                            wv[d][0] = 0.0;
+                            wv[d][1] = wresolve(cnc0[d], d - 1, 0);
+                        } else {
+                            wv[d][0] = wv[d][1];
+                            wv[d][1] = wv[d][2];
+                        }
+                        wv[d][2] = wresolve(cnc[d], d - 1, xq + 1);
+                    }
+                    int k = 0;
+#pragma unroll
+                    for (int d = 0; d < 3; ++d)
+#pragma unroll
+                        for (int e = 0; e < 3; ++e) {
+                            const bool pr = line + d - 1 >= 0 && line + d - 1 < P.nline &&
+                                            xq + e - 1 >= 0 && xq + e - 1 < P.npoint;
+                            if (pr) {
+                                acc = sub(acc, mul(lds_f64(fa + (unsigned)k * stride), wv[d][e]));
+                                ++k;
+                            }
+                        }
+                    fa += (unsigned)ng * stride;
+                } else if (NG > 0 && ng > 0) {
                     // cross-task values: resolve the (rare) pending ones by strong polls
                     unsigned long long u[NGA];
 #pragma unroll
@@ -504,6 +588,7 @@ struct HostPlan {
     std::vector<int16_t> offs;
     int R = 0, pwo = 0, ng = 0;
     bool gfirst = false;
+    bool win = false;  // cross-task entries are the previous step's 3x3 neighbourhood
     std::vector<unsigned char> blob;
     std::vector<int32_t> srow, sstride, scount;
     std::vector<int64_t> sval, sdiag;
@@ -626,6 +711,33 @@ bool build_plan(const std::vector<int64_t>& rp, const std::vector<int32_t>& ci,
         for (int e = pt[1]; e < pt[0]; ++e)
             if (pt[kPatHdr + 2 * e] == INT_MIN) gfirst = false;
     hp.gfirst = gfirst;
+    // Window eligibility (lower sweep, one time step per task, 2D grid): every
+    // polled row (g, y, x) reads exactly the present part of the 3x3 neighbourhood
+    // of (y, x) in the previous step's last node grid, in (dy, dx) order, i.e.
+    // global offsets -(g+1)*S + dy*npoint + dx.  The kernel then keeps a sliding
+    // 3x3 register window per thread (3 new values per row instead of 9 polls).
+    hp.win = false;
+    if (!upper && gfirst && NG == kNgWide && G * nline * npoint == TR && nline == npoint &&
+        !getenv("PD_WF_NO_WINDOW")) {
+        bool ok = true;
+        const int64_t S = nline * npoint;
+        for (int64_t q = 0; q < n && ok; ++q) {
+            const auto& pt = pats[pid[q]];
+            const int ngq = pt[1];
+            if (ngq == 0) continue;
+            const int64_t o = q % TR, th = o / npoint, x = o % npoint;
+            const int64_t gg = th / nline, yl = th % nline;
+            int k = 0;
+            for (int dy = -1; dy <= 1 && ok; ++dy)
+                for (int dx = -1; dx <= 1 && ok; ++dx) {
+                    if (yl + dy < 0 || yl + dy >= nline || x + dx < 0 || x + dx >= npoint) continue;
+                    if (k >= ngq || pt[2 + k] != -(gg + 1) * S + dy * npoint + dx) ok = false;
+                    ++k;
+                }
+            if (k != ngq) ok = false;
+        }
+        hp.win = ok;
+    }
     const int64_t RW = R + (gfirst ? 0 : NG);
     int maxlen = 1;
     for (auto& pt : pats) maxlen = std::max(maxlen, pt[0] - (gfirst ? pt[1] : 0));
@@ -760,6 +872,9 @@ bool configure_launch_pad(Ctx& c, WfPlan& p) {
     if (smem > attr_max) {
         PD_CUDA(cudaFuncSetAttribute(k_wf_sweep<UPPER, NG, PAD>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (!UPPER && NG == kNgWide)
+            PD_CUDA(cudaFuncSetAttribute(k_wf_sweep<false, kNgWide, PAD, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_max = smem;
     }
     int per_sm = 0;
@@ -789,6 +904,7 @@ void upload(WfPlan& p, HostPlan& hp, int64_t n, int G, int64_t nline, int64_t np
     p.ng = hp.ng;
     p.npat = (int)(hp.pattern.size() / (2 + hp.ng));
     p.gfirst = hp.gfirst;
+    p.win = hp.win;
     // tables are bulk-copied into shared memory: 16-byte multiples
     hp.pattern.resize(align_up(hp.pattern.size() * 4, 16) / 4, 0);
     hp.offs.resize(align_up(hp.offs.size() * 2, 16) / 2, 0);
@@ -932,6 +1048,15 @@ static void wf_trace_report(Ctx& c, WfPlan& p, const char* name) {
 template <bool UPPER, int NG>
 static void launch_sweep_ng(Ctx& c, WfPlan& p, const double* b, double* y,
                             unsigned long long* ctr, const int* guard, int want) {
+    if (!UPPER && NG == kNgWide && p.win) {
+        if (p.pad)
+            launch(k_wf_sweep<false, kNgWide, true, true>, p.blocks, p.threads, p.smem, c.stream,
+                   wf_dev(p), b, y, ctr, guard, want);
+        else
+            launch(k_wf_sweep<false, kNgWide, false, true>, p.blocks, p.threads, p.smem,
+                   c.stream, wf_dev(p), b, y, ctr, guard, want);
+        return;
+    }
     if (p.pad)
         launch(k_wf_sweep<UPPER, NG, true>, p.blocks, p.threads, p.smem, c.stream, wf_dev(p), b,
                y, ctr, guard, want);
