@@ -202,6 +202,11 @@ __device__ __forceinline__ int4 lds_v4s32(unsigned a) {
                  : "r"(a));
     return v;
 }
+__device__ __forceinline__ uint2 lds_v2u32(unsigned a) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+    return v;
+}
 __device__ __forceinline__ void lds_v4s16(unsigned a, int& o0, int& o1, int& o2, int& o3) {
     short x0, x1, x2, x3;
     asm volatile("ld.shared.v4.s16 {%0, %1, %2, %3}, [%4];"
@@ -511,11 +516,15 @@ __global__ void __launch_bounds__(NG <= kNgFine ? 768 : 512, 1)
                 }
                 const unsigned orow = pat + phase_b;
                 // PAD: len is padded to kChunk with zero entries, no per-entry predicates
+                // each chunk's offsets are loaded one chunk ahead: the ring loads of a
+                // chunk then wait on nothing but their own issue
+                uint2 onext = lds_v2u32(orow);
 #pragma unroll 1
                 for (int k0 = 0; k0 < len; k0 += kChunk) {
-                    int o0, o1, o2, o3;
-                    lds_v4s16(orow + 2u * (unsigned)k0, o0, o1, o2, o3);
-                    const int oi[kChunk] = {o0, o1, o2, o3};
+                    const uint2 oc = onext;
+                    if (k0 + kChunk < len) onext = lds_v2u32(orow + 2u * (unsigned)(k0 + kChunk));
+                    const int oi[kChunk] = {(int)(short)(oc.x & 0xffffu), (int)oc.x >> 16,
+                                            (int)(short)(oc.y & 0xffffu), (int)oc.y >> 16};
                     double v[kChunk], f[kChunk];
 #pragma unroll
                     for (int k = 0; k < kChunk; ++k)
