@@ -285,12 +285,17 @@ def run_b200(args):
         xh, rep_e = e2e_solve(b_pin, x_pin)
         torch.cuda.synchronize()
         e2e_times.append(time.perf_counter() - t0)
-    # the numpy drop-in path (pageable host arrays) for reference
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    # the numpy drop-in path (pageable numpy arrays in and out; large vectors are
+    # staged through reusable pinned buffers, set up by one untimed call)
     e2e_solve(b_host)
-    torch.cuda.synchronize()
-    t_e2e_numpy = time.perf_counter() - t0
+    np_times = []
+    for _ in range(max(1, min(args.steps, 3))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_solve(b_host)
+        torch.cuda.synchronize()
+        np_times.append(time.perf_counter() - t0)
+    t_e2e_numpy = sum(np_times) / len(np_times)
     t_e2e = float(np.mean(e2e_times))
     if dist:
         tt = torch.tensor([t_e2e], device=red_dev)

@@ -213,6 +213,99 @@ def ptr(t) -> _vp:
     return _vp(t.data_ptr()) if t is not None else _vp()
 
 
+# Large numpy vectors (a C2 space-time vector is 100 MB) cross the host/device
+# boundary through a reusable pinned staging buffer in chunks: host threads copy
+# chunk i between numpy and pinned memory while the DMA of its neighbours runs.
+# A pageable torch copy runs at a few GB/s; the staged copy runs near the
+# link's rate.  PD_STAGED_IO=0 turns it off.
+_STAGE_MIN_BYTES = 1 << 23
+_STAGE_CHUNK = 1 << 20  # doubles per chunk (8 MB)
+_stage_lock = threading.Lock()
+_stage_bufs: dict = {}  # (device index, direction) -> [pinned tensor, pending event or None]
+_stage_pool = None
+
+
+def _staging_enabled(nbytes: int) -> bool:
+    return nbytes >= _STAGE_MIN_BYTES and os.environ.get("PD_STAGED_IO", "1") != "0"
+
+
+def _pool():
+    global _stage_pool
+    if _stage_pool is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        _stage_pool = ThreadPoolExecutor(max_workers=max(1, min(8, os.cpu_count() or 1)),
+                                         thread_name_prefix="pd-stage")
+    return _stage_pool
+
+
+def _staging(ctx, direction: str, n: int):
+    """The pinned buffer for (device, direction), at least n doubles; waits for
+    the DMA that last used it."""
+    torch = torch_mod()
+    key = (ctx.device, direction)
+    ent = _stage_bufs.get(key)
+    if ent is None or ent[0].numel() < n:
+        if ent is not None and ent[1] is not None:
+            ent[1].synchronize()
+        ent = [torch.empty(n, dtype=torch.float64, pin_memory=True), None]
+        _stage_bufs[key] = ent
+    elif ent[1] is not None:
+        ent[1].synchronize()
+        ent[1] = None
+    return ent
+
+
+def _chunks(n: int):
+    return [(lo, min(n, lo + _STAGE_CHUNK)) for lo in range(0, n, _STAGE_CHUNK)]
+
+
+def _h2d_staged(a: np.ndarray, ctx):
+    torch = torch_mod()
+    n = a.size
+    out = torch.empty(n, dtype=torch.float64, device=ctx.torch_device)
+    with _stage_lock:
+        ent = _staging(ctx, "h2d", n)
+        buf = ent[0]
+        host = buf.numpy()
+        parts = _chunks(n)
+        futs = [_pool().submit(np.copyto, host[lo:hi], a[lo:hi]) for lo, hi in parts]
+        for f, (lo, hi) in zip(futs, parts):
+            f.result()
+            out[lo:hi].copy_(buf[lo:hi], non_blocking=True)
+        # complete on return, like a pageable copy: the caller may hand `out` to
+        # work on any stream
+        torch.cuda.current_stream(out.device).synchronize()
+    return out
+
+
+def _d2h_staged(t) -> np.ndarray:
+    torch = torch_mod()
+    n = t.numel()
+    res = np.empty(n, dtype=np.float64)
+    src = t.reshape(-1)
+    with _stage_lock, torch.cuda.device(t.device):
+        ent = _staging(context(t.device.index), "d2h", n)
+        buf = ent[0]
+        host = buf.numpy()
+        parts = _chunks(n)
+        evs = []
+        for lo, hi in parts:
+            buf[lo:hi].copy_(src[lo:hi], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            evs.append(ev)
+
+        def drain(i):
+            lo, hi = parts[i]
+            evs[i].synchronize()
+            np.copyto(res[lo:hi], host[lo:hi])
+
+        for f in [_pool().submit(drain, i) for i in range(len(parts))]:
+            f.result()
+    return res.reshape(tuple(t.shape))
+
+
 def to_device(x, ctx: Context | None = None):
     """numpy / torch -> contiguous float64 CUDA tensor on the context's device."""
     torch = torch_mod()
@@ -221,7 +314,17 @@ def to_device(x, ctx: Context | None = None):
         t = x.to(device=ctx.torch_device, dtype=torch.float64)
         return t.contiguous()
     a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+    if a.ndim == 1 and _staging_enabled(a.nbytes):
+        return _h2d_staged(a, ctx)
     return torch.from_numpy(a).to(ctx.torch_device)
+
+
+def to_host(t) -> np.ndarray:
+    """CUDA tensor -> numpy (staged through pinned memory when large)."""
+    if t.is_cuda and t.dtype == torch_mod().float64 and t.is_contiguous() and \
+            _staging_enabled(t.numel() * 8):
+        return _d2h_staged(t)
+    return t.cpu().numpy()
 
 
 def empty(n: int, ctx: Context | None = None):
@@ -265,4 +368,4 @@ def like_input(result, template, out=None):
         return out
     if is_tensor(template):
         return result if template.is_cuda else result.cpu()
-    return result.cpu().numpy()
+    return to_host(result)
