@@ -146,6 +146,7 @@ static void gspmv_gather(Ctx& c, const Csr& A, GridSpmv& g) {
 }
 
 bool csr_attach_grid(Ctx& c, Csr& A, int64_t nt, int M, int64_t n) {
+    ++c.epoch;
     A.grid.reset();
     A.grid_stale = false;
     if (getenv("PD_NO_GRID_SPMV") || M < 1 || M > 5 || n < 3 || nt < 1) return false;

@@ -91,6 +91,9 @@ struct Ctx {
     DevBuf<double> scalars;           // small result slots
     DevBuf<int> flags;                // misc device flags
     void* blas = nullptr;             // cuBLAS handle (plain DGEMMs only), lazily created
+    // bumped by every call that changes device state a captured CUDA graph
+    // would bake in (values, factors, plans): captured V-cycles are re-made
+    uint64_t epoch = 0;
     explicit Ctx(int dev, cudaStream_t s);
     ~Ctx();
     Ctx(const Ctx&) = delete;

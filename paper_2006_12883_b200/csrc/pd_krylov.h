@@ -85,6 +85,9 @@ class Multigrid {
     Multigrid(Ctx& c, std::vector<std::unique_ptr<Csr>> mats, std::vector<std::unique_ptr<Csr>> R,
               std::vector<std::unique_ptr<Csr>> P, int nu, int partitions, int restart,
               int smooth_solves);
+    ~Multigrid();
+    Multigrid(const Multigrid&) = delete;
+    Multigrid& operator=(const Multigrid&) = delete;
     // replace level matrix values (same patterns) and refactor (Newton refresh)
     void refactor();
     // device Galerkin: T_l = R_l A_l (scipy's stored order), A_{l+1} = T_l P_l
@@ -110,6 +113,24 @@ class Multigrid {
 
    private:
     void cycle(int l);
+    // one V-cycle: eager launches, or the captured CUDA graph of the same launch
+    // sequence when this (b, x, state epoch) was already solved once
+    void run_vcycle(const double* b, double* x, bool use_graph);
+    struct VGraph {
+        const double* b = nullptr;
+        double* x = nullptr;
+        uint64_t epoch = ~0ull;
+        cudaGraphExec_t exec = nullptr;
+    };
+    VGraph vgraph, vseen;
+    bool graph_off = false;
+    cudaStream_t cap_stream = nullptr;
+    // per-cycle status (|r|^2, non-finite flag, every level's GMRES error code)
+    // gathered on the device and read back with one copy into pinned memory
+    static constexpr int kStatusMax = 2 + 32;
+    DevBuf<double> status_dev;
+    double* status_host = nullptr;
+    const double* read_status(bool with_errors);
     const double* fine_r_norm2 = nullptr;  // set by solve(): lv[0].r already = b - A x
     Ctx& c;
     std::vector<MgLevel> lv;

@@ -253,6 +253,7 @@ std::unique_ptr<Csr> csr_upload(Ctx& c, int64_t nrows, int64_t ncols, int64_t nn
 }
 
 void csr_update_values(Ctx& c, Csr& A, const double* val, bool device_src) {
+    ++c.epoch;
     if (!A.nnz) return;
     PD_CUDA(cudaMemcpyAsync(A.val.p, val, A.nnz * sizeof(double),
                             device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
@@ -696,6 +697,7 @@ static void build_task_layout(Ctx& c, Ilu0& f) {
 }
 
 void ilu0_refactor(Ctx& c, Ilu0& f) {
+    ++c.epoch;
     const Csr& P = f.pat();
     const int64_t n = f.n;
     if (n == 0) return;
@@ -1001,6 +1003,7 @@ __global__ void k_spgemm_values(int64_t nrows, const int64_t* __restrict__ arp,
 }
 
 void spgemm_values(Ctx& c, const Csr& A, const Csr& B, Csr& C) {
+    ++c.epoch;
     if (A.nrows != C.nrows || A.ncols != B.nrows || B.ncols != C.ncols)
         throw ConfigError("fixed-pattern SpGEMM shape mismatch");
     if (C.nrows == 0) return;

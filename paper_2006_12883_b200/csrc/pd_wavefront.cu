@@ -949,6 +949,7 @@ bool wavefront_disabled() {
 
 bool ilu0_set_wavefront(Ctx& c, Ilu0& f, int64_t ngroup, int64_t nline, int64_t npoint,
                         int64_t ngroup_lower) {
+    ++c.epoch;
     f.wf_lo.reset();
     f.wf_up.reset();
     if (wavefront_disabled() || f.n == 0) return false;

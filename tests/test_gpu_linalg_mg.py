@@ -209,3 +209,49 @@ def test_sharded_mg_device_engine_one_rank_matches_serial():
     x2 = x2.cpu().numpy()
     assert r1.converged and r2.converged and r1.iterations == r2.iterations
     assert np.linalg.norm(x2 - x1) <= 1e-10 * np.linalg.norm(x1)
+
+
+def test_repeated_solves_replay_captured_cycle_bitwise(golden, monkeypatch):
+    """A second solve of the same state and vectors replays the V-cycle as a
+    captured CUDA graph: results must be bitwise the eager ones, for new
+    right-hand sides in the same buffers and after the values change."""
+    g = golden("c2_small")
+    spec = pd.StencilSpec(2, 15, "dirichlet", 1.0)
+    system = pd.assemble_system(pd.make_tableau(3), pd.fd_space(spec), pd.TimeGrid(8, 8 / 64),
+                                0.0, g["u0"])
+    h = pd.build_hierarchy(system, "SMG", 3, 3, partitions=4)
+    N = pd._native
+    b = N.to_device(system.rhs())
+    x = N.zeros(b.numel())
+
+    def run(bv):
+        b.copy_(N.to_device(bv))
+        x.zero_()
+        _, rep = h.solve_dev(b, x, 1e-10, 1e-10)
+        return x.cpu().numpy().copy(), rep.iterations
+
+    rhs = system.rhs()
+    ref, its = run(rhs)  # eager (first sighting)
+    for _ in range(3):  # capture, then replays
+        got, its2 = run(rhs)
+        np.testing.assert_array_equal(got, ref)
+        assert its2 == its
+    rhs2 = np.sin(np.arange(rhs.size)) * 1e-3 + rhs
+    got2, _ = run(rhs2)
+    monkeypatch.setenv("PD_MG_NO_GRAPH", "1")
+    eager2, _ = run(rhs2)
+    np.testing.assert_array_equal(got2, eager2)
+    monkeypatch.delenv("PD_MG_NO_GRAPH")
+    # new values (Newton refresh): the captured cycle must not be reused stale
+    A2 = system.global_matrix() * 1.5
+    h.set_fine_matrix(A2)
+    new1, _ = run(rhs)
+    new2, _ = run(rhs)
+    monkeypatch.setenv("PD_MG_NO_GRAPH", "1")
+    h_eager = pd.build_hierarchy(system, "SMG", 3, 3, partitions=4)
+    h_eager.set_fine_matrix(A2)
+    b2 = N.to_device(rhs)
+    x2 = N.zeros(b2.numel())
+    h_eager.solve_dev(b2, x2, 1e-10, 1e-10)
+    np.testing.assert_array_equal(new1, x2.cpu().numpy())
+    np.testing.assert_array_equal(new2, new1)
