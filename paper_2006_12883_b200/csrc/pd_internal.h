@@ -49,6 +49,18 @@ inline void launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     k<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
 }
 
+// Kernels launched while a stream is being captured do not run then: capture
+// takes them back off the counter and every replay of the graph adds them.
+inline uint64_t uncount_captured(unsigned long long before) {
+    const unsigned long long k = g_launches.load() - before;
+    g_launches.fetch_sub(k, std::memory_order_relaxed);
+    return k;
+}
+inline void graph_launch(cudaGraphExec_t exec, uint64_t kernels, cudaStream_t st) {
+    g_launches.fetch_add(kernels, std::memory_order_relaxed);
+    PD_CUDA(cudaGraphLaunch(exec, st));
+}
+
 // Owning device allocation (cudaMalloc/cudaFree; allocation happens at
 // plan/setup time only, never inside a solve).
 template <class T>

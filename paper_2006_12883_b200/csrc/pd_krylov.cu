@@ -573,20 +573,23 @@ void Multigrid::run_vcycle(const double* b, double* x, bool use_graph) {
         cudaGraph_t graph = nullptr;
         c.stream = cap_stream;
         PD_CUDA(cudaStreamBeginCapture(cap_stream, cudaStreamCaptureModeRelaxed));
+        const unsigned long long l0 = g_launches.load();
         try {
             enqueue_vcycle(b, x);
         } catch (...) {
             cudaStreamEndCapture(cap_stream, &graph);
             if (graph) cudaGraphDestroy(graph);
             c.stream = orig;
+            uncount_captured(l0);
             throw;
         }
         const cudaError_t ce = cudaStreamEndCapture(cap_stream, &graph);
+        const uint64_t nk = uncount_captured(l0);
         c.stream = orig;
         cudaGraphExec_t exec = nullptr;
         if (ce == cudaSuccess && graph && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
             if (vgraph.exec) cudaGraphExecDestroy(vgraph.exec);
-            vgraph = VGraph{b, x, c.epoch, exec};
+            vgraph = VGraph{b, x, c.epoch, exec, nk};
         } else {  // something in the cycle is not capturable: stay eager
             (void)cudaGetLastError();
             graph_off = true;
@@ -597,7 +600,7 @@ void Multigrid::run_vcycle(const double* b, double* x, bool use_graph) {
             return;
         }
     }
-    PD_CUDA(cudaGraphLaunch(vgraph.exec, c.stream));
+    graph_launch(vgraph.exec, vgraph.kernels, c.stream);
 }
 
 void Multigrid::enqueue_vcycle(const double* b, double* x) {

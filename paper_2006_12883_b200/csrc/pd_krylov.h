@@ -121,6 +121,7 @@ class Multigrid {
         double* x = nullptr;
         uint64_t epoch = ~0ull;
         cudaGraphExec_t exec = nullptr;
+        uint64_t kernels = 0;  // this library's kernels in one replay
     };
     VGraph vgraph, vseen;
     bool graph_off = false;

@@ -341,6 +341,7 @@ struct SdcLevelDev {
         const void *U, *U0, *tau, *u0c;
         int W, nu;
         cudaGraphExec_t exec;
+        uint64_t kernels;  // this library's kernels in one replay
     };
     std::vector<ChainGraph> chain_graphs;  // captured serial coarse chains (pd_sdc_chain)
     cudaStream_t capture_stream = nullptr;
@@ -1424,7 +1425,7 @@ int pd_sdc_chain(void* lvl, double* U, double* U0, const double* tau, int W, con
         }
         for (auto& g : L.chain_graphs)
             if (g.U == U && g.U0 == U0 && g.tau == tau && g.u0c == u0c && g.W == W && g.nu == nu) {
-                PD_CUDA(cudaGraphLaunch(g.exec, c.stream));
+                pd::graph_launch(g.exec, g.kernels, c.stream);
                 return;
             }
         // capture on a private stream (the context's stream may be the legacy
@@ -1441,18 +1442,21 @@ int pd_sdc_chain(void* lvl, double* U, double* U0, const double* tau, int W, con
             if (c.blas) cublasSetStream(static_cast<cublasHandle_t>(c.blas), orig);
         };
         PD_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));
+        const unsigned long long l0 = pd::g_launches.load();
         try {
             chain();
         } catch (...) {
             cudaStreamEndCapture(c.stream, &graph);
             if (graph) cudaGraphDestroy(graph);
             restore();
+            pd::uncount_captured(l0);
             throw;
         }
         const cudaError_t ce = cudaStreamEndCapture(c.stream, &graph);
+        const uint64_t nk = pd::uncount_captured(l0);
         restore();
         PD_CUDA(ce);
-        pd::SdcLevelDev::ChainGraph g{U, U0, tau, u0c, W, nu, nullptr};
+        pd::SdcLevelDev::ChainGraph g{U, U0, tau, u0c, W, nu, nullptr, nk};
         PD_CUDA(cudaGraphInstantiate(&g.exec, graph, 0));
         cudaGraphDestroy(graph);
         if (L.chain_graphs.size() >= 4) {
@@ -1460,7 +1464,7 @@ int pd_sdc_chain(void* lvl, double* U, double* U0, const double* tau, int W, con
             L.chain_graphs.erase(L.chain_graphs.begin());
         }
         L.chain_graphs.push_back(g);
-        PD_CUDA(cudaGraphLaunch(g.exec, c.stream));
+        pd::graph_launch(g.exec, g.kernels, c.stream);
     });
 }
 

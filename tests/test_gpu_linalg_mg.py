@@ -230,12 +230,18 @@ def test_repeated_solves_replay_captured_cycle_bitwise(golden, monkeypatch):
         _, rep = h.solve_dev(b, x, 1e-10, 1e-10)
         return x.cpu().numpy().copy(), rep.iterations
 
+    lib = N.load_library()
     rhs = system.rhs()
+    l0 = lib.pd_launch_count()
     ref, its = run(rhs)  # eager (first sighting)
+    eager_launches = lib.pd_launch_count() - l0
     for _ in range(3):  # capture, then replays
+        l0 = lib.pd_launch_count()
         got, its2 = run(rhs)
         np.testing.assert_array_equal(got, ref)
         assert its2 == its
+        # a replay counts the kernels of its graph, not one launch
+        assert lib.pd_launch_count() - l0 == eager_launches
     rhs2 = np.sin(np.arange(rhs.size)) * 1e-3 + rhs
     got2, _ = run(rhs2)
     monkeypatch.setenv("PD_MG_NO_GRAPH", "1")
