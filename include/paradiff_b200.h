@@ -170,6 +170,22 @@ int pd_sub(void *ctx, double *out, const double *a, const double *b, int64_t n);
 int pd_spread(void *ctx, const double *u0, double *U, double *U0, int W, int M, int64_t S);
 int pd_terminal(void *ctx, const double *U, double *out, int W, int M, int64_t S);
 
+/* ---- P-fast: matrix-free block-Jacobi-in-time smoother with inner spatial
+ *      V-cycles on structured grids (SURVEY §7.1 P-fast profile; no reference
+ *      counterpart — the outer loop follows multigrid.py:243-305, the time
+ *      blocks linalg.py:152-189 with one block per step, the operator
+ *      spacetime.py:77-80,117-124 with Kh = kappa h^{d-2}(-Lap stencil),
+ *      Mh = h^d I).  Parity: oracle/pfast_oracle.py.  Vectors (nt, M, n^d). -- */
+int pd_pfast_create(void *ctx, int dim, int64_t n, int bc_periodic, double kappa, int M,
+                    int64_t nt, double dt, const double *Kq, const double *Mq, const double *l0,
+                    int levels, int nu, int coarse_sweeps, double omega_s, double omega_t,
+                    void **plan_out); /* Kq, Mq (M x M row-major), l0 (M): host */
+int pd_pfast_residual(void *plan, const double *x, const double *b, double *r, double *norm2_dev);
+int pd_pfast_sweep(void *plan, const double *b, double *x);
+int pd_pfast_solve(void *plan, const double *b, double *x, double tol_rel, double tol_abs,
+                   int max_sweeps, pd_solve_report *report, double *hist /* host, optional */);
+int pd_pfast_destroy(void *plan);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,12 @@ _SIGNATURES = {
     "pd_mg_solve": (_int, [_vp, _vp, _vp, _vp, _dbl, _dbl, _int, ctypes.POINTER(SolveReportC),
                            _vp, _int]),
     "pd_mg_destroy": (_int, [_vp]),
+    "pd_pfast_create": (_int, [_vp, _int, _i64, _int, _dbl, _int, _i64, _dbl, _vp, _vp, _vp,
+                               _int, _int, _int, _dbl, _dbl, ctypes.POINTER(_vp)]),
+    "pd_pfast_residual": (_int, [_vp, _vp, _vp, _vp, _vp]),
+    "pd_pfast_sweep": (_int, [_vp, _vp, _vp]),
+    "pd_pfast_solve": (_int, [_vp, _vp, _vp, _dbl, _dbl, _int, ctypes.POINTER(SolveReportC), _vp]),
+    "pd_pfast_destroy": (_int, [_vp]),
     "pd_mg_set_fine_operator": (_int, [_vp, _vp]),
     "pd_mg_set_galerkin_intermediates": (_int, [_vp, _int, _vp]),
     "pd_mg_set_fine_values": (_int, [_vp, _vp]),
