@@ -335,6 +335,9 @@ def run_b200(args):
     pfasst = None
     if rank == 0 and not args.no_pfasst:
         pfasst = pfasst_c4_window()
+    pfast = None
+    if rank == 0 and not args.no_pfast:
+        pfast = pfast_c5(peak)
 
     if rank == 0:
         cpu = None
@@ -367,6 +370,7 @@ def run_b200(args):
                          "peak_kind": peak_kind},
             "cpu_baseline": cpu,
             "pfasst_c4": pfasst,
+            "pfast_c5": pfast,
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -406,6 +410,63 @@ def pfasst_c4_window(P: int = 32):
         return {"error": f"{type(e).__name__}: {e}"}
 
 
+def pfast_c5(peak: float, sweeps: int = 5):
+    """Secondary line item: the P-fast matrix-free smoother (pd_pfast.cu) on
+    BASELINE config 5's grid at full per-GPU size: 256^3 periodic (the even
+    variant SURVEY §8 allows for 255^3), coef 0.1, M=3, 32 steps, dt=1e-3 —
+    1.61 G space-time dofs.  Linear operator only (the cubic reaction's Newton
+    linearisation is not wired into P-fast).  value = dofs / (device time of
+    one outer sweep), CUDA events around `sweeps` sweeps after 2 warm-up
+    sweeps; alg_bytes_per_sweep counts every kernel of the sweep (DESIGN §4);
+    then a solve to |r| <= 1e-8 |r0|."""
+    import torch
+
+    try:
+        from paper_2006_12883_b200.pfast import PfastSolver
+        from paper_2006_12883_b200.problems import StencilSpec
+
+        import gc
+
+        gc.collect()
+        torch.cuda.empty_cache()
+        spec, M, Nt = StencilSpec(3, 256, "periodic", 0.1), 3, 32
+        s = PfastSolver(spec, M, Nt, 1e-3)
+        g = torch.Generator(device="cuda").manual_seed(0)
+        b = torch.rand(s.n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+        x = torch.zeros(s.n, dtype=torch.float64, device="cuda")
+        for _ in range(2):
+            s.sweep(b, x)
+        st = torch.cuda.current_stream()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(st)
+        for _ in range(sweeps):
+            s.sweep(b, x)
+        e1.record(st)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3 / sweeps
+        # algorithmic bytes of one sweep: level l has n_l = nt*M*S_l dofs
+        nl = [s.n // (8 ** l) for l in range(s.levels)]
+        by = 24 * nl[0] + 24 * nl[0]  # space-time residual + x update
+        for l in range(s.levels - 1):
+            by += 16 * nl[l] + 24 * (s.nu - 1) * nl[l] + 24 * nl[l]  # pre-smooth, residual
+            by += 8 * nl[l] + 8 * nl[l + 1] + 16 * nl[l] + 8 * nl[l + 1]  # restrict, prolong
+            by += 24 * s.nu * nl[l]  # post-smooth
+        by += 16 * nl[-1] + 24 * (s.coarse_sweeps - 1) * nl[-1]
+        xs, rep = s.solve(b, tol_rel=1e-8, max_sweeps=200)
+        torch.cuda.synchronize()
+        return {"workload": "C5 grid 256^3 periodic, coef 0.1, M=3, Nt=32, dt=1e-3 (linear "
+                            f"part), P-fast: block-Jacobi in time, {s.levels}-level spatial "
+                            f"V({s.nu},{s.nu}) point-block Jacobi w=0.8, {s.coarse_sweeps} "
+                            "coarsest sweeps", "dofs": s.n, "ms_per_sweep": t * 1e3,
+                "value": s.n / t / 1e9, "unit": "GDOF/s per outer smoother sweep",
+                "alg_bytes_per_sweep": by, "achieved_gbs": by / t / 1e9,
+                "frac_of_peak": by / t / 1e9 / peak,
+                "solve_to_1e-8": {"sweeps": rep.iterations, "converged": rep.converged}}
+    except Exception as e:  # informational item: never take the headline line down
+        return {"error": f"{type(e).__name__}: {e}"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -415,6 +476,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pfasst", action="store_true",
                     help="skip the secondary PFASST C4 window measurement")
+    ap.add_argument("--no-pfast", action="store_true",
+                    help="skip the secondary P-fast C5 smoother measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -56,12 +56,22 @@ template <int DIM, int M, int MODE, bool PER>
 __global__ void __launch_bounds__(PFB) k_pf_point(PfCoef C, int n, int64_t nt,
                                                  const double* __restrict__ x,
                                                  const double* __restrict__ b, double* out) {
-    const int64_t S = DIM == 2 ? (int64_t)n * n : (int64_t)n * n * n;
-    const int64_t total = nt * S;
-    for (int64_t g = blockIdx.x * (int64_t)PFB + threadIdx.x; g < total;
-         g += (int64_t)gridDim.x * PFB) {
-        const int64_t t = g / S;
-        const int64_t j = g - t * S;
+    // one warp per (step, grid row, 32-point x tile): 32-bit index math only
+    const unsigned nn = (unsigned)n;
+    const unsigned R = DIM == 2 ? nn : nn * nn;  // rows per step
+    const unsigned xt = (nn + 31u) / 32u;
+    const unsigned items = (unsigned)nt * R * xt;  // < 2^31 (checked at plan time)
+    const int64_t S = (int64_t)R * nn;
+    const unsigned lane = threadIdx.x & 31u;
+    for (unsigned w = blockIdx.x * (PFB / 32) + (threadIdx.x >> 5); w < items;
+         w += gridDim.x * (PFB / 32)) {
+        const unsigned row = w / xt;
+        const unsigned ix_u = (w - row * xt) * 32u + lane;
+        if (ix_u >= nn) continue;
+        const unsigned t_u = row / R;
+        const unsigned rr = row - t_u * R;
+        const int64_t t = t_u;
+        const int64_t j = (int64_t)rr * nn + ix_u;
         const int64_t base = t * M * S + j;
         double bv[M];
 #pragma unroll
@@ -76,9 +86,9 @@ __global__ void __launch_bounds__(PFB) k_pf_point(PfCoef C, int n, int64_t nt,
             }
             continue;
         }
-        const int ix = (int)(j % n);
-        const int iy = (int)((j / n) % n);
-        const int iz = DIM == 3 ? (int)(j / ((int64_t)n * n)) : 0;
+        const int ix = (int)ix_u;
+        const int iy = DIM == 2 ? (int)rr : (int)(rr % nn);
+        const int iz = DIM == 3 ? (int)(rr / nn) : 0;
         // neighbour offsets (relative to j); 0 marks "outside" for Dirichlet
         int64_t off[2 * DIM];
         bool ok[2 * DIM];
@@ -152,30 +162,43 @@ __global__ void __launch_bounds__(PFB) k_pf_restrict(int nc, int nf, int64_t pla
     const int64_t Sc = DIM == 2 ? (int64_t)nc * nc : (int64_t)nc * nc * nc;
     const int64_t Sf = DIM == 2 ? (int64_t)nf * nf : (int64_t)nf * nf * nf;
     const double w[3] = {0.5, 1.0, 0.5};
-    for (int64_t g = blockIdx.x * (int64_t)PFB + threadIdx.x; g < planes * Sc;
-         g += (int64_t)gridDim.x * PFB) {
-        const int64_t p = g / Sc;
-        const int64_t j = g - p * Sc;
-        const int cx = (int)(j % nc), cy = (int)((j / nc) % nc);
-        const int cz = DIM == 3 ? (int)(j / ((int64_t)nc * nc)) : 0;
+    const unsigned R = DIM == 2 ? (unsigned)nc : (unsigned)nc * nc;  // coarse rows per plane
+    const unsigned xt = ((unsigned)nc + 31u) / 32u;
+    const unsigned items = (unsigned)planes * R * xt;
+    const unsigned lane = threadIdx.x & 31u;
+    for (unsigned wi = blockIdx.x * (PFB / 32) + (threadIdx.x >> 5); wi < items;
+         wi += gridDim.x * (PFB / 32)) {
+        const unsigned row = wi / xt;
+        const unsigned cx_u = (wi - row * xt) * 32u + lane;
+        if (cx_u >= (unsigned)nc) continue;
+        const unsigned p_u = row / R;
+        const unsigned rr = row - p_u * R;
+        const int64_t p = p_u;
+        const int64_t g = p * Sc + (int64_t)rr * nc + cx_u;
+        const int cx = (int)cx_u;
+        const int cy = DIM == 2 ? (int)rr : (int)(rr % (unsigned)nc);
+        const int cz = DIM == 3 ? (int)(rr / (unsigned)nc) : 0;
         int fx[3], fy[3], fz[3] = {0, 0, 0};
         rstencil<PER>(cx, nf, fx);
         rstencil<PER>(cy, nf, fy);
         if (DIM == 3) rstencil<PER>(cz, nf, fz);
         const double* src = fine + p * Sf;
         double acc = 0.0;
-        for (int a = 0; a < (DIM == 3 ? 3 : 1); ++a) {
-            const double wa = DIM == 3 ? w[a] : 1.0;
-            if (DIM == 3 && fz[a] < 0) continue;
-            for (int bb = 0; bb < 3; ++bb) {
-                if (fy[bb] < 0) continue;
+#pragma unroll
+        for (int a = 0; a < (DIM == 3 ? 3 : 1); ++a)
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb)
+#pragma unroll
                 for (int cc = 0; cc < 3; ++cc) {
-                    if (fx[cc] < 0) continue;
-                    const int64_t idx = ((int64_t)fz[a] * nf + fy[bb]) * nf + fx[cc];
-                    acc = fma(wa * w[bb] * w[cc], src[idx], acc);
+                    const bool ok = (DIM == 2 || fz[a] >= 0) && fy[bb] >= 0 && fx[cc] >= 0;
+                    const unsigned idx =
+                        ok ? ((unsigned)fz[a] * (unsigned)nf + (unsigned)fy[bb]) * (unsigned)nf +
+                                 (unsigned)fx[cc]
+                           : 0u;
+                    const double v = __ldg(src + idx);
+                    const double wa = DIM == 3 ? w[a] : 1.0;
+                    if (ok) acc = fma(wa * w[bb] * w[cc], v, acc);
                 }
-            }
-        }
         coarse[g] = acc;
     }
 }
@@ -203,31 +226,47 @@ __global__ void __launch_bounds__(PFB) k_pf_prolong_add(int nc, int nf, int64_t 
                                                        double* fine) {
     const int64_t Sc = DIM == 2 ? (int64_t)nc * nc : (int64_t)nc * nc * nc;
     const int64_t Sf = DIM == 2 ? (int64_t)nf * nf : (int64_t)nf * nf * nf;
-    for (int64_t g = blockIdx.x * (int64_t)PFB + threadIdx.x; g < planes * Sf;
-         g += (int64_t)gridDim.x * PFB) {
-        const int64_t p = g / Sf;
-        const int64_t j = g - p * Sf;
-        const int fx = (int)(j % nf), fy = (int)((j / nf) % nf);
-        const int fz = DIM == 3 ? (int)(j / ((int64_t)nf * nf)) : 0;
+    const unsigned R = DIM == 2 ? (unsigned)nf : (unsigned)nf * nf;  // fine rows per plane
+    const unsigned xt = ((unsigned)nf + 31u) / 32u;
+    const unsigned items = (unsigned)planes * R * xt;
+    const unsigned lane = threadIdx.x & 31u;
+    for (unsigned w = blockIdx.x * (PFB / 32) + (threadIdx.x >> 5); w < items;
+         w += gridDim.x * (PFB / 32)) {
+        const unsigned row = w / xt;
+        const unsigned fx_u = (w - row * xt) * 32u + lane;
+        if (fx_u >= (unsigned)nf) continue;
+        const unsigned p_u = row / R;
+        const unsigned rr = row - p_u * R;
+        const int64_t p = p_u;
+        const int64_t g = p * Sf + (int64_t)rr * nf + fx_u;
+        const int fx = (int)fx_u;
+        const int fy = DIM == 2 ? (int)rr : (int)(rr % (unsigned)nf);
+        const int fz = DIM == 3 ? (int)(rr / (unsigned)nf) : 0;
         int cx[2], cy[2], cz[2] = {0, -1};
         double wx[2], wy[2], wz[2] = {1.0, 0.0};
         pstencil<PER>(fx, nc, cx, wx);
         pstencil<PER>(fy, nc, cy, wy);
         if (DIM == 3) pstencil<PER>(fz, nc, cz, wz);
+        const double fv = fine[g];
         const double* src = coarse + p * Sc;
         double acc = 0.0;
-        for (int a = 0; a < 2; ++a) {
-            if (cz[a] < 0) continue;
-            for (int bb = 0; bb < 2; ++bb) {
-                if (cy[bb] < 0) continue;
+        // branch-free taps: every load issues back to back (a missing tap
+        // reads entry 0 and is not accumulated)
+#pragma unroll
+        for (int a = 0; a < (DIM == 3 ? 2 : 1); ++a)
+#pragma unroll
+            for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
                 for (int cc = 0; cc < 2; ++cc) {
-                    if (cx[cc] < 0) continue;
-                    const int64_t idx = ((int64_t)cz[a] * nc + cy[bb]) * nc + cx[cc];
-                    acc = fma(wz[a] * wy[bb] * wx[cc], src[idx], acc);
+                    const bool ok = cz[a] >= 0 && cy[bb] >= 0 && cx[cc] >= 0;
+                    const unsigned idx =
+                        ok ? ((unsigned)cz[a] * (unsigned)nc + (unsigned)cy[bb]) * (unsigned)nc +
+                                 (unsigned)cx[cc]
+                           : 0u;
+                    const double v = __ldg(src + idx);
+                    if (ok) acc = fma(wz[a] * wy[bb] * wx[cc], v, acc);
                 }
-            }
-        }
-        fine[g] += acc;
+        fine[g] = fv + acc;
     }
 }
 
@@ -314,8 +353,9 @@ namespace {
 
 template <int DIM, int M, bool PER>
 void launch_point(PfastPlan& P, int l, int mode, const double* x, const double* b, double* out) {
-    const int64_t S = P.len[l] / (P.nt * M);
-    const int g = P.c.grid_for(P.nt * S, PFB, 8);
+    const int64_t nl = P.n[l];
+    const int64_t rows = P.nt * (P.dim == 2 ? nl : nl * nl);
+    const int g = P.c.grid_for(rows * ((nl + 31) / 32) * 32, PFB, 8);
     const PfCoef& C = P.coef[l];
     switch (mode) {
         case 0: launch(k_pf_point<DIM, M, 0, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out); break;
@@ -351,8 +391,9 @@ PointFn pick(const PfastPlan& P) {
 
 void restrict_to(PfastPlan& P, int l, const double* fine, double* coarse) {
     const int64_t planes = P.nt * P.M;
-    const int g = P.c.grid_for(P.len[l + 1], PFB, 8);
     const int nc = P.n[l + 1], nf = P.n[l];
+    const int64_t rows = planes * (P.dim == 2 ? nc : (int64_t)nc * nc);
+    const int g = P.c.grid_for(rows * ((nc + 31) / 32) * 32, PFB, 8);
     if (P.dim == 2) {
         if (P.periodic) launch(k_pf_restrict<2, true>, g, PFB, 0, P.c.stream, nc, nf, planes, fine, coarse);
         else launch(k_pf_restrict<2, false>, g, PFB, 0, P.c.stream, nc, nf, planes, fine, coarse);
@@ -365,8 +406,9 @@ void restrict_to(PfastPlan& P, int l, const double* fine, double* coarse) {
 
 void prolong_add(PfastPlan& P, int l, const double* coarse, double* fine) {
     const int64_t planes = P.nt * P.M;
-    const int g = P.c.grid_for(P.len[l], PFB, 8);
     const int nc = P.n[l + 1], nf = P.n[l];
+    const int64_t rows = planes * (P.dim == 2 ? nf : (int64_t)nf * nf);
+    const int g = P.c.grid_for(rows * ((nf + 31) / 32) * 32, PFB, 8);
     if (P.dim == 2) {
         if (P.periodic) launch(k_pf_prolong_add<2, true>, g, PFB, 0, P.c.stream, nc, nf, planes, coarse, fine);
         else launch(k_pf_prolong_add<2, false>, g, PFB, 0, P.c.stream, nc, nf, planes, coarse, fine);
@@ -466,6 +508,8 @@ int pd_pfast_create(void* ctx, int dim, int64_t n, int bc_periodic, double kappa
                 }
             }
             if (nl > (1 << 20)) throw pd::ConfigError("grid too large");
+            if (nt * M * nl * (dim == 3 ? nl : 1) * ((nl + 31) / 32) >= (int64_t(1) << 31))
+                throw pd::ConfigError("P-fast grid x steps too large for one plan");
             P->n.push_back((int)nl);
             int64_t S = nl * nl * (dim == 3 ? nl : 1);
             P->len.push_back(nt * M * S);
