@@ -154,7 +154,9 @@ __device__ __forceinline__ void rstencil(int c, int nf, int f[3]) {
     f[2] = nb<PER>(ctr, 1, nf);
 }
 
-// coarse = Pᵀ fine over planes (nt·M of them)
+// coarse = Pᵀ fine over planes (nt·M of them).  One warp per coarse row: the
+// row's plane/y/z decomposition and its 3×3 fine source rows once per row,
+// lanes across x.
 template <int DIM, bool PER>
 __global__ void __launch_bounds__(PFB) k_pf_restrict(int nc, int nf, int64_t planes,
                                                     const double* __restrict__ fine,
@@ -163,43 +165,47 @@ __global__ void __launch_bounds__(PFB) k_pf_restrict(int nc, int nf, int64_t pla
     const int64_t Sf = DIM == 2 ? (int64_t)nf * nf : (int64_t)nf * nf * nf;
     const double w[3] = {0.5, 1.0, 0.5};
     const unsigned R = DIM == 2 ? (unsigned)nc : (unsigned)nc * nc;  // coarse rows per plane
-    const unsigned xt = ((unsigned)nc + 31u) / 32u;
-    const unsigned items = (unsigned)planes * R * xt;
-    const unsigned lane = threadIdx.x & 31u;
-    for (unsigned wi = blockIdx.x * (PFB / 32) + (threadIdx.x >> 5); wi < items;
-         wi += gridDim.x * (PFB / 32)) {
-        const unsigned row = wi / xt;
-        const unsigned cx_u = (wi - row * xt) * 32u + lane;
-        if (cx_u >= (unsigned)nc) continue;
+    const unsigned rows = (unsigned)planes * R;
+    const int lane = threadIdx.x & 31;
+    for (unsigned row = blockIdx.x * (PFB / 32) + (threadIdx.x >> 5); row < rows;
+         row += gridDim.x * (PFB / 32)) {
         const unsigned p_u = row / R;
         const unsigned rr = row - p_u * R;
-        const int64_t p = p_u;
-        const int64_t g = p * Sc + (int64_t)rr * nc + cx_u;
-        const int cx = (int)cx_u;
         const int cy = DIM == 2 ? (int)rr : (int)(rr % (unsigned)nc);
         const int cz = DIM == 3 ? (int)(rr / (unsigned)nc) : 0;
-        int fx[3], fy[3], fz[3] = {0, 0, 0};
-        rstencil<PER>(cx, nf, fx);
+        int fy[3], fz[3] = {0, -1, -1};
         rstencil<PER>(cy, nf, fy);
         if (DIM == 3) rstencil<PER>(cz, nf, fz);
-        const double* src = fine + p * Sf;
-        double acc = 0.0;
+        const double* src = fine + (int64_t)p_u * Sf;
+        // up to 9 source rows with their weights (missing rows: weight 0, row 0)
+        const double* rp[9];
+        double rw[9];
 #pragma unroll
-        for (int a = 0; a < (DIM == 3 ? 3 : 1); ++a)
+        for (int a = 0; a < 3; ++a)
 #pragma unroll
-            for (int bb = 0; bb < 3; ++bb)
+            for (int bb = 0; bb < 3; ++bb) {
+                const bool ok = (DIM == 3 ? fz[a] >= 0 : a == 1) && fy[bb] >= 0;
+                const int zz = DIM == 3 ? fz[a] : 0;
+                rp[a * 3 + bb] = src + (ok ? ((int64_t)zz * nf + fy[bb]) * nf : 0);
+                rw[a * 3 + bb] = ok ? (DIM == 3 ? w[a] : 1.0) * w[bb] : 0.0;
+            }
+        double* dst = coarse + (int64_t)p_u * Sc + (int64_t)rr * nc;
+        for (int cx = lane; cx < nc; cx += 32) {
+            int fx[3];
+            rstencil<PER>(cx, nf, fx);
+            const bool okl = fx[0] >= 0;  // Dirichlet: always; periodic: wrapped
+            double acc = 0.0;
 #pragma unroll
-                for (int cc = 0; cc < 3; ++cc) {
-                    const bool ok = (DIM == 2 || fz[a] >= 0) && fy[bb] >= 0 && fx[cc] >= 0;
-                    const unsigned idx =
-                        ok ? ((unsigned)fz[a] * (unsigned)nf + (unsigned)fy[bb]) * (unsigned)nf +
-                                 (unsigned)fx[cc]
-                           : 0u;
-                    const double v = __ldg(src + idx);
-                    const double wa = DIM == 3 ? w[a] : 1.0;
-                    if (ok) acc = fma(wa * w[bb] * w[cc], v, acc);
-                }
-        coarse[g] = acc;
+            for (int k = 0; k < 9; ++k) {
+                if (rw[k] == 0.0) continue;
+                const double* r = rp[k];
+                double v = okl ? 0.5 * __ldg(r + fx[0]) : 0.0;
+                v = fma(1.0, __ldg(r + fx[1]), v);
+                v = fma(0.5, __ldg(r + fx[2]), v);
+                acc = fma(rw[k], v, acc);
+            }
+            dst[cx] = acc;
+        }
     }
 }
 
@@ -219,7 +225,8 @@ __device__ __forceinline__ void pstencil(int f, int nc, int c[2], double w[2]) {
     }
 }
 
-// fine += P coarse over planes
+// fine += P coarse over planes.  One warp per fine row: its (≤ 2×2) coarse
+// source rows and weights once per row, lanes across x.
 template <int DIM, bool PER>
 __global__ void __launch_bounds__(PFB) k_pf_prolong_add(int nc, int nf, int64_t planes,
                                                        const double* __restrict__ coarse,
@@ -227,46 +234,54 @@ __global__ void __launch_bounds__(PFB) k_pf_prolong_add(int nc, int nf, int64_t 
     const int64_t Sc = DIM == 2 ? (int64_t)nc * nc : (int64_t)nc * nc * nc;
     const int64_t Sf = DIM == 2 ? (int64_t)nf * nf : (int64_t)nf * nf * nf;
     const unsigned R = DIM == 2 ? (unsigned)nf : (unsigned)nf * nf;  // fine rows per plane
-    const unsigned xt = ((unsigned)nf + 31u) / 32u;
-    const unsigned items = (unsigned)planes * R * xt;
-    const unsigned lane = threadIdx.x & 31u;
-    for (unsigned w = blockIdx.x * (PFB / 32) + (threadIdx.x >> 5); w < items;
-         w += gridDim.x * (PFB / 32)) {
-        const unsigned row = w / xt;
-        const unsigned fx_u = (w - row * xt) * 32u + lane;
-        if (fx_u >= (unsigned)nf) continue;
+    const unsigned rows = (unsigned)planes * R;
+    const int lane = threadIdx.x & 31;
+    for (unsigned row = blockIdx.x * (PFB / 32) + (threadIdx.x >> 5); row < rows;
+         row += gridDim.x * (PFB / 32)) {
         const unsigned p_u = row / R;
         const unsigned rr = row - p_u * R;
-        const int64_t p = p_u;
-        const int64_t g = p * Sf + (int64_t)rr * nf + fx_u;
-        const int fx = (int)fx_u;
         const int fy = DIM == 2 ? (int)rr : (int)(rr % (unsigned)nf);
         const int fz = DIM == 3 ? (int)(rr / (unsigned)nf) : 0;
-        int cx[2], cy[2], cz[2] = {0, -1};
-        double wx[2], wy[2], wz[2] = {1.0, 0.0};
-        pstencil<PER>(fx, nc, cx, wx);
+        int cy[2], cz[2] = {0, -1};
+        double wy[2], wz[2] = {1.0, 0.0};
         pstencil<PER>(fy, nc, cy, wy);
         if (DIM == 3) pstencil<PER>(fz, nc, cz, wz);
-        const double fv = fine[g];
-        const double* src = coarse + p * Sc;
-        double acc = 0.0;
-        // branch-free taps: every load issues back to back (a missing tap
-        // reads entry 0 and is not accumulated)
+        const double* src = coarse + (int64_t)p_u * Sc;
+        const double* rp[4];
+        double rw[4];
 #pragma unroll
-        for (int a = 0; a < (DIM == 3 ? 2 : 1); ++a)
+        for (int a = 0; a < 2; ++a)
 #pragma unroll
-            for (int bb = 0; bb < 2; ++bb)
+            for (int bb = 0; bb < 2; ++bb) {
+                const bool ok = cz[a] >= 0 && cy[bb] >= 0;
+                rp[a * 2 + bb] = src + (ok ? ((int64_t)cz[a] * nc + cy[bb]) * nc : 0);
+                rw[a * 2 + bb] = ok ? wz[a] * wy[bb] : 0.0;
+            }
+        double* dst = fine + (int64_t)p_u * Sf + (int64_t)rr * nf;
+        // 4 x tiles per pass: the fine loads of all four are in flight together
+        for (int fx0 = lane; fx0 < nf; fx0 += 128) {
+            double fv[4];
 #pragma unroll
-                for (int cc = 0; cc < 2; ++cc) {
-                    const bool ok = cz[a] >= 0 && cy[bb] >= 0 && cx[cc] >= 0;
-                    const unsigned idx =
-                        ok ? ((unsigned)cz[a] * (unsigned)nc + (unsigned)cy[bb]) * (unsigned)nc +
-                                 (unsigned)cx[cc]
-                           : 0u;
-                    const double v = __ldg(src + idx);
-                    if (ok) acc = fma(wz[a] * wy[bb] * wx[cc], v, acc);
+            for (int u = 0; u < 4; ++u) fv[u] = fx0 + 32 * u < nf ? dst[fx0 + 32 * u] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int fx = fx0 + 32 * u;
+                if (fx >= nf) break;
+                int cx[2];
+                double wx[2];
+                pstencil<PER>(fx, nc, cx, wx);
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    if (rw[k] == 0.0) continue;
+                    const double* r = rp[k];
+                    double v = cx[0] >= 0 ? wx[0] * __ldg(r + cx[0]) : 0.0;
+                    if (cx[1] >= 0) v = fma(wx[1], __ldg(r + cx[1]), v);
+                    acc = fma(rw[k], v, acc);
                 }
-        fine[g] = fv + acc;
+                dst[fx] = fv[u] + acc;
+            }
+        }
     }
 }
 
@@ -393,7 +408,7 @@ void restrict_to(PfastPlan& P, int l, const double* fine, double* coarse) {
     const int64_t planes = P.nt * P.M;
     const int nc = P.n[l + 1], nf = P.n[l];
     const int64_t rows = planes * (P.dim == 2 ? nc : (int64_t)nc * nc);
-    const int g = P.c.grid_for(rows * ((nc + 31) / 32) * 32, PFB, 8);
+    const int g = P.c.grid_for(rows * 32, PFB, 8);
     if (P.dim == 2) {
         if (P.periodic) launch(k_pf_restrict<2, true>, g, PFB, 0, P.c.stream, nc, nf, planes, fine, coarse);
         else launch(k_pf_restrict<2, false>, g, PFB, 0, P.c.stream, nc, nf, planes, fine, coarse);
@@ -408,7 +423,7 @@ void prolong_add(PfastPlan& P, int l, const double* coarse, double* fine) {
     const int64_t planes = P.nt * P.M;
     const int nc = P.n[l + 1], nf = P.n[l];
     const int64_t rows = planes * (P.dim == 2 ? nf : (int64_t)nf * nf);
-    const int g = P.c.grid_for(rows * ((nf + 31) / 32) * 32, PFB, 8);
+    const int g = P.c.grid_for(rows * 32, PFB, 8);
     if (P.dim == 2) {
         if (P.periodic) launch(k_pf_prolong_add<2, true>, g, PFB, 0, P.c.stream, nc, nf, planes, coarse, fine);
         else launch(k_pf_prolong_add<2, false>, g, PFB, 0, P.c.stream, nc, nf, planes, coarse, fine);
