@@ -258,13 +258,13 @@ __global__ void __launch_bounds__(PFB) k_pf_prolong_add(int nc, int nf, int64_t 
                 rw[a * 2 + bb] = ok ? wz[a] * wy[bb] : 0.0;
             }
         double* dst = fine + (int64_t)p_u * Sf + (int64_t)rr * nf;
-        // 4 x tiles per pass: the fine loads of all four are in flight together
-        for (int fx0 = lane; fx0 < nf; fx0 += 128) {
-            double fv[4];
+        // 8 x tiles per pass: the fine loads of all eight are in flight together
+        for (int fx0 = lane; fx0 < nf; fx0 += 256) {
+            double fv[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) fv[u] = fx0 + 32 * u < nf ? dst[fx0 + 32 * u] : 0.0;
+            for (int u = 0; u < 8; ++u) fv[u] = fx0 + 32 * u < nf ? dst[fx0 + 32 * u] : 0.0;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 const int fx = fx0 + 32 * u;
                 if (fx >= nf) break;
                 int cx[2];
