@@ -184,6 +184,11 @@ int pd_pfast_residual(void *plan, const double *x, const double *b, double *r, d
 int pd_pfast_sweep(void *plan, const double *b, double *x);
 int pd_pfast_solve(void *plan, const double *b, double *x, double tol_rel, double tol_abs,
                    int max_sweeps, pd_solve_report *report, double *hist /* host, optional */);
+/* Time-slab sharding: the plan's steps are one rank's slab; `halo` (device, n^d
+ * doubles, or NULL for the first slab) is the previous slab's x[last step,
+ * M-1], used by the residual of the first step.  The pointer is read at every
+ * later residual/sweep/solve call (the caller refreshes its contents). */
+int pd_pfast_set_halo(void *plan, const double *halo);
 int pd_pfast_destroy(void *plan);
 
 #ifdef __cplusplus

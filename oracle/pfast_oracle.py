@@ -102,11 +102,15 @@ class PfastOracle:
     def shape(self):
         return (self.Nt, self.M) + (self.n0,) * self.dim
 
-    def residual(self, x, b):
-        """b − L x (spacetime.py:117-124 structure)."""
+    def residual(self, x, b, halo=None):
+        """b − L x (spacetime.py:117-124 structure); `halo` = the previous time
+        slab's last node when the steps are one rank's slab."""
         L0 = self.levels[0]
         r = b - L0.apply(x)
-        r[1:] -= self.cprev.reshape((1, self.M) + (1,) * self.dim) * x[:-1, -1:]
+        cp = self.cprev.reshape((1, self.M) + (1,) * self.dim)
+        r[1:] -= cp * x[:-1, -1:]
+        if halo is not None:
+            r[:1] -= cp * np.asarray(halo).reshape((1, 1) + (self.n0,) * self.dim)
         return r
 
     def vcycle(self, l, b):
@@ -129,8 +133,8 @@ class PfastOracle:
             e = Lv.jacobi(e, b)
         return e
 
-    def sweep(self, x, b):
-        return x + self.omega_t * self.vcycle(0, self.residual(x, b))
+    def sweep(self, x, b, halo=None):
+        return x + self.omega_t * self.vcycle(0, self.residual(x, b, halo))
 
     def solve(self, b, x0=None, tol_rel=1e-10, tol_abs=0.0, max_sweeps=1000):
         """Returns (x flat, sweeps, converged, diverged, history) (multigrid.py:275-305)."""
@@ -156,3 +160,29 @@ class PfastOracle:
                 div = True
                 break
         return x.ravel(), it, conv, div, hist
+
+
+class OracleSlab:
+    """One rank's time slab for pfast.solve_time_slabs (CPU, numpy)."""
+
+    def __init__(self, orc: PfastOracle, b):
+        self.o = orc
+        self.b = np.asarray(b, dtype=np.float64).reshape(orc.shape())
+        self.x = np.zeros(orc.shape())
+        self.halo = None
+
+    def last_node(self):
+        return self.x[-1, -1].ravel().copy()
+
+    def set_halo(self, h):
+        self.halo = None if h is None else np.asarray(h, dtype=np.float64)
+
+    def residual_norm2(self):
+        r = self.o.residual(self.x, self.b, self.halo)
+        return float(np.sum(r * r))
+
+    def sweep(self):
+        self.x = self.o.sweep(self.x, self.b, self.halo)
+
+    def solution(self):
+        return self.x.ravel()

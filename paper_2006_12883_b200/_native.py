@@ -71,6 +71,7 @@ _SIGNATURES = {
     "pd_pfast_residual": (_int, [_vp, _vp, _vp, _vp, _vp]),
     "pd_pfast_sweep": (_int, [_vp, _vp, _vp]),
     "pd_pfast_solve": (_int, [_vp, _vp, _vp, _dbl, _dbl, _int, ctypes.POINTER(SolveReportC), _vp]),
+    "pd_pfast_set_halo": (_int, [_vp, _vp]),
     "pd_pfast_destroy": (_int, [_vp]),
     "pd_mg_set_fine_operator": (_int, [_vp, _vp]),
     "pd_mg_set_galerkin_intermediates": (_int, [_vp, _int, _vp]),

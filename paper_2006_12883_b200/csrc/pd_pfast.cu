@@ -51,11 +51,13 @@ __device__ __forceinline__ int nb(int v, int d, int n) {
 // MODE 0: out = x + Dinv(b − A x)     (damped point-block Jacobi)
 // MODE 1: out = Dinv b                (first sweep from a zero guess)
 // MODE 2: out = b − A x               (level residual)
-// MODE 3: out = b − A x − cprev·x[t-1, M-1]  (space-time residual, level 0)
+// MODE 3: out = b − A x − cprev·x[t-1, M-1]  (space-time residual, level 0;
+//         at t = 0 the coupling uses `halo` when non-null)
 template <int DIM, int M, int MODE, bool PER>
 __global__ void __launch_bounds__(PFB) k_pf_point(PfCoef C, int n, int64_t nt,
                                                  const double* __restrict__ x,
-                                                 const double* __restrict__ b, double* out) {
+                                                 const double* __restrict__ b, double* out,
+                                                 const double* __restrict__ halo) {
     // one warp per (step, grid row, 32-point x tile): 32-bit index math only
     const unsigned nn = (unsigned)n;
     const unsigned R = DIM == 2 ? nn : nn * nn;  // rows per step
@@ -125,8 +127,10 @@ __global__ void __launch_bounds__(PFB) k_pf_point(PfCoef C, int n, int64_t nt,
             }
             r[m] = bv[m] - ax;
         }
-        if (MODE == 3 && t > 0) {
-            const double xp = x[base - S];  // x[t-1, M-1, j]
+        if (MODE == 3 && (t > 0 || halo)) {
+            // x[t-1, M-1, j]; the first step of a time slab reads the previous
+            // slab's last node (halo) when the steps are sharded over ranks
+            const double xp = t > 0 ? x[base - S] : halo[j];
 #pragma unroll
             for (int m = 0; m < M; ++m) r[m] = fma(-C.cprev[m], xp, r[m]);
         }
@@ -358,6 +362,7 @@ struct PfastPlan {
     std::vector<DevBuf<double>> B, E, T;  // level rhs, iterate, ping-pong
     DevBuf<double> part, norm;
     double* pinned = nullptr;
+    const double* halo = nullptr;  // previous slab's last node (sharded steps)
     PfastPlan(Ctx& c_) : c(c_) {}
     ~PfastPlan() {
         if (pinned) cudaFreeHost(pinned);
@@ -373,10 +378,10 @@ void launch_point(PfastPlan& P, int l, int mode, const double* x, const double* 
     const int g = P.c.grid_for(rows * ((nl + 31) / 32) * 32, PFB, 8);
     const PfCoef& C = P.coef[l];
     switch (mode) {
-        case 0: launch(k_pf_point<DIM, M, 0, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out); break;
-        case 1: launch(k_pf_point<DIM, M, 1, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out); break;
-        case 2: launch(k_pf_point<DIM, M, 2, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out); break;
-        default: launch(k_pf_point<DIM, M, 3, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out);
+        case 0: launch(k_pf_point<DIM, M, 0, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out, (const double*)nullptr); break;
+        case 1: launch(k_pf_point<DIM, M, 1, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out, (const double*)nullptr); break;
+        case 2: launch(k_pf_point<DIM, M, 2, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out, (const double*)nullptr); break;
+        default: launch(k_pf_point<DIM, M, 3, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out, (const double*)P.halo);
     }
     PD_LAUNCH_CHECK();
 }
@@ -622,6 +627,10 @@ int pd_pfast_solve(void* plan, const double* b, double* x, double tol_rel, doubl
         rep->diverged = div;
         rep->hist_len = hist ? it + 1 : 0;
     });
+}
+
+int pd_pfast_set_halo(void* plan, const double* halo) {
+    return guarded_pf([&] { static_cast<pd::PfastPlan*>(plan)->halo = halo; });
 }
 
 int pd_pfast_destroy(void* plan) {

@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _native as N
 from .collocation import make_tableau
-from .errors import ConfigurationError
+from .errors import ConfigurationError, SolverError
 from .problems import StencilSpec
 from .report import SolveReport
 
@@ -123,3 +123,113 @@ class PfastSolver:
                              residual_history=hist[:rep.hist_len].tolist())
         out = x if N.is_tensor(b) else N.to_host(x)
         return out, report
+
+
+class DeviceSlab:
+    """One time slab on the device for `solve_time_slabs`: the solver's Nt steps
+    are this slab's steps; the previous slab's last node arrives as the halo."""
+
+    def __init__(self, solver: PfastSolver, b):
+        self.s = solver
+        self.b = solver._dev(b)
+        self.x = N.zeros(solver.n, solver.ctx)
+        S = solver.spec.ndof
+        self.halo_buf = N.zeros(S, solver.ctx)
+        self.norm = N.empty(1, solver.ctx)
+        self.r = N.empty(solver.n, solver.ctx)
+        self._last = slice(solver.n - S, solver.n)
+
+    def last_node(self):
+        return self.x[self._last]
+
+    def set_halo(self, h):
+        if h is None:
+            N.call("pd_pfast_set_halo", self.s.handle, ctypes.c_void_p())
+        else:
+            self.halo_buf.copy_(h if N.is_tensor(h) else N.to_device(np.asarray(h)))
+            N.call("pd_pfast_set_halo", self.s.handle, N.ptr(self.halo_buf))
+
+    def residual_norm2(self):
+        N.call("pd_pfast_residual", self.s.handle, N.ptr(self.x), N.ptr(self.b), N.ptr(self.r),
+               N.ptr(self.norm))
+        return float(self.norm.item())
+
+    def sweep(self):
+        N.call("pd_pfast_sweep", self.s.handle, N.ptr(self.b), N.ptr(self.x))
+
+    def solution(self):
+        return self.x
+
+
+def solve_time_slabs(slabs, tol_rel: float = 1e-10, tol_abs: float = 0.0,
+                     max_sweeps: int = 1000, group=None):
+    """P-fast over time slabs (north_star subsystem 4): `slabs` are this
+    process's consecutive slabs in time order; with a torch.distributed group,
+    ranks hold consecutive groups of slabs.  Per sweep the only exchange is
+    each slab's last node to its successor (send/recv between ranks) plus one
+    sum-allreduce of |r|^2 — block-Jacobi in time has no other coupling.
+    Same stopping/divergence rules and iterates as the serial solve
+    (multigrid.py:275-305).  Returns (sweeps, converged, diverged, history)."""
+    import math
+
+    torch = N.torch_mod()
+    dist = None
+    if group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()):
+        dist = torch.distributed
+    rank = dist.get_rank(group) if dist else 0
+    world = dist.get_world_size(group) if dist else 1
+
+    def exchange():
+        # halo of slab i = last node of slab i-1 (within the process) / of the
+        # previous rank's last slab
+        prev = None
+        if dist and world > 1:
+            last = slabs[-1].last_node()
+            send = last if N.is_tensor(last) else torch.from_numpy(np.ascontiguousarray(last))
+            recv = torch.empty_like(send)
+            reqs = []
+            if rank + 1 < world:
+                reqs.append(dist.isend(send.contiguous(), rank + 1, group=group))
+            if rank > 0:
+                reqs.append(dist.irecv(recv, rank - 1, group=group))
+            for q in reqs:
+                q.wait()
+            prev = recv if rank > 0 else None
+        halos = [prev] + [s.last_node() for s in slabs[:-1]]
+        for s, h in zip(slabs, halos):
+            s.set_halo(h)
+
+    def resid():
+        exchange()
+        n2 = sum(s.residual_norm2() for s in slabs)
+        if dist and world > 1:
+            t = torch.tensor([n2], dtype=torch.float64,
+                             device=slabs[0].last_node().device if N.is_tensor(slabs[0].last_node())
+                             else "cpu")
+            dist.all_reduce(t, group=group)
+            n2 = float(t.item())
+        return math.sqrt(n2)
+
+    r = resid()
+    thr = max(tol_abs, tol_rel * r)
+    lowest, hist, it = r, [r], 0
+    conv = div = False
+    while True:
+        if r <= thr:
+            conv = True
+            break
+        if it >= max_sweeps:
+            div = True
+            break
+        for s in slabs:
+            s.sweep()  # the halos set by resid() still describe the current x
+        it += 1
+        r = resid()
+        hist.append(r)
+        if not math.isfinite(r):
+            raise SolverError("non-finite residual in P-fast sweep")
+        lowest = min(lowest, r)
+        if r > 10.0 * lowest:
+            div = True
+            break
+    return it, conv, div, hist

@@ -102,3 +102,90 @@ def test_gpu_pfast_config_errors():
         PfastSolver(PB.StencilSpec(2, 16, "dirichlet"), 3, 2, 0.1, levels=2)  # even Dirichlet
     with pytest.raises(ConfigurationError):
         PfastSolver(PB.StencilSpec(2, 15, "dirichlet"), 7, 2, 0.1, levels=1)  # M > 5
+
+
+# ---------------------------------------------------------------- time slabs
+def _slab_parts(case, nslab):
+    dim, n, bc, coef, M, Nt, dt, levels = case
+    spec, tab, u0, orc = _case(*case)
+    from paper_2006_12883_b200.pfast import pfast_rhs
+    b = pfast_rhs(spec, M, Nt, u0, tab).reshape(Nt, -1)
+    k = Nt // nslab
+    parts = [b[i * k:(i + 1) * k].ravel() for i in range(nslab)]
+    orcs = [PfastOracle(dim, n, bc == "periodic", coef, M, k, dt, tab.Kq, tab.Mq,
+                        tab.left_values, levels) for _ in range(nslab)]
+    return b.ravel(), parts, orcs, orc
+
+
+def test_time_slabs_in_process_equal_serial():
+    """Block-Jacobi in time over 2 slabs (halo = previous slab's last node):
+    the same iterates and sweep counts as the serial restatement."""
+    from oracle.pfast_oracle import OracleSlab
+    from paper_2006_12883_b200.pfast import solve_time_slabs
+
+    b, parts, orcs, orc = _slab_parts(CASES[3], 2)
+    slabs = [OracleSlab(o, p) for o, p in zip(orcs, parts)]
+    its, conv, div, hist = solve_time_slabs(slabs, tol_rel=1e-10)
+    x_ref, its_ref, conv_ref, _, hist_ref = orc.solve(b, tol_rel=1e-10)
+    assert conv and conv_ref and its == its_ref
+    x = np.concatenate([s.solution() for s in slabs])
+    assert np.linalg.norm(x - x_ref) <= 1e-13 * np.linalg.norm(x_ref)
+    np.testing.assert_allclose(hist, hist_ref, rtol=1e-12)
+
+
+SLAB_CASE = (3, 7, "dirichlet", 1.0, 5, 4, 1 / 256, 2)  # C4-type, 4 steps -> 2 slabs
+
+
+def _gloo_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    from oracle.pfast_oracle import OracleSlab
+    from paper_2006_12883_b200.pfast import solve_time_slabs
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    b, parts, orcs, orc = _slab_parts(SLAB_CASE, world)
+    mine = [OracleSlab(orcs[rank], parts[rank])]
+    its, conv, div, hist = solve_time_slabs(mine, tol_rel=1e-10)
+    np.save(f"{out}/x{rank}.npy", mine[0].solution())
+    np.save(f"{out}/meta{rank}.npy", np.array([its, conv, div]))
+    dist.destroy_process_group()
+
+
+def test_time_slabs_gloo_world2_equal_serial(tmp_path):
+    """Two ranks (gloo), one slab each: only the slab-end state crosses ranks
+    (send/recv) plus one allreduce per sweep; equal to the serial restatement."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_gloo_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    b, parts, orcs, orc = _slab_parts(SLAB_CASE, 2)
+    x_ref, its_ref, conv_ref, _, _ = orc.solve(b, tol_rel=1e-10)
+    x = np.concatenate([np.load(tmp_path / f"x{r}.npy") for r in range(2)])
+    for r in range(2):
+        its, conv, div = np.load(tmp_path / f"meta{r}.npy")
+        assert its == its_ref and bool(conv) == conv_ref
+    assert np.linalg.norm(x - x_ref) <= 1e-13 * np.linalg.norm(x_ref)
+
+
+@pytest.mark.gpu
+def test_gpu_time_slabs_equal_serial_device():
+    """Two device slabs in one process (the per-rank schedule without waiting
+    kernels): equal sweep counts and 1e-12 vs the serial device solve."""
+    from paper_2006_12883_b200 import _native as N
+    from paper_2006_12883_b200.pfast import DeviceSlab, PfastSolver, solve_time_slabs
+
+    dim, n, bc, coef, M, Nt, dt, levels = CASES[3]
+    spec, tab, _, _ = _case(*CASES[3])
+    b, parts, orcs, orc = _slab_parts(CASES[3], 2)
+    slabs = [DeviceSlab(PfastSolver(spec, M, Nt // 2, dt, levels=levels, tableau=tab), p)
+             for p in parts]
+    its, conv, div, hist = solve_time_slabs(slabs, tol_rel=1e-10)
+    x_ser, rep = PfastSolver(spec, M, Nt, dt, levels=levels, tableau=tab).solve(b, tol_rel=1e-10)
+    assert conv and rep.converged and its == rep.iterations
+    x = np.concatenate([N.to_host(s.solution()) for s in slabs])
+    assert np.linalg.norm(x - x_ser) <= 1e-12 * np.linalg.norm(x_ser)
