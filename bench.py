@@ -447,7 +447,9 @@ def pfast_c5(peak: float, sweeps: int = 5):
         t = e0.elapsed_time(e1) / 1e3 / sweeps
         # algorithmic bytes of one sweep: level l has n_l = nt*M*S_l dofs
         nl = [s.n // (8 ** l) for l in range(s.levels)]
-        by = 24 * nl[0] + 24 * nl[0]  # space-time residual + x update
+        # space-time residual; the x update is fused into the last level-0 sweep
+        # (it reads and writes x on top of that sweep's 24 B/dof)
+        by = 24 * nl[0] + 16 * nl[0] - 8 * nl[0]
         for l in range(s.levels - 1):
             by += 16 * nl[l] + 24 * (s.nu - 1) * nl[l] + 24 * nl[l]  # pre-smooth, residual
             by += 8 * nl[l] + 8 * nl[l + 1] + 16 * nl[l] + 8 * nl[l + 1]  # restrict, prolong

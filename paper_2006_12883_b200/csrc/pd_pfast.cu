@@ -38,6 +38,7 @@ struct PfCoef {  // one level's point-block operator (row-major M×M each)
     double Ao[kPfMaxM * kPfMaxM];    // −dt·Mq·κh^{d-2} (per neighbour)
     double Dinv[kPfMaxM * kPfMaxM];  // ω·Ac⁻¹
     double cprev[kPfMaxM];           // −l0[m]·h^d (level 0 time coupling)
+    double omega_t;                  // outer damping (MODE 4)
 };
 
 // per-axis neighbour of coordinate v (−1 = outside a Dirichlet grid)
@@ -53,6 +54,7 @@ __device__ __forceinline__ int nb(int v, int d, int n) {
 // MODE 2: out = b − A x               (level residual)
 // MODE 3: out = b − A x − cprev·x[t-1, M-1]  (space-time residual, level 0;
 //         at t = 0 the coupling uses `halo` when non-null)
+// MODE 4: out += ω_t (x + Dinv(b − A x))  (MODE 0 fused with the outer update)
 template <int DIM, int M, int MODE, bool PER>
 __global__ void __launch_bounds__(PFB) k_pf_point(PfCoef C, int n, int64_t nt,
                                                  const double* __restrict__ x,
@@ -134,7 +136,7 @@ __global__ void __launch_bounds__(PFB) k_pf_point(PfCoef C, int n, int64_t nt,
 #pragma unroll
             for (int m = 0; m < M; ++m) r[m] = fma(-C.cprev[m], xp, r[m]);
         }
-        if (MODE >= 2) {
+        if (MODE == 2 || MODE == 3) {
 #pragma unroll
             for (int m = 0; m < M; ++m) out[base + m * S] = r[m];
         } else {
@@ -143,7 +145,10 @@ __global__ void __launch_bounds__(PFB) k_pf_point(PfCoef C, int n, int64_t nt,
                 double acc = xc[m];
 #pragma unroll
                 for (int k = 0; k < M; ++k) acc = fma(C.Dinv[m * M + k], r[k], acc);
-                out[base + m * S] = acc;
+                if (MODE == 4)  // last level-0 sweep: straight into the solution
+                    out[base + m * S] = fma(C.omega_t, acc, out[base + m * S]);
+                else
+                    out[base + m * S] = acc;
             }
         }
     }
@@ -381,6 +386,7 @@ void launch_point(PfastPlan& P, int l, int mode, const double* x, const double* 
         case 0: launch(k_pf_point<DIM, M, 0, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out, (const double*)nullptr); break;
         case 1: launch(k_pf_point<DIM, M, 1, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out, (const double*)nullptr); break;
         case 2: launch(k_pf_point<DIM, M, 2, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out, (const double*)nullptr); break;
+        case 4: launch(k_pf_point<DIM, M, 4, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out, (const double*)nullptr); break;
         default: launch(k_pf_point<DIM, M, 3, PER>, g, PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out, (const double*)P.halo);
     }
     PD_LAUNCH_CHECK();
@@ -439,32 +445,42 @@ void prolong_add(PfastPlan& P, int l, const double* coarse, double* fine) {
     PD_LAUNCH_CHECK();
 }
 
-// e_l ≈ A_l⁻¹ B_l from a zero guess; result in P.E[l] (T[l] is scratch)
-void vcycle(PfastPlan& P, int l) {
+// e_l ≈ A_l⁻¹ B_l from a zero guess; result in P.E[l] (T[l] is scratch).
+// With xupd (level 0) the last smoothing sweep, when it is a MODE 0 sweep,
+// adds ω_t·e straight into xupd instead of storing e (returns true then).
+bool vcycle(PfastPlan& P, int l, double* xupd = nullptr) {
+    bool fused = false;
     const PointFn op = pick(P);
     const int sweeps = (l == P.levels - 1) ? P.coarse_sweeps : P.nu;
     double* e = P.E[l].p;
     double* t = P.T[l].p;
     const double* b = P.B[l].p;
+    bool last = false;  // the smoothing pass that ends this level's work
     auto smooth = [&](int count, bool from_zero) {
         for (int s = 0; s < count; ++s) {
             if (from_zero && s == 0) {
                 op(P, l, 1, nullptr, b, e);
+            } else if (last && xupd && s == count - 1) {
+                op(P, l, 4, e, b, xupd);
+                fused = true;
             } else {
                 op(P, l, 0, e, b, t);
                 std::swap(e, t);
             }
         }
     };
+    last = l == P.levels - 1;
     smooth(sweeps, true);
     if (l < P.levels - 1) {
         op(P, l, 2, e, b, t);  // t = b − A e
         restrict_to(P, l, t, P.B[l + 1].p);
         vcycle(P, l + 1);
         prolong_add(P, l, P.E[l + 1].p, e);
+        last = true;
         smooth(P.nu, false);
     }
     if (e != P.E[l].p) std::swap(P.E[l].p, P.T[l].p);  // current iterate back in E[l]
+    return fused;
 }
 
 void norm2(PfastPlan& P, const double* v, int64_t n, double* out_dev) {
@@ -549,6 +565,7 @@ int pd_pfast_create(void* ctx, int dim, int64_t n, int bc_periodic, double kappa
             if (!pd::invert(D, Di, M)) throw pd::ConfigError("singular point block");
             for (int i = 0; i < M * M; ++i) C.Dinv[i] = omega_s * Di[i];
             for (int m = 0; m < M; ++m) C.cprev[m] = -l0[m] * mh;
+            C.omega_t = omega_t;
             P->coef.push_back(C);
         }
         P->B.resize(levels);
@@ -580,10 +597,11 @@ int pd_pfast_sweep(void* plan, const double* b, double* x) {
     return guarded_pf([&] {
         auto& P = *static_cast<pd::PfastPlan*>(plan);
         pd::pick(P)(P, 0, 3, x, b, P.B[0].p);
-        pd::vcycle(P, 0);
-        pd::launch(pd::k_pf_axpy, P.c.grid_for(P.len[0], pd::PFB, 8), pd::PFB, 0, P.c.stream,
-                   P.len[0], P.omega_t, (const double*)P.E[0].p, x);
-        PD_LAUNCH_CHECK();
+        if (!pd::vcycle(P, 0, x)) {
+            pd::launch(pd::k_pf_axpy, P.c.grid_for(P.len[0], pd::PFB, 8), pd::PFB, 0, P.c.stream,
+                       P.len[0], P.omega_t, (const double*)P.E[0].p, x);
+            PD_LAUNCH_CHECK();
+        }
     });
 }
 
@@ -611,10 +629,11 @@ int pd_pfast_solve(void* plan, const double* b, double* x, double tol_rel, doubl
         while (true) {
             if (r <= thr) { conv = 1; break; }
             if (it >= max_sweeps) { div = 1; break; }
-            pd::vcycle(P, 0);
-            pd::launch(pd::k_pf_axpy, P.c.grid_for(P.len[0], pd::PFB, 8), pd::PFB, 0, P.c.stream,
-                       P.len[0], P.omega_t, (const double*)P.E[0].p, x);
-            PD_LAUNCH_CHECK();
+            if (!pd::vcycle(P, 0, x)) {
+                pd::launch(pd::k_pf_axpy, P.c.grid_for(P.len[0], pd::PFB, 8), pd::PFB, 0,
+                           P.c.stream, P.len[0], P.omega_t, (const double*)P.E[0].p, x);
+                PD_LAUNCH_CHECK();
+            }
             ++it;
             r = resid();
             if (hist) hist[it] = r;
