@@ -23,6 +23,7 @@
 #include "pd_internal.h"
 
 #include <cmath>
+#include <cstdlib>
 #include <memory>
 #include <vector>
 
@@ -383,6 +384,8 @@ template <class K>
 int one_wave(const PfastPlan& P, K kernel, int64_t threads) {
     int occ = 0;
     PD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, PFB, 0));
+    static const int cap = getenv("PD_PF_BLOCKS") ? atoi(getenv("PD_PF_BLOCKS")) : 0;
+    if (cap > 0) occ = std::min(occ, cap);  // probe knob: fewer resident rows per SM
     return P.c.grid_for(threads, PFB, std::max(occ, 1));
 }
 
