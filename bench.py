@@ -44,7 +44,7 @@ UNIT = "GDOF/s"
 NU, LEVELS, PARTS, TOL = 3, 7, 8, 1e-10
 
 
-def workload_config(Nt=64):
+def workload_config(Nt=64):  # identical in both arms (like-for-like)
     return {
         "workload": "C2: 2D heat 255^2 Dirichlet FD, Nt=64, M=3 Radau, fp64; SMG L=7 V(3,3), "
                     "block-Jacobi(P=8 time slabs) ILU(0)-GMRES(3) smoother, dense-LU coarsest, "
@@ -109,13 +109,29 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU arm (oracle port)
-def cpu_sample(steps: int, warmup: int, threads: int):
-    """Reference algorithm on host cores: C2 with Nt=8 (same grid/M/hierarchy),
-    one V-cycle per step; returns (GDOF/s per sweep, sample description)."""
+def host_info():
+    """nproc and the CPU model of the box the CPU legs run on."""
+    model = ""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count() or 1, "cpu_model": model}
+
+
+def oracle_c2(threads: int, mats=None):
+    """The reference algorithm's CPU restatement (oracle/, a port pinned bitwise to the
+    reference's golden fixtures) on the SAME C2 configuration as the GPU arm: 255^2,
+    Nt=64, M=3, SMG L=7, nu=3, block-Jacobi P=8.  `mats` = prebuilt Galerkin level
+    matrices (the GPU arm's host copies, identical to the oracle's own products) to
+    skip the host Galerkin setup.  Returns (oracle hierarchy, b, dofs)."""
     from oracle import paradiff_oracle as O
     from paper_2006_12883_b200 import problems as PB
 
-    cfg = PB.baseline_config("C2", Nt=8)
+    cfg = PB.baseline_config("C2")
     ops = PB.fd_space(cfg.spec)
     s = O.OSystem(O.tableau(3), ops.Kh, ops.lumped_diagonal, cfg.Nt, cfg.T, 0.0, cfg.u0())
     specs = [cfg.spec]
@@ -123,43 +139,68 @@ def cpu_sample(steps: int, warmup: int, threads: int):
         specs.append(specs[-1].coarse())
     dims = [O.Dims(cfg.Nt, 3, sp_.ndof) for sp_ in specs]
     pairs = [PB.fd_transfers(specs[l]) for l in range(LEVELS - 1)]
-    mg = O.OMultigrid(s.global_matrix(), dims, O.composite_transfers(dims, pairs), NU, PARTS,
-                      threads=threads)
-    b = s.rhs()
+    trs = O.composite_transfers(dims, pairs)
+    A = s.global_matrix() if mats is None else mats[0]
+    mg = O.OMultigrid(A, dims, trs, NU, PARTS, threads=threads, mats=mats)
+    return mg, s.rhs(), s.size
+
+
+def cpu_cycles(mg, b, dofs, warmup: int, steps: int, tol=TOL):
+    """Time V-cycles of the C2 solve on host cores.  The cycles run from x = 0 as in
+    MultigridHierarchy.solve (multigrid.py:275-305): the warm-up cycles are the
+    solve itself (its cycle count and time are reported when it converges within
+    them); each timed step is one further V-cycle (same work per cycle)."""
     x = np.zeros_like(b)
-    for _ in range(warmup):
+    thr = max(tol, tol * float(np.linalg.norm(b)))
+    solve_t, solve_cycles, t_acc = None, None, 0.0
+    for k in range(warmup):
+        t0 = time.perf_counter()
         x = mg.vcycle(b, x)
+        res = float(np.linalg.norm(b - mg.mats[0] @ x))
+        t_acc += time.perf_counter() - t0
+        if solve_t is None and res <= thr:
+            solve_t, solve_cycles = t_acc, k + 1
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
         x = mg.vcycle(b, x)
         times.append(time.perf_counter() - t0)
     t = float(np.mean(times))
-    value = s.size * 2 * NU / t / 1e9
-    sample = (f"C2 grid 255^2, M=3, Nt=8 (of 64), SMG L=7 nu=3 P=8: one V-cycle per step, "
-              f"{t:.2f} s/cycle")
-    return value, sample, t
+    return dofs * 2 * NU / t / 1e9, t, solve_t, solve_cycles
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
-    threads = min(PARTS, os.cpu_count() or 1)
-    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count() or 1))
-    value, sample, t = cpu_sample(args.steps, args.warmup, threads)
+    hi = host_info()
+    threads = min(PARTS, hi["nproc"])  # the block-Jacobi pool has P = 8 blocks
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", str(hi["nproc"]))
+    t0 = time.perf_counter()
+    mg, b, dofs = oracle_c2(threads)
+    setup = time.perf_counter() - t0
+    value, t, solve_t, solve_cycles = cpu_cycles(mg, b, dofs, args.warmup, args.steps)
+    sample = (f"full C2 system (Nt=64, 12,484,800 dofs), oracle port on {threads} host threads "
+              f"({hi['nproc']} cores, {hi['cpu_model']}); one step = one V-cycle of the solve "
+              f"from x=0 ({t:.2f} s/cycle); setup {setup:.0f} s excluded")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(8) | {"sample": sample},
+        "config": workload_config() | {"parallelism": parallelism_label(world)},
+        "solve_time_s": solve_t, "cycles_per_solve": solve_cycles, "setup_s": setup,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, **hi},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def parallelism_label(world: int) -> str:
+    return "1 GPU" if world == 1 else f"time-slab sharded MG over {world} GPUs"
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -342,19 +383,25 @@ def run_b200(args):
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline:
-            threads = min(PARTS, os.cpu_count() or 1)
-            cv, sample, _ = cpu_sample(1, 1, threads)
-            cpu = {"value": cv, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample}
+            # bounded sample of the same workload: one V-cycle of the full C2 system on
+            # the host cores, reusing this run's Galerkin matrices (no host re-setup)
+            hi = host_info()
+            threads = min(PARTS, hi["nproc"])
+            mg_o, b_o, dofs_o = oracle_c2(threads, mats=[pd.linalg.as_csr(m)
+                                                         for m in h.matrices])
+            cv, ct, _, _ = cpu_cycles(mg_o, b_o, dofs_o, 0, 1)
+            del mg_o
+            cpu = {"value": cv, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": f"one V-cycle of the full C2 system (Nt=64) on {threads} host "
+                             f"threads: {ct:.2f} s", **hi}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_dev / args.steps * 1e3, "higher_is_better": True,
             "scaling": "weak" if replicas > 1 else "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": workload_config() | {"parallelism": (
-                f"time-slab sharded MG over {world} GPUs (block-Jacobi partitions "
-                f"{PARTS // world}/rank, NCCL halo + allreduce)") if smg is not None else (
-                f"replicas x{world} (sharded setup refused)" if world > 1 else "1 GPU")},
+            "config": workload_config() | {"parallelism": parallelism_label(world) if (
+                world == 1 or smg is not None) else f"replicas x{world} (sharded setup refused)"},
             "solve_time_s": t_dev / args.steps, "cycles_per_solve": cycles / max(args.steps, 1),
             "setup_s": setup_s,
             "clocks": clk.summary(),

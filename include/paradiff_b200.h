@@ -70,6 +70,14 @@ int pd_ilu0_levels(void *ilu, int32_t *lower_levels, int32_t *upper_levels); /* 
  * linalg.py:104-113; the reference has no counterpart. */
 int pd_ilu0_set_wavefront(void *ctx, void *ilu, int64_t ngroup, int64_t nline, int64_t npoint,
                           int64_t ngroup_lower, int *applied);                    /* synchronising */
+/* Copy the factor values (L strictly below, U on and above the diagonal, on the
+ * factor's CSR pattern; host or device `out`, `cap` >= nnz) — linalg.py:138-145
+ * Ilu0.factors(). */
+int pd_ilu0_factor_values(void *ctx, void *ilu, double *out, int64_t cap); /* synchronising */
+/* Which executor runs this factor's sweeps: 2 = template-structured skewed
+ * wavefront (pd_wf2.cu: one thread per grid line over all M nodes), 1 = pattern-table
+ * wavefront (pd_wavefront.cu), 0 = level-scheduled value-as-flag sweeps. */
+int pd_ilu0_sweep_kind(void *ilu, int *kind);
 int pd_ilu0_destroy(void *ilu);
 /* Structured SpMV for a 2D-grid space-time operator (SMG Galerkin levels: every
  * row couples to the previous step's last node and to each node of its own

@@ -645,19 +645,26 @@ def composite_transfers(dims, space_pairs):
 class OMultigrid:
     """multigrid.py:197-305 (Galerkin hierarchy, GMRES(nu)+ILU smoother, dense-LU coarsest)."""
 
-    def __init__(self, A, dims, transfers, nu, partitions=1, restart=30, smooth_solves=1, threads=1):
+    def __init__(self, A, dims, transfers, nu, partitions=1, restart=30, smooth_solves=1, threads=1,
+                 mats=None):
         self.dims, self.transfers, self.nu = dims, transfers, nu
         self.partitions, self.restart, self.smooth_solves = partitions, restart, smooth_solves
         self.threads = threads
-        self.set_fine_matrix(A)
+        self.set_fine_matrix(A, mats)
 
-    def set_fine_matrix(self, A):
-        """multigrid.py:224-241."""
+    def set_fine_matrix(self, A, mats=None):
+        """multigrid.py:224-241.  `mats`: the level matrices R A P already formed
+        (bench.py's CPU leg hands over the GPU arm's host copies of the same scipy
+        products to skip the host Galerkin setup)."""
         A = canon(A)
         if A.shape[0] != self.dims[0].size:
             raise OracleConfigError("fine matrix size mismatch")
         self.mats = [A]
-        for R, P in self.transfers:
+        if mats is not None:
+            if len(mats) != len(self.dims):
+                raise OracleConfigError("level matrix count mismatch")
+            self.mats += [canon(m) for m in mats[1:]]
+        for R, P in self.transfers[len(self.mats) - 1:]:
             self.mats.append(canon(R @ self.mats[-1] @ P))
         self.pre = []
         for Al in self.mats[:-1]:

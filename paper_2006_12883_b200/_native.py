@@ -51,6 +51,8 @@ _SIGNATURES = {
     "pd_ilu0_solve": (_int, [_vp, _vp, _vp, _vp]),
     "pd_ilu0_levels": (_int, [_vp, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "pd_ilu0_set_wavefront": (_int, [_vp, _vp, _i64, _i64, _i64, _i64, ctypes.POINTER(_int)]),
+    "pd_ilu0_sweep_kind": (_int, [_vp, ctypes.POINTER(_int)]),
+    "pd_ilu0_factor_values": (_int, [_vp, _vp, _vp, _i64]),
     "pd_csr_set_grid": (_int, [_vp, _vp, _i64, _int, _i64, ctypes.POINTER(_int)]),
     "pd_ilu0_destroy": (_int, [_vp]),
     "pd_dense_lu_create": (_int, [_vp, _vp, ctypes.POINTER(_vp)]),

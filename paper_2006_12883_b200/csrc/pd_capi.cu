@@ -128,6 +128,22 @@ int pd_ilu0_set_wavefront(void* ctx, void* ilu, int64_t ngroup, int64_t nline, i
         if (applied) *applied = ok ? 1 : 0;
     });
 }
+int pd_ilu0_factor_values(void* ctx, void* ilu, double* out, int64_t cap) {
+    return guarded([&] {
+        auto* c = H<pd::Ctx>(ctx, "ctx");
+        auto* f = H<pd::Ilu0>(ilu, "ilu");
+        const pd::Csr& P = f->pat();
+        if (cap < P.nnz) throw pd::ConfigError("factor value buffer too small");
+        PD_CUDA(cudaStreamSynchronize(c->stream));
+        PD_CUDA(cudaMemcpy(out, f->fac.p, P.nnz * sizeof(double), cudaMemcpyDefault));
+    });
+}
+int pd_ilu0_sweep_kind(void* ilu, int* kind) {
+    return guarded([&] {
+        auto* f = H<pd::Ilu0>(ilu, "ilu");
+        *kind = f->w2_lo ? 2 : f->wf_lo ? 1 : 0;
+    });
+}
 int pd_csr_set_grid(void* ctx, void* csr, int64_t nt, int M, int64_t n, int* applied) {
     return guarded([&] {
         const bool ok = pd::csr_attach_grid(*C(ctx), *H<pd::Csr>(csr, "csr"), nt, M, n);

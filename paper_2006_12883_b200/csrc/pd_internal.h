@@ -154,6 +154,8 @@ struct WfPlan {
     DevBuf<unsigned long long> trace;  // PD_WF_TRACE diagnostics
 };
 
+struct Wf2Plan;  // skewed-wavefront sweeps for structured 2D levels (pd_wf2.cu)
+
 // ILU(0) factors with level schedules (see pd_sparse.cu).
 struct Ilu0 {
     int64_t n = 0;
@@ -175,6 +177,7 @@ struct Ilu0 {
     DevBuf<double> tval_lo, tval_up, tdiag;
     std::vector<std::pair<int64_t, int64_t>> ranges;
     std::unique_ptr<WfPlan> wf_lo, wf_up;  // structured sweeps (optional)
+    std::shared_ptr<Wf2Plan> w2_lo, w2_up; // template-structured sweeps (preferred when set)
     const Csr& pat() const { return use_masked ? masked : *pattern; }
 };
 
@@ -220,6 +223,10 @@ void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard = 
 bool ilu0_set_wavefront(Ctx& c, Ilu0& f, int64_t ngroup, int64_t nline, int64_t npoint,
                         int64_t ngroup_lower);
 void wf_gather(Ctx& c, Ilu0& f);
+// template-structured sweeps (pd_wf2.cu): rows [task][M][nline][npoint]; false = not applicable
+bool ilu0_set_wf2(Ctx& c, Ilu0& f, int M, int64_t nline, int64_t npoint);
+void wf2_gather(Ctx& c, Ilu0& f);
+void wf2_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int want);
 // fill a sweep output with the value-as-flag pending sentinel (coalesced)
 void arm_pending(Ctx& c, double* y, int64_t n, const int* guard, int want);  // refresh plan values after a (re)factorization
 void wf_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int want);

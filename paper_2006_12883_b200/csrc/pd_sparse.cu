@@ -732,6 +732,7 @@ void ilu0_refactor(Ctx& c, Ilu0& f) {
     }
     build_task_layout(c, f);
     wf_gather(c, f);
+    wf2_gather(c, f);
 }
 
 static void configure_polling_once() {
@@ -749,6 +750,10 @@ void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, i
     const int64_t n = f.n;
     if (n == 0) return;
     if (b == x) throw ConfigError("ILU(0) solve needs distinct input and output buffers");
+    if (f.w2_lo) {
+        wf2_solve(c, f, b, x, guard, want);
+        return;
+    }
     if (f.wf_lo) {
         wf_solve(c, f, b, x, guard, want);
         return;

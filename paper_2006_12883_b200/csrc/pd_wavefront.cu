@@ -953,6 +953,8 @@ bool ilu0_set_wavefront(Ctx& c, Ilu0& f, int64_t ngroup, int64_t nline, int64_t 
     f.wf_lo.reset();
     f.wf_up.reset();
     if (wavefront_disabled() || f.n == 0) return false;
+    // template-structured sweeps first (one time step per task, pd_wf2.cu)
+    if (ngroup > 0 && ngroup <= 8 && ilu0_set_wf2(c, f, (int)ngroup, nline, npoint)) return true;
     // the lower sweep's tasks may span several time steps (in-task time coupling
     // through the ring instead of cross-CTA polls); the upper factor has no time
     // coupling, so its tasks stay one step each

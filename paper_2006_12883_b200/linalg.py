@@ -144,6 +144,30 @@ class Ilu0:
         (the lower sweep's tasks span `ngroup_lower` grids when > 0)."""
         return set_wavefront(self.ctx, self.handle, ngroup, nline, npoint, ngroup_lower)
 
+    def factors(self) -> tuple[sp.csr_matrix, sp.csr_matrix]:
+        """(L, U) as explicit CSR matrices, unit diagonal on L (linalg.py:138-145):
+        the device factor values copied back onto the factor's pattern."""
+        if type(self) is not Ilu0 or self._A._indptr is None:
+            raise ConfigurationError("factors() is defined for a single ILU(0) of a host matrix")
+        rp, ci = self._A._indptr, self._A._indices
+        vals = np.empty(int(rp[-1]), dtype=np.float64)
+        N.call("pd_ilu0_factor_values", self.ctx.handle, self.handle,
+               vals.ctypes.data_as(ctypes.c_void_p), int(vals.size))
+        full = sp.csr_matrix((vals, ci, rp), shape=(self.n, self.n))
+        L = sp.tril(full, k=-1) + sp.eye(self.n, format="csr")
+        U = sp.triu(full, k=0)
+        return as_csr(L), as_csr(U)
+
+    def update_values(self, A) -> None:
+        """New values on the same pattern (e.g. a Newton Jacobian): device refactor."""
+        self._A.set_values(as_csr(A).data)
+        N.call("pd_ilu0_refactor", self.ctx.handle, self.handle)
+
+    def sweep_kind(self) -> int:
+        """2: template-structured wavefront (pd_wf2.cu), 1: pattern-table wavefront,
+        0: level-scheduled sweeps."""
+        return sweep_kind(self.handle)
+
     def solve_dev(self, b, out=None):
         self.ctx.sync_stream()
         out = N.empty(self.n, self.ctx) if out is None else out
@@ -167,6 +191,12 @@ def set_wavefront(ctx, ilu_handle, ngroup: int, nline: int, npoint: int,
     N.call("pd_ilu0_set_wavefront", ctx.handle, ilu_handle, int(ngroup), int(nline), int(npoint),
            int(ngroup_lower), ctypes.byref(applied))
     return bool(applied.value)
+
+
+def sweep_kind(ilu_handle) -> int:
+    k = ctypes.c_int()
+    N.call("pd_ilu0_sweep_kind", ilu_handle, ctypes.byref(k))
+    return k.value
 
 
 def ilu0(A) -> Ilu0:

@@ -31,3 +31,15 @@ def per_node_rel(a, b, shape, floor=NODE_FLOOR):
 def per_node_rel_strict(a, b, shape):
     """Per-node relative L2 against each node's own norm (no floor)."""
     return per_node_rel(a, b, shape, floor=0.0)
+
+
+def slab_projections(X, k=4, seed=12345):
+    """k seeded Gaussian projections of every (step, node) slab of X (..., S).
+
+    Compact at-size fixtures store these instead of the full solution
+    (tests/golden/make_golden_sized.py): |P(a) - P(b)| <= ||a - b|| * ||g||
+    per slab, so a per-node relative L2 of 1e-10 bounds the projection error.
+    """
+    X = np.asarray(X)
+    g = np.random.default_rng(seed).standard_normal((k, X.shape[-1]))
+    return X @ g.T

@@ -23,11 +23,14 @@ def _system(name, n, Nt):
                                    pd.TimeGrid(cfg.Nt, cfg.T), 0.0, cfg.u0())
 
 
-def _check(A, ngroup, nline, npoint, parts, seed=0, repeats=2, applies=True, ngroup_lower=0):
+def _check(A, ngroup, nline, npoint, parts, seed=0, repeats=2, applies=True, ngroup_lower=0,
+           kind=None):
     A = pd.linalg.as_csr(A)
     rng = np.random.default_rng(seed)
     dev = pd.BlockJacobiPrecond(A, parts) if parts > 1 else pd.Ilu0(A)
     assert dev.set_wavefront(ngroup, nline, npoint, ngroup_lower) == applies
+    if kind is not None:
+        assert dev.sweep_kind() == kind
     ref = O.OBlockJacobi(A, parts) if parts > 1 else O.OIlu0(A)
     for _ in range(repeats):  # repeated solves exercise the re-arming protocol
         b = rng.standard_normal(A.shape[0])
@@ -54,15 +57,19 @@ def test_wavefront_3d_planes_fall_back():
     _check(s.global_matrix(), 1, cfg.spec.n, cfg.spec.n, 2, applies=False)
 
 
-def test_wavefront_single_group_ring_and_globals_bitwise():
-    """One node grid per task (M=1 layout view): node couplings become globals."""
+def test_wavefront_single_group_ring_and_globals_bitwise(monkeypatch):
+    """One node grid per task (M=1 layout view): node couplings become globals
+    (pattern-table executor)."""
+    monkeypatch.setenv("PD_WF2", "0")
     cfg, s = _system("C2", 15, 4)
     A = pd.linalg.as_csr(s.global_matrix())
     # a 2-group task view of a 1-node-per-task split still has <= 2 globals per row
     _check(A, cfg.M, cfg.spec.n, cfg.spec.n, 4, seed=3)
 
 
-def test_wavefront_galerkin_levels_bitwise():
+@pytest.mark.parametrize("wf2", ["1", "0"])
+def test_wavefront_galerkin_levels_bitwise(monkeypatch, wf2):
+    monkeypatch.setenv("PD_WF2", wf2)
     cfg, s = _system("C2", 31, 8)
     h = pd.build_hierarchy(s, "SMG", 4, 2, partitions=2)
     assert h.wavefront == [True, True, True]
@@ -73,8 +80,10 @@ def test_wavefront_galerkin_levels_bitwise():
 
 
 @pytest.mark.parametrize("k", [2, 4])
-def test_wavefront_multistep_lower_tasks_bitwise(k):
-    """Lower-sweep tasks spanning k time steps (time coupling through the ring)."""
+def test_wavefront_multistep_lower_tasks_bitwise(monkeypatch, k):
+    """Lower-sweep tasks spanning k time steps (time coupling through the ring;
+    pattern-table executor, the template executor pinned off)."""
+    monkeypatch.setenv("PD_WF2", "0")
     cfg, s = _system("C2", 15, 8)
     _check(s.global_matrix(), cfg.M, cfg.spec.n, cfg.spec.n, 2, seed=k, ngroup_lower=cfg.M * k)
     h = pd.build_hierarchy(s, "SMG", 3, 2, partitions=2)
@@ -141,3 +150,56 @@ def test_grid_spmv_galerkin_levels_bitwise(monkeypatch):
     x2, r2 = h2.solve(b, tol_rel=1e-10, tol_abs=1e-10)
     assert r1.iterations == r2.iterations and r1.converged
     assert np.linalg.norm(x1 - x2) <= 1e-12 * np.linalg.norm(x2)
+
+
+# ---- template-structured skewed wavefront (csrc/pd_wf2.cu) -------------------------
+@pytest.mark.parametrize("n,parts", [(15, 1), (31, 2), (63, 4), (127, 8)])
+def test_wf2_fine_level_bitwise(n, parts):
+    """Fine level (5-point x M x M, point coupling to the previous step), every
+    line-block size class (NLP 32/64/128): kind 2, bitwise the numba reference."""
+    cfg, s = _system("C2", n, 8)
+    _check(s.global_matrix(), cfg.M, n, n, parts, seed=n, kind=2)
+
+
+@pytest.mark.parametrize("n,parts", [(31, 1), (63, 2), (127, 8)])
+def test_wf2_galerkin_levels_bitwise(n, parts):
+    """SMG Galerkin levels (9-point x M x M, 3x3 coupling to the previous step)."""
+    cfg, s = _system("C2", n, 8)
+    h = pd.build_hierarchy(s, "SMG", 3, 2, partitions=parts)
+    spec = cfg.spec
+    for l, A in enumerate(h.matrices[:-1]):
+        _check(A, cfg.M, spec.n, spec.n, parts, seed=l, kind=2)
+        spec = spec.coarse()
+
+
+def test_wf2_equals_pattern_table_executor(monkeypatch):
+    """Both wavefront executors on a 127^2 fine level and its Galerkin level: bitwise."""
+    cfg, s = _system("C2", 127, 8)
+    h = pd.build_hierarchy(s, "SMG", 3, 2, partitions=8)
+    rng = np.random.default_rng(11)
+    spec = cfg.spec
+    for A in h.matrices[:-1]:
+        A = pd.linalg.as_csr(A)
+        b = rng.standard_normal(A.shape[0])
+        outs = []
+        for flag, kind in (("1", 2), ("0", 1)):
+            monkeypatch.setenv("PD_WF2", flag)
+            dev = pd.BlockJacobiPrecond(A, 8)
+            assert dev.set_wavefront(cfg.M, spec.n, spec.n)
+            assert dev.sweep_kind() == kind
+            outs.append(dev.solve(b))
+        np.testing.assert_array_equal(outs[0], outs[1])
+        spec = spec.coarse()
+
+
+def test_wf2_refactor_refreshes_values():
+    """A values-only refactor (Newton) regathers the step blocks."""
+    cfg, s = _system("C2", 31, 4)
+    A = pd.linalg.as_csr(s.global_matrix())
+    dev = pd.BlockJacobiPrecond(A, 2)
+    assert dev.set_wavefront(cfg.M, 31, 31) and dev.sweep_kind() == 2
+    A2 = A.copy()
+    A2.data = A2.data * (1.0 + 0.01 * np.random.default_rng(2).standard_normal(A2.nnz))
+    dev.update_values(A2)
+    b = np.random.default_rng(3).standard_normal(A.shape[0])
+    np.testing.assert_array_equal(dev.solve(b), O.OBlockJacobi(A2, 2).solve(b))
