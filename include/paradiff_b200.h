@@ -75,8 +75,9 @@ int pd_ilu0_set_wavefront(void *ctx, void *ilu, int64_t ngroup, int64_t nline, i
  * Ilu0.factors(). */
 int pd_ilu0_factor_values(void *ctx, void *ilu, double *out, int64_t cap); /* synchronising */
 /* Which executor runs this factor's sweeps: 2 = template-structured skewed
- * wavefront (pd_wf2.cu: one thread per grid line over all M nodes), 1 = pattern-table
- * wavefront (pd_wavefront.cu), 0 = level-scheduled value-as-flag sweeps. */
+ * wavefront for both sweeps (pd_wf2.cu), 3 = pattern-table lower sweep + template
+ * upper sweep, 1 = pattern-table wavefront (pd_wavefront.cu), 0 = level-scheduled
+ * value-as-flag sweeps. */
 int pd_ilu0_sweep_kind(void *ilu, int *kind);
 int pd_ilu0_destroy(void *ilu);
 /* Structured SpMV for a 2D-grid space-time operator (SMG Galerkin levels: every

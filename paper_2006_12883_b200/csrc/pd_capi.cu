@@ -141,7 +141,7 @@ int pd_ilu0_factor_values(void* ctx, void* ilu, double* out, int64_t cap) {
 int pd_ilu0_sweep_kind(void* ilu, int* kind) {
     return guarded([&] {
         auto* f = H<pd::Ilu0>(ilu, "ilu");
-        *kind = f->w2_lo ? 2 : f->wf_lo ? 1 : 0;
+        *kind = f->w2_lo ? 2 : (f->w2_up && f->wf_lo) ? 3 : f->wf_lo ? 1 : 0;
     });
 }
 int pd_csr_set_grid(void* ctx, void* csr, int64_t nt, int M, int64_t n, int* applied) {

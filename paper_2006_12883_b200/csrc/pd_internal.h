@@ -227,6 +227,11 @@ void wf_gather(Ctx& c, Ilu0& f);
 bool ilu0_set_wf2(Ctx& c, Ilu0& f, int M, int64_t nline, int64_t npoint);
 void wf2_gather(Ctx& c, Ilu0& f);
 void wf2_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int want);
+// mixed executors: pattern-table lower sweep (b -> scratch), template upper (scratch -> x)
+bool wf2_lower_preferred(const Ilu0& f);
+void wf2_drop_lower(Ilu0& f);
+void wf2_solve_upper(Ctx& c, Ilu0& f, double* x, const int* guard, int want);
+void wf_solve_lower(Ctx& c, Ilu0& f, const double* b, const int* guard, int want);
 // fill a sweep output with the value-as-flag pending sentinel (coalesced)
 void arm_pending(Ctx& c, double* y, int64_t n, const int* guard, int want);  // refresh plan values after a (re)factorization
 void wf_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int want);

@@ -754,6 +754,11 @@ void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, i
         wf2_solve(c, f, b, x, guard, want);
         return;
     }
+    if (f.w2_up && f.wf_lo) {  // pattern-table lower sweep + template upper sweep
+        wf_solve_lower(c, f, b, guard, want);
+        wf2_solve_upper(c, f, x, guard, want);
+        return;
+    }
     if (f.wf_lo) {
         wf_solve(c, f, b, x, guard, want);
         return;

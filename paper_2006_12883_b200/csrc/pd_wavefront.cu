@@ -953,8 +953,11 @@ bool ilu0_set_wavefront(Ctx& c, Ilu0& f, int64_t ngroup, int64_t nline, int64_t 
     f.wf_lo.reset();
     f.wf_up.reset();
     if (wavefront_disabled() || f.n == 0) return false;
-    // template-structured sweeps first (one time step per task, pd_wf2.cu)
-    if (ngroup > 0 && ngroup <= 8 && ilu0_set_wf2(c, f, (int)ngroup, nline, npoint)) return true;
+    // template-structured sweeps first (one time step per task, pd_wf2.cu); where its
+    // lower sweep is not the faster one (wf2_lower_preferred) the pattern-table lower
+    // sweep below runs with the template upper sweep
+    const bool w2 = ngroup > 0 && ngroup <= 8 && ilu0_set_wf2(c, f, (int)ngroup, nline, npoint);
+    if (w2 && wf2_lower_preferred(f)) return true;
     // the lower sweep's tasks may span several time steps (in-task time coupling
     // through the ring instead of cross-CTA polls); the upper factor has no time
     // coupling, so its tasks stay one step each
@@ -996,6 +999,14 @@ bool ilu0_set_wavefront(Ctx& c, Ilu0& f, int64_t ngroup, int64_t nline, int64_t 
             }
         return false;
     };
+    if (w2) {
+        if (!build(false, glo, *lo)) return true;  // template sweeps for both
+        f.wf_lo = std::move(lo);
+        wf2_drop_lower(f);
+        wf_gather(c, f);
+        PD_CUDA(cudaStreamSynchronize(c.stream));
+        return true;
+    }
     if (!build(false, glo, *lo) || !build(true, ngroup, *up)) return false;
     f.wf_lo = std::move(lo);
     f.wf_up = std::move(up);
@@ -1008,6 +1019,7 @@ void wf_gather(Ctx& c, Ilu0& f) {
     if (!f.wf_lo) return;
     const Csr& P = f.pat();
     for (int upper = 0; upper < 2; ++upper) {
+        if (upper && !f.wf_up) continue;
         WfPlan& p = upper ? *f.wf_up : *f.wf_lo;
         const int g = c.grid_for(p.nslot, 256);
         double* blobd = reinterpret_cast<double*>(p.blob.p);
@@ -1086,6 +1098,14 @@ static void launch_sweep(Ctx& c, WfPlan& p, const double* b, double* y, unsigned
         launch_sweep_ng<UPPER, kNgFine>(c, p, b, y, ctr, guard, want);
     else
         launch_sweep_ng<UPPER, kNgWide>(c, p, b, y, ctr, guard, want);
+}
+
+void wf_solve_lower(Ctx& c, Ilu0& f, const double* b, const int* guard, int want) {
+    WfPlan& lo = *f.wf_lo;
+    if (lo.ng > 0) arm_pending(c, f.scratch.p, f.n, guard, want);
+    launch(k_wf_begin, 1, 1, 0, c.stream, f.counter.p, guard, want);
+    launch_sweep<false>(c, lo, b, f.scratch.p, f.counter.p, guard, want);
+    PD_LAUNCH_CHECK();
 }
 
 void wf_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int want) {

@@ -714,10 +714,24 @@ bool w2_disabled() {
 
 }  // namespace
 
+bool wf2_lower_preferred(const Ilu0& f) {
+    // measured on C2 (scripts/wf2_probe.py): the template lower sweep wins on the
+    // Galerkin levels (3x3 coupling to the previous step); on the fine level the
+    // pattern-table lower sweep is faster (its one-point time coupling pipelines
+    // with a shorter lag).  PD_WF2_LOWER=all|none overrides.
+    const char* e = getenv("PD_WF2_LOWER");
+    if (e && !strcmp(e, "all")) return true;
+    if (e && !strcmp(e, "none")) return false;
+    return f.w2_lo && f.w2_lo->kind == kGal9;
+}
+
+void wf2_drop_lower(Ilu0& f) { f.w2_lo.reset(); }
+
 void wf2_gather(Ctx& c, Ilu0& f) {
-    if (!f.w2_lo) return;
+    if (!f.w2_up) return;
     const Csr& P = f.pat();
     for (int upper = 0; upper < 2; ++upper) {
+        if (!upper && !f.w2_lo) continue;
         Wf2Plan& p = upper ? *f.w2_up : *f.w2_lo;
         const int g = c.grid_for(p.n, 256);
         if (upper)
@@ -788,6 +802,16 @@ static void w2_trace_report(Ctx& c, Wf2Plan& p, const char* name) {
             "pending hits %.1f, start wait %.0f clk\n",
             name, p.NL, p.NS, p.ntask, (t1 - t0) * 1e-3, dur / n * 1e-3, dur / n / p.NS, st / n,
             sb / n, sp / n, st / n / p.NS, sb / n / p.NS, sp / n / p.NS, hits / n, pro / n);
+}
+
+void wf2_solve_upper(Ctx& c, Ilu0& f, double* x, const int* guard, int want) {
+    Wf2Plan& up = *f.w2_up;
+    static const bool trace = getenv("PD_WF2_TRACE") != nullptr;
+    if (trace && !up.trace.p) up.trace.alloc(5 * (size_t)up.ntask);
+    launch(k_wf2_begin, 1, 256, 0, c.stream, f.counter.p, up.prog.p, up.ntask, guard, want);
+    w2_call(up, false, &c, f.scratch.p, x, f.counter.p, guard, want);
+    PD_LAUNCH_CHECK();
+    if (trace) w2_trace_report(c, up, "upper");
 }
 
 void wf2_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, int want) {

@@ -120,9 +120,11 @@ def test_pfasst_monodomain_implicit_newton_node_solves(golden):
     assert per_node_rel(x, g["mono_implicit_x"], (16, 2, 65)) < 1e-9
 
 
-def test_c2_small_pfasst_reference_gmres_node_solves(golden, monkeypatch):
-    """Node solves by the reference's own ILU(0)-GMRES(30) on device (pfasst.py:118-132)."""
-    monkeypatch.setenv("PD_NODE_SOLVER", "gmres")
+@pytest.mark.parametrize("solver", ["gmres", "spectral", "dense"])
+def test_c2_small_pfasst_node_solvers(golden, monkeypatch, solver):
+    """Node solves by the reference's own ILU(0)-GMRES(30) on device (pfasst.py:118-132,
+    the default), and the exact alternatives (tensor-product eigen-solve, dense LU)."""
+    monkeypatch.setenv("PD_NODE_SOLVER", solver)
     g = golden("c2_small")
     spec = pd.StencilSpec(2, 15, "dirichlet", 1.0)
     ops = pd.fd_space(spec)

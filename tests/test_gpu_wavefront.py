@@ -30,7 +30,7 @@ def _check(A, ngroup, nline, npoint, parts, seed=0, repeats=2, applies=True, ngr
     dev = pd.BlockJacobiPrecond(A, parts) if parts > 1 else pd.Ilu0(A)
     assert dev.set_wavefront(ngroup, nline, npoint, ngroup_lower) == applies
     if kind is not None:
-        assert dev.sweep_kind() == kind
+        assert dev.sweep_kind() in (kind if isinstance(kind, tuple) else (kind,))
     ref = O.OBlockJacobi(A, parts) if parts > 1 else O.OIlu0(A)
     for _ in range(repeats):  # repeated solves exercise the re-arming protocol
         b = rng.standard_normal(A.shape[0])
@@ -156,9 +156,18 @@ def test_grid_spmv_galerkin_levels_bitwise(monkeypatch):
 @pytest.mark.parametrize("n,parts", [(15, 1), (31, 2), (63, 4), (127, 8)])
 def test_wf2_fine_level_bitwise(n, parts):
     """Fine level (5-point x M x M, point coupling to the previous step), every
-    line-block size class (NLP 32/64/128): kind 2, bitwise the numba reference."""
+    line-block size class (NLP 32/64/128): template upper sweep with the pattern-table
+    lower sweep (kind 3, the default on FINE5 levels) and both template sweeps (kind 2,
+    PD_WF2_LOWER=all), bitwise the numba reference."""
     cfg, s = _system("C2", n, 8)
-    _check(s.global_matrix(), cfg.M, n, n, parts, seed=n, kind=2)
+    _check(s.global_matrix(), cfg.M, n, n, parts, seed=n, kind=3)
+
+
+@pytest.mark.parametrize("n,parts", [(15, 1), (63, 4), (127, 8)])
+def test_wf2_fine_level_template_lower_bitwise(monkeypatch, n, parts):
+    monkeypatch.setenv("PD_WF2_LOWER", "all")
+    cfg, s = _system("C2", n, 8)
+    _check(s.global_matrix(), cfg.M, n, n, parts, seed=n + 1, kind=2)
 
 
 @pytest.mark.parametrize("n,parts", [(31, 1), (63, 2), (127, 8)])
@@ -168,7 +177,7 @@ def test_wf2_galerkin_levels_bitwise(n, parts):
     h = pd.build_hierarchy(s, "SMG", 3, 2, partitions=parts)
     spec = cfg.spec
     for l, A in enumerate(h.matrices[:-1]):
-        _check(A, cfg.M, spec.n, spec.n, parts, seed=l, kind=2)
+        _check(A, cfg.M, spec.n, spec.n, parts, seed=l, kind=3 if l == 0 else 2)
         spec = spec.coarse()
 
 
@@ -182,11 +191,11 @@ def test_wf2_equals_pattern_table_executor(monkeypatch):
         A = pd.linalg.as_csr(A)
         b = rng.standard_normal(A.shape[0])
         outs = []
-        for flag, kind in (("1", 2), ("0", 1)):
+        for flag, kinds in (("1", (2, 3)), ("0", (1,))):
             monkeypatch.setenv("PD_WF2", flag)
             dev = pd.BlockJacobiPrecond(A, 8)
             assert dev.set_wavefront(cfg.M, spec.n, spec.n)
-            assert dev.sweep_kind() == kind
+            assert dev.sweep_kind() in kinds
             outs.append(dev.solve(b))
         np.testing.assert_array_equal(outs[0], outs[1])
         spec = spec.coarse()
@@ -197,7 +206,7 @@ def test_wf2_refactor_refreshes_values():
     cfg, s = _system("C2", 31, 4)
     A = pd.linalg.as_csr(s.global_matrix())
     dev = pd.BlockJacobiPrecond(A, 2)
-    assert dev.set_wavefront(cfg.M, 31, 31) and dev.sweep_kind() == 2
+    assert dev.set_wavefront(cfg.M, 31, 31) and dev.sweep_kind() in (2, 3)
     A2 = A.copy()
     A2.data = A2.data * (1.0 + 0.01 * np.random.default_rng(2).standard_normal(A2.nnz))
     dev.update_values(A2)
