@@ -189,16 +189,52 @@ int pd_pfast_create(void *ctx, int dim, int64_t n, int bc_periodic, double kappa
                     int64_t nt, double dt, const double *Kq, const double *Mq, const double *l0,
                     int levels, int nu, int coarse_sweeps, double omega_s, double omega_t,
                     void **plan_out); /* Kq, Mq (M x M row-major), l0 (M): host */
-int pd_pfast_residual(void *plan, const double *x, const double *b, double *r, double *norm2_dev);
-int pd_pfast_sweep(void *plan, const double *b, double *x);
-int pd_pfast_solve(void *plan, const double *b, double *x, double tol_rel, double tol_abs,
-                   int max_sweeps, pd_solve_report *report, double *hist /* host, optional */);
-/* Time-slab sharding: the plan's steps are one rank's slab; `halo` (device, n^d
- * doubles, or NULL for the first slab) is the previous slab's x[last step,
- * M-1], used by the residual of the first step.  The pointer is read at every
- * later residual/sweep/solve call (the caller refreshes its contents). */
-int pd_pfast_set_halo(void *plan, const double *halo);
+/* halo (device, n^d doubles, or NULL): time-slab sharding — the plan's steps are one
+ * rank's slab and `halo` is the previous slab's x[last step, M-1], coupled to the first
+ * step by the residual.  Passed per call; the library keeps no pointer to it. */
+int pd_pfast_residual(void *plan, const double *x, const double *b, double *r, const double *halo,
+                      double *norm2_dev);
+int pd_pfast_sweep(void *plan, const double *b, double *x, const double *halo);
+int pd_pfast_solve(void *plan, const double *b, double *x, const double *halo, double tol_rel,
+                   double tol_abs, int max_sweeps, pd_solve_report *report,
+                   double *hist /* host, optional */);
+/* Newton pieces (spacetime.py:126-151): out = rhs - L u - gamma (I (x) Mqh) r(u) = -F(u)
+ * (kind 0: cubic u^3-u, spacetime.py:44-50; 1: Fisher u^2-u), and the linearisation
+ * state W = gamma dt h^d r'(u) that turns L into J = L + gamma (I (x) Mqh) diag(r'(u))
+ * in every later residual/sweep/solve (NULL u: back to L).  set_state synchronises. */
+int pd_pfast_nl_residual(void *plan, const double *u, const double *rhs, double *out,
+                         const double *halo, double gamma, int kind, double *norm2_dev);
+int pd_pfast_set_state(void *plan, const double *u, double gamma, int kind);
 int pd_pfast_destroy(void *plan);
+
+/* ---- P-fast STMG: the space-time V(nu_t, nu_t) cycle around that smoother (north_star
+ *      subsystem 2: "space-time coarsening and interpolation").  Level l: nt[l] =
+ *      nt[0]/2^l steps of dt[l] = 2^l dt[0] on an n[l]^d grid (n[l+1] = n[l] or its 2:1
+ *      coarsening; schedule = multigrid.py:148-157's STMG rule with space coarsened
+ *      only while kappa dt/h^2 allows it, built by pfast.st_schedule); rediscretised
+ *      operators; time transfers P1/P2 (M x M, host): the coarse element's collocation
+ *      polynomial at the first/second fine element's nodes, restriction = transpose;
+ *      E/half: fine cardinal values at the coarse nodes (weights).  The coarsest level
+ *      runs coarse_t_sweeps undamped sweeps.  Parity: oracle/pfast_oracle.py. -- */
+int pd_pfast_st_create(void *ctx, int dim, int bc_periodic, double kappa, int M, const double *Kq,
+                       const double *Mq, const double *l0, int nlevels, const int64_t *nt,
+                       const int64_t *n, const double *dt, const int *space_levels,
+                       const double *P1, const double *P2, const double *E, const int *half,
+                       int nu_t, int coarse_t_sweeps, int nu, int coarse_sweeps, double omega_s,
+                       double omega_t, void **st_out);
+int pd_pfast_st_destroy(void *st);
+int pd_pfast_st_set_state(void *st, const double *u, double gamma, int kind); /* synchronising */
+int pd_pfast_st_cycle(void *st, const double *b, double *x);
+int pd_pfast_st_solve(void *st, const double *b, double *x, double tol_rel, double tol_abs,
+                      int max_cycles, pd_solve_report *report, double *hist /* host, optional */);
+/* level primitives for the time-slab sharded cycle (pfast.StmgSlab drives them; b / x
+ * NULL select the level's own vectors on levels >= 1; halo as above, per level) */
+int pd_pfast_st_level_plan(void *st, int level, void **plan_out); /* borrowed smoother */
+int pd_pfast_st_level_sweep(void *st, int level, const double *b, double *x, const double *halo);
+int pd_pfast_st_level_restrict(void *st, int level, const double *b, const double *x,
+                               const double *halo);
+int pd_pfast_st_level_prolong(void *st, int level, double *x);
+int pd_pfast_st_level_last(void *st, int level, const double *x, double *out);
 
 #ifdef __cplusplus
 }

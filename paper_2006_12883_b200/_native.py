@@ -70,10 +70,25 @@ _SIGNATURES = {
     "pd_mg_destroy": (_int, [_vp]),
     "pd_pfast_create": (_int, [_vp, _int, _i64, _int, _dbl, _int, _i64, _dbl, _vp, _vp, _vp,
                                _int, _int, _int, _dbl, _dbl, ctypes.POINTER(_vp)]),
-    "pd_pfast_residual": (_int, [_vp, _vp, _vp, _vp, _vp]),
-    "pd_pfast_sweep": (_int, [_vp, _vp, _vp]),
-    "pd_pfast_solve": (_int, [_vp, _vp, _vp, _dbl, _dbl, _int, ctypes.POINTER(SolveReportC), _vp]),
-    "pd_pfast_set_halo": (_int, [_vp, _vp]),
+    "pd_pfast_residual": (_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "pd_pfast_sweep": (_int, [_vp, _vp, _vp, _vp]),
+    "pd_pfast_solve": (_int, [_vp, _vp, _vp, _vp, _dbl, _dbl, _int, ctypes.POINTER(SolveReportC),
+                              _vp]),
+    "pd_pfast_nl_residual": (_int, [_vp, _vp, _vp, _vp, _vp, _dbl, _int, _vp]),
+    "pd_pfast_set_state": (_int, [_vp, _vp, _dbl, _int]),
+    "pd_pfast_st_create": (_int, [_vp, _int, _int, _dbl, _int, _vp, _vp, _vp, _int, _vp, _vp, _vp,
+                                  _vp, _vp, _vp, _vp, _vp, _int, _int, _int, _int, _dbl, _dbl,
+                                  ctypes.POINTER(_vp)]),
+    "pd_pfast_st_destroy": (_int, [_vp]),
+    "pd_pfast_st_set_state": (_int, [_vp, _vp, _dbl, _int]),
+    "pd_pfast_st_cycle": (_int, [_vp, _vp, _vp]),
+    "pd_pfast_st_solve": (_int, [_vp, _vp, _vp, _dbl, _dbl, _int, ctypes.POINTER(SolveReportC),
+                                 _vp]),
+    "pd_pfast_st_level_plan": (_int, [_vp, _int, ctypes.POINTER(_vp)]),
+    "pd_pfast_st_level_sweep": (_int, [_vp, _int, _vp, _vp, _vp]),
+    "pd_pfast_st_level_restrict": (_int, [_vp, _int, _vp, _vp, _vp]),
+    "pd_pfast_st_level_prolong": (_int, [_vp, _int, _vp]),
+    "pd_pfast_st_level_last": (_int, [_vp, _int, _vp, _vp]),
     "pd_pfast_destroy": (_int, [_vp]),
     "pd_mg_set_fine_operator": (_int, [_vp, _vp]),
     "pd_mg_set_galerkin_intermediates": (_int, [_vp, _int, _vp]),

@@ -16,6 +16,15 @@
 // There is no reference counterpart; parity is against the CPU restatement in
 // oracle/pfast_oracle.py.
 //
+// Round 2: (a) the Newton linearisation J = L + γ(I⊗Mqh)diag(r'(u))
+// (spacetime.py:126-129,144-151) enters the point blocks through a per-point
+// weight array W = γ·dt·h^d·r'(u) (NL kernels: block = Ac(I + G·diag(w)), G = Ac⁻¹Mq,
+// solved per point in registers) and MODE 5 evaluates the nonlinear residual
+// (spacetime.py:131-142); (b) `PfastSt`: the space-time V-cycle around the
+// smoother — time halved on every level, space while μ = κ·dt/h² allows it
+// (schedule built by the host, pfast.st_schedule), rediscretised operators,
+// time transfers = the coarse element's polynomial at the fine elements' nodes.
+//
 // Layout: (nt, M, n^d) C-order fp64, the last grid axis fastest — the layout
 // of every other kernel of the library.  Every kernel is one pass over HBM
 // with the neighbour planes served from L1/L2 (algorithmic bytes in DESIGN §4).
@@ -40,7 +49,58 @@ struct PfCoef {  // one level's point-block operator (row-major M×M each)
     double Dinv[kPfMaxM * kPfMaxM];  // ω·Ac⁻¹
     double cprev[kPfMaxM];           // −l0[m]·h^d (level 0 time coupling)
     double omega_t;                  // outer damping (MODE 4)
+    double Ainv[kPfMaxM * kPfMaxM];  // Ac⁻¹ (NL: first half of the block solve)
+    double G[kPfMaxM * kPfMaxM];     // Ac⁻¹·Mq (NL: block = Ac(I + G·diag(w)))
+    double Mq[kPfMaxM * kPfMaxM];    // NL apply / MODE 5: Σ_k Mq[m,k]·(w_k x_k | r(x_k))
+    double omega_s;                  // spatial damping (NL)
+    double rs;                       // MODE 5: γ·dt·h^d
+    int kind;                        // MODE 5: 0 cubic u³−u, 1 Fisher u²−u
 };
+
+struct PfTime {  // time transfers between space-time levels (row-major M×M)
+    double P1[kPfMaxM * kPfMaxM];  // coarse polynomial at the first fine element's nodes
+    double P2[kPfMaxM * kPfMaxM];  // ... at the second fine element's nodes
+    double E[kPfMaxM * kPfMaxM];   // fine cardinal values at coarse node m
+    int half[kPfMaxM];             // coarse node m lies in fine element 2tc + half[m]
+};
+
+// d = ω_s (I + G diag(w))⁻¹ Ac⁻¹ r: unrolled elimination without pivoting (the host
+// checks ‖G‖∞·max|w| < 1, so the matrix is strictly diagonally dominant)
+template <int M>
+__device__ __forceinline__ void nl_block_solve(const PfCoef& C, const double (&w)[M],
+                                               const double (&r)[M], double (&d)[M]) {
+    double B[M][M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            acc = fma(C.Ainv[m * M + k], r[k], acc);
+            B[m][k] = fma(C.G[m * M + k], w[k], m == k ? 1.0 : 0.0);
+        }
+        d[m] = acc;
+    }
+#pragma unroll
+    for (int c = 0; c < M; ++c) {
+        const double inv = 1.0 / B[c][c];
+#pragma unroll
+        for (int i = c + 1; i < M; ++i) {
+            const double f = B[i][c] * inv;
+#pragma unroll
+            for (int k = c + 1; k < M; ++k) B[i][k] = fma(-f, B[c][k], B[i][k]);
+            d[i] = fma(-f, d[c], d[i]);
+        }
+    }
+#pragma unroll
+    for (int c = M - 1; c >= 0; --c) {
+        double acc = d[c];
+#pragma unroll
+        for (int k = c + 1; k < M; ++k) acc = fma(-B[c][k], d[k], acc);
+        d[c] = acc / B[c][c];
+    }
+#pragma unroll
+    for (int m = 0; m < M; ++m) d[m] *= C.omega_s;
+}
 
 // per-axis neighbour of coordinate v (−1 = outside a Dirichlet grid)
 template <bool PER>
@@ -56,11 +116,14 @@ __device__ __forceinline__ int nb(int v, int d, int n) {
 // MODE 3: out = b − A x − cprev·x[t-1, M-1]  (space-time residual, level 0;
 //         at t = 0 the coupling uses `halo` when non-null)
 // MODE 4: out += ω_t (x + Dinv(b − A x))  (MODE 0 fused with the outer update)
-template <int DIM, int M, int MODE, bool PER>
+// MODE 5: out = b − A x − cprev·x[t-1, M-1] − rs·Mq r(x)  (nonlinear residual −F(x))
+// NL: A and the point block carry the linearisation weights W (same layout as x)
+template <int DIM, int M, int MODE, bool PER, bool NL>
 __global__ void __launch_bounds__(PFB) k_pf_point(PfCoef C, int n, int64_t nt,
                                                  const double* __restrict__ x,
                                                  const double* __restrict__ b, double* out,
-                                                 const double* __restrict__ halo) {
+                                                 const double* __restrict__ halo,
+                                                 const double* __restrict__ W) {
     // one warp per (step, grid row, 32-point x tile): 32-bit index math only
     const unsigned nn = (unsigned)n;
     const unsigned R = DIM == 2 ? nn : nn * nn;  // rows per step
@@ -81,7 +144,19 @@ __global__ void __launch_bounds__(PFB) k_pf_point(PfCoef C, int n, int64_t nt,
         double bv[M];
 #pragma unroll
         for (int m = 0; m < M; ++m) bv[m] = b[base + m * S];
+        double wv[M];
+        if (NL) {
+#pragma unroll
+            for (int m = 0; m < M; ++m) wv[m] = W[base + m * S];
+        }
         if (MODE == 1) {
+            if (NL) {
+                double d[M];
+                nl_block_solve<M>(C, wv, bv, d);
+#pragma unroll
+                for (int m = 0; m < M; ++m) out[base + m * S] = d[m];
+                continue;
+            }
 #pragma unroll
             for (int m = 0; m < M; ++m) {
                 double acc = 0.0;
@@ -127,25 +202,45 @@ __global__ void __launch_bounds__(PFB) k_pf_point(PfCoef C, int n, int64_t nt,
             for (int k = 0; k < M; ++k) {
                 ax = fma(C.Ac[m * M + k], xc[k], ax);
                 ax = fma(C.Ao[m * M + k], ns[k], ax);
+                if (NL) ax = fma(C.Mq[m * M + k], wv[k] * xc[k], ax);
             }
             r[m] = bv[m] - ax;
         }
-        if (MODE == 3 && (t > 0 || halo)) {
+        if (MODE == 5) {
+            double rx[M];
+#pragma unroll
+            for (int k = 0; k < M; ++k)
+                rx[k] = C.kind == 0 ? xc[k] * xc[k] * xc[k] - xc[k] : xc[k] * xc[k] - xc[k];
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < M; ++k) acc = fma(C.Mq[m * M + k], rx[k], acc);
+                r[m] = fma(-C.rs, acc, r[m]);
+            }
+        }
+        if ((MODE == 3 || MODE == 5) && (t > 0 || halo)) {
             // x[t-1, M-1, j]; the first step of a time slab reads the previous
             // slab's last node (halo) when the steps are sharded over ranks
             const double xp = t > 0 ? x[base - S] : halo[j];
 #pragma unroll
             for (int m = 0; m < M; ++m) r[m] = fma(-C.cprev[m], xp, r[m]);
         }
-        if (MODE == 2 || MODE == 3) {
+        if (MODE == 2 || MODE == 3 || MODE == 5) {
 #pragma unroll
             for (int m = 0; m < M; ++m) out[base + m * S] = r[m];
         } else {
+            double d[M];
+            if (NL) nl_block_solve<M>(C, wv, r, d);
 #pragma unroll
             for (int m = 0; m < M; ++m) {
                 double acc = xc[m];
+                if (NL) {
+                    acc += d[m];
+                } else {
 #pragma unroll
-                for (int k = 0; k < M; ++k) acc = fma(C.Dinv[m * M + k], r[k], acc);
+                    for (int k = 0; k < M; ++k) acc = fma(C.Dinv[m * M + k], r[k], acc);
+                }
                 if (MODE == 4)  // last level-0 sweep: straight into the solution
                     out[base + m * S] = fma(C.omega_t, acc, out[base + m * S]);
                 else
@@ -301,6 +396,92 @@ __global__ void __launch_bounds__(PFB) k_pf_axpy(int64_t n, double a, const doub
         x[i] = fma(a, e[i], x[i]);
 }
 
+// W = rs·r'(u) (linearisation weights, spacetime.py:48-50,126-129) and max|W|
+// (bit pattern of a non-negative double orders like an unsigned integer)
+__global__ void __launch_bounds__(PFB) k_pf_weights(int64_t n, double rs, int kind,
+                                                   const double* __restrict__ u, double* W,
+                                                   unsigned long long* wmax) {
+    double mx = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)PFB + threadIdx.x; i < n; i += (int64_t)gridDim.x * PFB) {
+        const double v = u[i];
+        const double w = rs * (kind == 0 ? fma(3.0 * v, v, -1.0) : fma(2.0, v, -1.0));
+        W[i] = w;
+        mx = fmax(mx, fabs(w));
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx > 0.0) atomicMax(wmax, (unsigned long long)__double_as_longlong(mx));
+}
+
+__global__ void __launch_bounds__(PFB) k_pf_absmax(int64_t n, const double* __restrict__ w,
+                                                  unsigned long long* wmax) {
+    double mx = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)PFB + threadIdx.x; i < n; i += (int64_t)gridDim.x * PFB)
+        mx = fmax(mx, fabs(w[i]));
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0 && mx > 0.0) atomicMax(wmax, (unsigned long long)__double_as_longlong(mx));
+}
+
+// Time transfers between space-time levels; vectors (nt, M, S), one thread per
+// (coarse step, point).
+// KIND 0 (residual restriction):  out[tc,m] = Σ_k P1[k,m]·in[2tc,k] + P2[k,m]·in[2tc+1,k]
+// KIND 1 (weights):               out[tc,m] = 2 Σ_k E[m,k]·in[2tc+half[m],k]
+template <int M, int KIND>
+__global__ void __launch_bounds__(PFB) k_pf_tcombine(PfTime T, int64_t ntc, int64_t S,
+                                                    const double* __restrict__ in, double* out) {
+    const int64_t total = ntc * S;
+    for (int64_t i = blockIdx.x * (int64_t)PFB + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * PFB) {
+        const int64_t tc = i / S, j = i - tc * S;
+        double a[M], c[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            a[k] = in[((2 * tc) * M + k) * S + j];
+            c[k] = in[((2 * tc + 1) * M + k) * S + j];
+        }
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            double acc = 0.0;
+            if (KIND == 0) {
+#pragma unroll
+                for (int k = 0; k < M; ++k) acc = fma(T.P1[k * M + m], a[k], acc);
+#pragma unroll
+                for (int k = 0; k < M; ++k) acc = fma(T.P2[k * M + m], c[k], acc);
+            } else {
+#pragma unroll
+                for (int k = 0; k < M; ++k) acc = fma(T.E[m * M + k], T.half[m] ? c[k] : a[k], acc);
+                acc *= 2.0;
+            }
+            out[(tc * M + m) * S + j] = acc;
+        }
+    }
+}
+
+// prolongation in time: fine[2tc+s, m] (+)= Σ_k P{s}[m,k]·coarse[tc,k], s = 0, 1
+template <int M, bool ADD>
+__global__ void __launch_bounds__(PFB) k_pf_texpand(PfTime T, int64_t ntc, int64_t S,
+                                                   const double* __restrict__ coarse,
+                                                   double* fine) {
+    const int64_t total = ntc * S;
+    for (int64_t i = blockIdx.x * (int64_t)PFB + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * PFB) {
+        const int64_t tc = i / S, j = i - tc * S;
+        double e[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) e[k] = coarse[(tc * M + k) * S + j];
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < M; ++k)
+                    acc = fma(s ? T.P2[m * M + k] : T.P1[m * M + k], e[k], acc);
+                double* dst = fine + ((2 * tc + s) * M + m) * S + j;
+                *dst = ADD ? *dst + acc : acc;
+            }
+    }
+}
+
 // deterministic two-pass |v|^2 (fixed grid, fixed partial order)
 __global__ void __launch_bounds__(PFB) k_pf_norm_part(int64_t n, const double* __restrict__ v,
                                                      double* part) {
@@ -361,18 +542,21 @@ struct PfastPlan {
     int dim, M, levels, nu, coarse_sweeps;
     bool periodic;
     int64_t nt;
-    double omega_t;
+    double omega_t, dt, kappa, ginf = 0.0;  // ginf = ‖Ac⁻¹Mq‖∞ of level 0
     std::vector<int> n;            // grid points per axis per level
     std::vector<int64_t> len;      // nt·M·n^d per level
     std::vector<PfCoef> coef;
     std::vector<DevBuf<double>> B, E, T;  // level rhs, iterate, ping-pong
+    std::vector<DevBuf<double>> W;        // linearisation weights per level (lazily allocated)
+    bool nl = false;                      // weights active
     DevBuf<double> part, norm;
+    DevBuf<unsigned long long> wmax;
     double* pinned = nullptr;
-    const double* halo = nullptr;  // previous slab's last node (sharded steps)
     PfastPlan(Ctx& c_) : c(c_) {}
     ~PfastPlan() {
         if (pinned) cudaFreeHost(pinned);
     }
+    int64_t S(int l) const { return dim == 2 ? (int64_t)n[l] * n[l] : (int64_t)n[l] * n[l] * n[l]; }
 };
 
 namespace {
@@ -381,40 +565,49 @@ namespace {
 // with only 6 resident per SM left a second, mostly empty wave (ncu: achieved
 // occupancy 52% of a theoretical 75%).
 template <class K>
-int one_wave(const PfastPlan& P, K kernel, int64_t threads) {
+int one_wave(Ctx& c, K kernel, int64_t threads) {
     int occ = 0;
     PD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, PFB, 0));
     static const int cap = getenv("PD_PF_BLOCKS") ? atoi(getenv("PD_PF_BLOCKS")) : 0;
     if (cap > 0) occ = std::min(occ, cap);  // probe knob: fewer resident rows per SM
-    return P.c.grid_for(threads, PFB, std::max(occ, 1));
+    return c.grid_for(threads, PFB, std::max(occ, 1));
 }
 
-template <int DIM, int M, bool PER>
-void launch_point(PfastPlan& P, int l, int mode, const double* x, const double* b, double* out) {
+template <int DIM, int M, bool PER, bool NL>
+void launch_point(PfastPlan& P, int l, int mode, const double* x, const double* b, double* out,
+                  const double* halo) {
     const int64_t nl = P.n[l];
     const int64_t rows = P.nt * (P.dim == 2 ? nl : nl * nl);
     const int64_t threads = rows * ((nl + 31) / 32) * 32;
     const PfCoef& C = P.coef[l];
-    auto go = [&](auto kernel, const double* halo) {
-        launch(kernel, one_wave(P, kernel, threads), PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out,
-               halo);
+    const double* W = NL ? P.W[l].p : nullptr;
+    auto go = [&](auto kernel, const double* h) {
+        launch(kernel, one_wave(P.c, kernel, threads), PFB, 0, P.c.stream, C, P.n[l], P.nt, x, b, out,
+               h, W);
     };
     switch (mode) {
-        case 0: go(k_pf_point<DIM, M, 0, PER>, nullptr); break;
-        case 1: go(k_pf_point<DIM, M, 1, PER>, nullptr); break;
-        case 2: go(k_pf_point<DIM, M, 2, PER>, nullptr); break;
-        case 4: go(k_pf_point<DIM, M, 4, PER>, nullptr); break;
-        default: go(k_pf_point<DIM, M, 3, PER>, P.halo);
+        case 0: go(k_pf_point<DIM, M, 0, PER, NL>, nullptr); break;
+        case 1: go(k_pf_point<DIM, M, 1, PER, NL>, nullptr); break;
+        case 2: go(k_pf_point<DIM, M, 2, PER, NL>, nullptr); break;
+        case 4: go(k_pf_point<DIM, M, 4, PER, NL>, nullptr); break;
+        case 5:
+            if constexpr (!NL) go(k_pf_point<DIM, M, 5, PER, false>, halo);
+            break;
+        default: go(k_pf_point<DIM, M, 3, PER, NL>, halo);
     }
     PD_LAUNCH_CHECK();
 }
 
+// mode 5 (nonlinear residual) never uses the weights
 template <int DIM, int M, bool PER>
-void point_op(PfastPlan& P, int l, int mode, const double* x, const double* b, double* out) {
-    launch_point<DIM, M, PER>(P, l, mode, x, b, out);
+void point_op(PfastPlan& P, int l, int mode, const double* x, const double* b, double* out,
+              const double* halo) {
+    if (P.nl && mode != 5) launch_point<DIM, M, PER, true>(P, l, mode, x, b, out, halo);
+    else launch_point<DIM, M, PER, false>(P, l, mode, x, b, out, halo);
 }
 
-using PointFn = void (*)(PfastPlan&, int, int, const double*, const double*, double*);
+using PointFn = void (*)(PfastPlan&, int, int, const double*, const double*, double*,
+                         const double*);
 
 template <int DIM, bool PER>
 PointFn pick_m(int M) {
@@ -432,32 +625,46 @@ PointFn pick(const PfastPlan& P) {
     return P.periodic ? pick_m<3, true>(P.M) : pick_m<3, false>(P.M);
 }
 
-void restrict_to(PfastPlan& P, int l, const double* fine, double* coarse) {
-    const int64_t planes = P.nt * P.M;
-    const int nc = P.n[l + 1], nf = P.n[l];
-    const int64_t rows = planes * (P.dim == 2 ? nc : (int64_t)nc * nc);
-    if (P.dim == 2) {
-        if (P.periodic) launch(k_pf_restrict<2, true>, one_wave(P, k_pf_restrict<2, true>, rows * 32), PFB, 0, P.c.stream, nc, nf, planes, fine, coarse);
-        else launch(k_pf_restrict<2, false>, one_wave(P, k_pf_restrict<2, false>, rows * 32), PFB, 0, P.c.stream, nc, nf, planes, fine, coarse);
+// coarse = Pᵀ fine over `planes` grids (nf → nc points per axis)
+void restrict_planes(Ctx& c, int dim, bool periodic, int nc, int nf, int64_t planes,
+                     const double* fine, double* coarse) {
+    const int64_t rows = planes * (dim == 2 ? nc : (int64_t)nc * nc);
+    auto go = [&](auto kernel) {
+        launch(kernel, one_wave(c, kernel, rows * 32), PFB, 0, c.stream, nc, nf, planes, fine, coarse);
+    };
+    if (dim == 2) {
+        if (periodic) go(k_pf_restrict<2, true>);
+        else go(k_pf_restrict<2, false>);
     } else {
-        if (P.periodic) launch(k_pf_restrict<3, true>, one_wave(P, k_pf_restrict<3, true>, rows * 32), PFB, 0, P.c.stream, nc, nf, planes, fine, coarse);
-        else launch(k_pf_restrict<3, false>, one_wave(P, k_pf_restrict<3, false>, rows * 32), PFB, 0, P.c.stream, nc, nf, planes, fine, coarse);
+        if (periodic) go(k_pf_restrict<3, true>);
+        else go(k_pf_restrict<3, false>);
     }
     PD_LAUNCH_CHECK();
 }
 
-void prolong_add(PfastPlan& P, int l, const double* coarse, double* fine) {
-    const int64_t planes = P.nt * P.M;
-    const int nc = P.n[l + 1], nf = P.n[l];
-    const int64_t rows = planes * (P.dim == 2 ? nf : (int64_t)nf * nf);
-    if (P.dim == 2) {
-        if (P.periodic) launch(k_pf_prolong_add<2, true>, one_wave(P, k_pf_prolong_add<2, true>, rows * 32), PFB, 0, P.c.stream, nc, nf, planes, coarse, fine);
-        else launch(k_pf_prolong_add<2, false>, one_wave(P, k_pf_prolong_add<2, false>, rows * 32), PFB, 0, P.c.stream, nc, nf, planes, coarse, fine);
+// fine += P coarse over `planes` grids
+void prolong_add_planes(Ctx& c, int dim, bool periodic, int nc, int nf, int64_t planes,
+                        const double* coarse, double* fine) {
+    const int64_t rows = planes * (dim == 2 ? nf : (int64_t)nf * nf);
+    auto go = [&](auto kernel) {
+        launch(kernel, one_wave(c, kernel, rows * 32), PFB, 0, c.stream, nc, nf, planes, coarse, fine);
+    };
+    if (dim == 2) {
+        if (periodic) go(k_pf_prolong_add<2, true>);
+        else go(k_pf_prolong_add<2, false>);
     } else {
-        if (P.periodic) launch(k_pf_prolong_add<3, true>, one_wave(P, k_pf_prolong_add<3, true>, rows * 32), PFB, 0, P.c.stream, nc, nf, planes, coarse, fine);
-        else launch(k_pf_prolong_add<3, false>, one_wave(P, k_pf_prolong_add<3, false>, rows * 32), PFB, 0, P.c.stream, nc, nf, planes, coarse, fine);
+        if (periodic) go(k_pf_prolong_add<3, true>);
+        else go(k_pf_prolong_add<3, false>);
     }
     PD_LAUNCH_CHECK();
+}
+
+void restrict_to(PfastPlan& P, int l, const double* fine, double* coarse) {
+    restrict_planes(P.c, P.dim, P.periodic, P.n[l + 1], P.n[l], P.nt * P.M, fine, coarse);
+}
+
+void prolong_add(PfastPlan& P, int l, const double* coarse, double* fine) {
+    prolong_add_planes(P.c, P.dim, P.periodic, P.n[l + 1], P.n[l], P.nt * P.M, coarse, fine);
 }
 
 // e_l ≈ A_l⁻¹ B_l from a zero guess; result in P.E[l] (T[l] is scratch).
@@ -474,12 +681,12 @@ bool vcycle(PfastPlan& P, int l, double* xupd = nullptr) {
     auto smooth = [&](int count, bool from_zero) {
         for (int s = 0; s < count; ++s) {
             if (from_zero && s == 0) {
-                op(P, l, 1, nullptr, b, e);
+                op(P, l, 1, nullptr, b, e, nullptr);
             } else if (last && xupd && s == count - 1) {
-                op(P, l, 4, e, b, xupd);
+                op(P, l, 4, e, b, xupd, nullptr);
                 fused = true;
             } else {
-                op(P, l, 0, e, b, t);
+                op(P, l, 0, e, b, t, nullptr);
                 std::swap(e, t);
             }
         }
@@ -487,7 +694,7 @@ bool vcycle(PfastPlan& P, int l, double* xupd = nullptr) {
     last = l == P.levels - 1;
     smooth(sweeps, true);
     if (l < P.levels - 1) {
-        op(P, l, 2, e, b, t);  // t = b − A e
+        op(P, l, 2, e, b, t, nullptr);  // t = b − A e
         restrict_to(P, l, t, P.B[l + 1].p);
         vcycle(P, l + 1);
         prolong_add(P, l, P.E[l + 1].p, e);
@@ -502,6 +709,272 @@ void norm2(PfastPlan& P, const double* v, int64_t n, double* out_dev) {
     launch(k_pf_norm_part, kPfNormBlocks, PFB, 0, P.c.stream, n, v, P.part.p);
     launch(k_pf_norm_final, 1, PFB, 0, P.c.stream, (const double*)P.part.p, out_dev);
     PD_LAUNCH_CHECK();
+}
+
+// x += ω_t · Vcycle(b − L x); the residual is left in B[0]
+void sweep(PfastPlan& P, const double* b, double* x, const double* halo) {
+    pick(P)(P, 0, 3, x, b, P.B[0].p, halo);
+    if (!vcycle(P, 0, x)) {
+        launch(k_pf_axpy, P.c.grid_for(P.len[0], PFB, 8), PFB, 0, P.c.stream, P.len[0], P.omega_t,
+               (const double*)P.E[0].p, x);
+        PD_LAUNCH_CHECK();
+    }
+}
+
+double read_scalar(PfastPlan& P, const double* dev) {
+    PD_CUDA(cudaMemcpyAsync(P.pinned, dev, sizeof(double), cudaMemcpyDeviceToHost, P.c.stream));
+    PD_CUDA(cudaStreamSynchronize(P.c.stream));
+    return *P.pinned;
+}
+
+// max|W[0]| of a plan (synchronising)
+double weights_absmax(PfastPlan& P) {
+    PD_CUDA(cudaMemsetAsync(P.wmax.p, 0, sizeof(unsigned long long), P.c.stream));
+    launch(k_pf_absmax, P.c.grid_for(P.len[0], PFB, 8), PFB, 0, P.c.stream, P.len[0],
+           (const double*)P.W[0].p, P.wmax.p);
+    PD_LAUNCH_CHECK();
+    static_assert(sizeof(double) == sizeof(unsigned long long), "bit copy");
+    return read_scalar(P, reinterpret_cast<const double*>(P.wmax.p));
+}
+
+void alloc_weights(PfastPlan& P) {
+    if (!P.W.empty()) return;
+    P.W.resize(P.levels);
+    for (int l = 0; l < P.levels; ++l) P.W[l].alloc(P.len[l]);
+}
+
+// W[0] is set: restrict it down the spatial levels (Pᵀ W), check the point blocks
+// stay diagonally dominant, switch the NL kernels on
+void weights_ready(PfastPlan& P) {
+    for (int l = 0; l + 1 < P.levels; ++l) restrict_to(P, l, P.W[l].p, P.W[l + 1].p);
+    const double wm = weights_absmax(P);
+    if (!(P.ginf * wm < 1.0))
+        throw ConfigError("P-fast: reaction too stiff for the point-block solve "
+                          "(|Ac^-1 Mq| max|gamma dt h^d r'(u)| >= 1); use fewer time levels");
+    P.nl = true;
+}
+
+std::unique_ptr<PfastPlan> make_plan(Ctx& c, int dim, int64_t n, int bc_periodic, double kappa, int M,
+                                     int64_t nt, double dt, const double* Kq, const double* Mq,
+                                     const double* l0, int levels, int nu, int coarse_sweeps,
+                                     double omega_s, double omega_t) {
+    if (dim != 2 && dim != 3) throw ConfigError("P-fast needs a 2D or 3D grid");
+    if (M < 1 || M > kPfMaxM) throw ConfigError("P-fast supports 1..5 nodes");
+    if (nt < 1 || n < 1) throw ConfigError("P-fast needs nt >= 1 and n >= 1");
+    if (levels < 1 || nu < 1 || coarse_sweeps < 1)
+        throw ConfigError("P-fast needs levels, nu and coarse_sweeps >= 1");
+    auto P = std::make_unique<PfastPlan>(c);
+    P->dim = dim;
+    P->M = M;
+    P->nt = nt;
+    P->dt = dt;
+    P->kappa = kappa;
+    P->levels = levels;
+    P->nu = nu;
+    P->coarse_sweeps = coarse_sweeps;
+    P->periodic = bc_periodic != 0;
+    P->omega_t = omega_t;
+    int64_t nl = n;
+    for (int l = 0; l < levels; ++l) {
+        if (l > 0) {
+            if (P->periodic) {
+                if (nl % 2 || nl < 4) throw ConfigError("cannot coarsen the periodic grid");
+                nl /= 2;
+            } else {
+                if (nl % 2 == 0 || nl < 3) throw ConfigError("cannot coarsen the Dirichlet grid");
+                nl = (nl - 1) / 2;
+            }
+        }
+        if (nl > (1 << 20)) throw ConfigError("grid too large");
+        if (nt * M * nl * (dim == 3 ? nl : 1) * ((nl + 31) / 32) >= (int64_t(1) << 31))
+            throw ConfigError("P-fast grid x steps too large for one plan");
+        P->n.push_back((int)nl);
+        int64_t S = nl * nl * (dim == 3 ? nl : 1);
+        P->len.push_back(nt * M * S);
+        // h of this level (StencilSpec.h: Dirichlet 1/(n+1), periodic 1/n)
+        const double h = P->periodic ? 1.0 / (double)nl : 1.0 / (double)(nl + 1);
+        const double mh = std::pow(h, dim);
+        const double ks = kappa * std::pow(h, dim - 2);
+        PfCoef C{};
+        double D[kPfMaxM * kPfMaxM];
+        for (int i = 0; i < M; ++i)
+            for (int k = 0; k < M; ++k) {
+                C.Ac[i * M + k] = Kq[i * M + k] * mh + dt * Mq[i * M + k] * (ks * 2.0 * dim);
+                C.Ao[i * M + k] = -dt * Mq[i * M + k] * ks;
+                C.Mq[i * M + k] = Mq[i * M + k];
+                D[i * M + k] = C.Ac[i * M + k];
+            }
+        double Di[kPfMaxM * kPfMaxM];
+        if (!invert(D, Di, M)) throw ConfigError("singular point block");
+        double ginf = 0.0;
+        for (int i = 0; i < M; ++i) {
+            double rowsum = 0.0;
+            for (int k = 0; k < M; ++k) {
+                C.Dinv[i * M + k] = omega_s * Di[i * M + k];
+                C.Ainv[i * M + k] = Di[i * M + k];
+                double g = 0.0;
+                for (int q = 0; q < M; ++q) g += Di[i * M + q] * Mq[q * M + k];
+                C.G[i * M + k] = g;
+                rowsum += std::fabs(g);
+            }
+            ginf = std::max(ginf, rowsum);
+        }
+        if (l == 0) P->ginf = ginf;
+        for (int m = 0; m < M; ++m) C.cprev[m] = -l0[m] * mh;
+        C.omega_t = omega_t;
+        C.omega_s = omega_s;
+        P->coef.push_back(C);
+    }
+    P->B.resize(levels);
+    P->E.resize(levels);
+    P->T.resize(levels);
+    for (int l = 0; l < levels; ++l) {
+        P->B[l].alloc(P->len[l]);
+        P->E[l].alloc(P->len[l]);
+        P->T[l].alloc(P->len[l]);
+    }
+    P->part.alloc(kPfNormBlocks);
+    P->norm.alloc(1);
+    P->wmax.alloc(1);
+    PD_CUDA(cudaMallocHost(&P->pinned, sizeof(double)));
+    return P;
+}
+
+// stopping / divergence rules of multigrid.py:275-305 around `step`
+template <class Resid, class Step>
+void iterate(Resid&& resid, Step&& step, double tol_rel, double tol_abs, int max_it,
+             pd_solve_report* rep, double* hist) {
+    double r = resid();
+    int it = 0, conv = 0, div = 0;
+    if (hist) hist[0] = r;
+    if (!std::isfinite(r)) {
+        div = 1;  // a non-finite residual reports divergence (multigrid.py:296-300), no throw
+    } else {
+        const double thr = std::max(tol_abs, tol_rel * r);
+        double lowest = r;
+        while (true) {
+            if (r <= thr) { conv = 1; break; }
+            if (it >= max_it) { div = 1; break; }
+            step();
+            ++it;
+            r = resid();
+            if (hist) hist[it] = r;
+            if (!std::isfinite(r)) { div = 1; break; }
+            lowest = std::min(lowest, r);
+            if (r > 10.0 * lowest) { div = 1; break; }
+        }
+    }
+    rep->iterations = it;
+    rep->converged = conv;
+    rep->diverged = div;
+    rep->hist_len = hist ? it + 1 : 0;
+}
+
+}  // namespace
+
+// Space-time multigrid around the smoother: level l has nt_l = nt_0 / 2^l steps of
+// dt_l = 2^l dt_0 on an n_l^d grid (n_{l+1} = n_l or its 2:1 coarsening).
+struct PfastSt {
+    Ctx& c;
+    int M = 0, dim = 0, nu_t = 1, coarse_t_sweeps = 1;
+    bool periodic = false;
+    PfTime T{};
+    std::vector<std::unique_ptr<PfastPlan>> sm;  // one smoother (spatial hierarchy) per level
+    std::vector<int> space;                      // space coarsened between l and l+1
+    std::vector<DevBuf<double>> X, Bv;           // level iterates / right-hand sides, l >= 1
+    explicit PfastSt(Ctx& c_) : c(c_) {}
+};
+
+namespace {
+
+template <class F>
+void for_m(int M, F&& f) {
+    switch (M) {
+        case 1: f(std::integral_constant<int, 1>{}); break;
+        case 2: f(std::integral_constant<int, 2>{}); break;
+        case 3: f(std::integral_constant<int, 3>{}); break;
+        case 4: f(std::integral_constant<int, 4>{}); break;
+        default: f(std::integral_constant<int, 5>{});
+    }
+}
+
+// in (level l layout, or already space-restricted) -> level l+1, KIND as k_pf_tcombine
+template <int KIND>
+void time_combine(PfastSt& S, int l, const double* in, double* out) {
+    PfastPlan& C = *S.sm[l + 1];
+    const int64_t Sc = C.S(0), total = C.nt * Sc;
+    for_m(S.M, [&](auto m) {
+        constexpr int MM = decltype(m)::value;
+        launch(k_pf_tcombine<MM, KIND>, S.c.grid_for(total, PFB, 8), PFB, 0, S.c.stream, S.T, C.nt, Sc,
+               in, out);
+    });
+    PD_LAUNCH_CHECK();
+}
+
+// b_{l+1} = Rt Rs r_l; r_l = the level-l smoother's B[0]; T[0] is scratch
+void st_restrict(PfastSt& S, int l, double* bc) {
+    PfastPlan& F = *S.sm[l];
+    const double* r = F.B[0].p;
+    if (S.space[l]) {
+        restrict_planes(S.c, S.dim, S.periodic, S.sm[l + 1]->n[0], F.n[0], F.nt * F.M, r, F.T[0].p);
+        r = F.T[0].p;
+    }
+    time_combine<0>(S, l, r, bc);
+}
+
+// x_l += Ps Pt e_{l+1}
+void st_prolong(PfastSt& S, int l, const double* ec, double* x) {
+    PfastPlan& F = *S.sm[l];
+    PfastPlan& C = *S.sm[l + 1];
+    const int64_t Sc = C.S(0), total = C.nt * Sc;
+    const bool sp = S.space[l] != 0;
+    double* dst = sp ? F.T[0].p : x;
+    for_m(S.M, [&](auto m) {
+        constexpr int MM = decltype(m)::value;
+        if (sp)
+            launch(k_pf_texpand<MM, false>, S.c.grid_for(total, PFB, 8), PFB, 0, S.c.stream, S.T, C.nt,
+                   Sc, ec, dst);
+        else
+            launch(k_pf_texpand<MM, true>, S.c.grid_for(total, PFB, 8), PFB, 0, S.c.stream, S.T, C.nt,
+                   Sc, ec, dst);
+    });
+    PD_LAUNCH_CHECK();
+    if (sp) prolong_add_planes(S.c, S.dim, S.periodic, C.n[0], F.n[0], F.nt * F.M, dst, x);
+}
+
+void st_cycle(PfastSt& S, int l, const double* b, double* x) {
+    PfastPlan& P = *S.sm[l];
+    const int L = (int)S.sm.size();
+    if (l == L - 1) {
+        for (int s = 0; s < S.coarse_t_sweeps; ++s) sweep(P, b, x, nullptr);
+        return;
+    }
+    for (int s = 0; s < S.nu_t; ++s) sweep(P, b, x, nullptr);
+    pick(P)(P, 0, 3, x, b, P.B[0].p, nullptr);
+    st_restrict(S, l, S.Bv[l + 1].p);
+    PD_CUDA(cudaMemsetAsync(S.X[l + 1].p, 0, S.sm[l + 1]->len[0] * sizeof(double), S.c.stream));
+    st_cycle(S, l + 1, S.Bv[l + 1].p, S.X[l + 1].p);
+    st_prolong(S, l, S.X[l + 1].p, x);
+    for (int s = 0; s < S.nu_t; ++s) sweep(P, b, x, nullptr);
+}
+
+// weights of level 0 are set: all coarser space-time levels and spatial levels
+void st_weights_ready(PfastSt& S) {
+    const int L = (int)S.sm.size();
+    for (int l = 0; l < L; ++l) {
+        PfastPlan& F = *S.sm[l];
+        if (l + 1 < L) {
+            PfastPlan& C = *S.sm[l + 1];
+            alloc_weights(C);
+            const double* w = F.W[0].p;
+            if (S.space[l]) {  // T[0] is scratch outside a sweep
+                restrict_planes(S.c, S.dim, S.periodic, C.n[0], F.n[0], F.nt * F.M, w, F.T[0].p);
+                w = F.T[0].p;
+            }
+            time_combine<1>(S, l, w, C.W[0].p);
+        }
+        weights_ready(F);
+    }
 }
 
 }  // namespace
@@ -533,142 +1006,238 @@ int pd_pfast_create(void* ctx, int dim, int64_t n, int bc_periodic, double kappa
                     int nu, int coarse_sweeps, double omega_s, double omega_t, void** out) {
     return guarded_pf([&] {
         auto& c = *static_cast<pd::Ctx*>(ctx);
-        if (dim != 2 && dim != 3) throw pd::ConfigError("P-fast needs a 2D or 3D grid");
-        if (M < 1 || M > pd::kPfMaxM) throw pd::ConfigError("P-fast supports 1..5 nodes");
-        if (nt < 1 || n < 1) throw pd::ConfigError("P-fast needs nt >= 1 and n >= 1");
-        if (levels < 1 || nu < 1 || coarse_sweeps < 1)
-            throw pd::ConfigError("P-fast needs levels, nu and coarse_sweeps >= 1");
-        auto P = std::make_unique<pd::PfastPlan>(c);
-        P->dim = dim;
-        P->M = M;
-        P->nt = nt;
-        P->levels = levels;
-        P->nu = nu;
-        P->coarse_sweeps = coarse_sweeps;
-        P->periodic = bc_periodic != 0;
-        P->omega_t = omega_t;
-        int64_t nl = n;
-        for (int l = 0; l < levels; ++l) {
-            if (l > 0) {
-                if (P->periodic) {
-                    if (nl % 2 || nl < 4) throw pd::ConfigError("cannot coarsen the periodic grid");
-                    nl /= 2;
-                } else {
-                    if (nl % 2 == 0 || nl < 3) throw pd::ConfigError("cannot coarsen the Dirichlet grid");
-                    nl = (nl - 1) / 2;
-                }
-            }
-            if (nl > (1 << 20)) throw pd::ConfigError("grid too large");
-            if (nt * M * nl * (dim == 3 ? nl : 1) * ((nl + 31) / 32) >= (int64_t(1) << 31))
-                throw pd::ConfigError("P-fast grid x steps too large for one plan");
-            P->n.push_back((int)nl);
-            int64_t S = nl * nl * (dim == 3 ? nl : 1);
-            P->len.push_back(nt * M * S);
-            // h of this level (StencilSpec.h: Dirichlet 1/(n+1), periodic 1/n)
-            const double h = P->periodic ? 1.0 / (double)nl : 1.0 / (double)(nl + 1);
-            const double mh = std::pow(h, dim);
-            const double ks = kappa * std::pow(h, dim - 2);
-            pd::PfCoef C{};
-            double D[pd::kPfMaxM * pd::kPfMaxM];
-            for (int i = 0; i < M; ++i)
-                for (int k = 0; k < M; ++k) {
-                    C.Ac[i * M + k] = Kq[i * M + k] * mh + dt * Mq[i * M + k] * (ks * 2.0 * dim);
-                    C.Ao[i * M + k] = -dt * Mq[i * M + k] * ks;
-                    D[i * M + k] = C.Ac[i * M + k];
-                }
-            double Di[pd::kPfMaxM * pd::kPfMaxM];
-            if (!pd::invert(D, Di, M)) throw pd::ConfigError("singular point block");
-            for (int i = 0; i < M * M; ++i) C.Dinv[i] = omega_s * Di[i];
-            for (int m = 0; m < M; ++m) C.cprev[m] = -l0[m] * mh;
-            C.omega_t = omega_t;
-            P->coef.push_back(C);
-        }
-        P->B.resize(levels);
-        P->E.resize(levels);
-        P->T.resize(levels);
-        for (int l = 0; l < levels; ++l) {
-            P->B[l].alloc(P->len[l]);
-            P->E[l].alloc(P->len[l]);
-            P->T[l].alloc(P->len[l]);
-        }
-        P->part.alloc(pd::kPfNormBlocks);
-        P->norm.alloc(1);
-        PD_CUDA(cudaMallocHost(&P->pinned, sizeof(double)));
-        *out = P.release();
+        *out = pd::make_plan(c, dim, n, bc_periodic, kappa, M, nt, dt, Kq, Mq, l0, levels, nu,
+                             coarse_sweeps, omega_s, omega_t)
+                   .release();
     });
 }
 
-/* r = b − L x (the space-time residual at level 0); |r|^2 into *norm2_dev when non-null */
-int pd_pfast_residual(void* plan, const double* x, const double* b, double* r, double* norm2_dev) {
+/* r = b − L x (or b − J x with weights set) at level 0; |r|^2 into *norm2_dev when
+ * non-null; halo: the previous slab's last node (NULL: none) */
+int pd_pfast_residual(void* plan, const double* x, const double* b, double* r, const double* halo,
+                      double* norm2_dev) {
     return guarded_pf([&] {
         auto& P = *static_cast<pd::PfastPlan*>(plan);
-        pd::pick(P)(P, 0, 3, x, b, r);
+        pd::pick(P)(P, 0, 3, x, b, r, halo);
         if (norm2_dev) pd::norm2(P, r, P.len[0], norm2_dev);
     });
 }
 
-/* one outer block-Jacobi-in-time sweep: x += ω_t · Vcycle(b − L x) */
-int pd_pfast_sweep(void* plan, const double* b, double* x) {
+/* out = rhs − L u − γ(I⊗Mqh) r(u) = −F(u) (spacetime.py:131-142); kind 0 cubic, 1 Fisher */
+int pd_pfast_nl_residual(void* plan, const double* u, const double* rhs, double* out,
+                         const double* halo, double gamma, int kind, double* norm2_dev) {
     return guarded_pf([&] {
         auto& P = *static_cast<pd::PfastPlan*>(plan);
-        pd::pick(P)(P, 0, 3, x, b, P.B[0].p);
-        if (!pd::vcycle(P, 0, x)) {
-            pd::launch(pd::k_pf_axpy, P.c.grid_for(P.len[0], pd::PFB, 8), pd::PFB, 0, P.c.stream,
-                       P.len[0], P.omega_t, (const double*)P.E[0].p, x);
-            PD_LAUNCH_CHECK();
-        }
+        if (kind != 0 && kind != 1) throw pd::ConfigError("unknown reaction kind");
+        const double h = P.periodic ? 1.0 / P.n[0] : 1.0 / (P.n[0] + 1);
+        P.coef[0].rs = gamma * P.dt * std::pow(h, P.dim);
+        P.coef[0].kind = kind;
+        pd::pick(P)(P, 0, 5, u, rhs, out, halo);
+        if (norm2_dev) pd::norm2(P, out, P.len[0], norm2_dev);
     });
+}
+
+/* Linearisation state: W = γ·dt·h^d·r'(u) on every spatial level (NULL u: back to
+ * the linear operator).  Synchronising (checks the point blocks). */
+int pd_pfast_set_state(void* plan, const double* u, double gamma, int kind) {
+    return guarded_pf([&] {
+        auto& P = *static_cast<pd::PfastPlan*>(plan);
+        if (!u) {
+            P.nl = false;
+            return;
+        }
+        if (kind != 0 && kind != 1) throw pd::ConfigError("unknown reaction kind");
+        pd::alloc_weights(P);
+        const double h = P.periodic ? 1.0 / P.n[0] : 1.0 / (P.n[0] + 1);
+        PD_CUDA(cudaMemsetAsync(P.wmax.p, 0, sizeof(unsigned long long), P.c.stream));
+        pd::launch(pd::k_pf_weights, P.c.grid_for(P.len[0], pd::PFB, 8), pd::PFB, 0, P.c.stream,
+                   P.len[0], gamma * P.dt * std::pow(h, P.dim), kind, u, P.W[0].p, P.wmax.p);
+        PD_LAUNCH_CHECK();
+        pd::weights_ready(P);
+    });
+}
+
+/* one outer block-Jacobi-in-time sweep: x += ω_t · Vcycle(b − L x) */
+int pd_pfast_sweep(void* plan, const double* b, double* x, const double* halo) {
+    return guarded_pf([&] { pd::sweep(*static_cast<pd::PfastPlan*>(plan), b, x, halo); });
 }
 
 /* sweeps until |b − L x| <= max(tol_abs, tol_rel |b − L x0|) (multigrid.py:275-305
  * stopping and divergence rules); hist (host, max_sweeps + 1) optional */
-int pd_pfast_solve(void* plan, const double* b, double* x, double tol_rel, double tol_abs,
-                   int max_sweeps, pd_solve_report* rep, double* hist) {
+int pd_pfast_solve(void* plan, const double* b, double* x, const double* halo, double tol_rel,
+                   double tol_abs, int max_sweeps, pd_solve_report* rep, double* hist) {
     return guarded_pf([&] {
         auto& P = *static_cast<pd::PfastPlan*>(plan);
-        const auto op = pd::pick(P);
         auto resid = [&]() {
-            op(P, 0, 3, x, b, P.B[0].p);
+            pd::pick(P)(P, 0, 3, x, b, P.B[0].p, halo);
             pd::norm2(P, P.B[0].p, P.len[0], P.norm.p);
-            PD_CUDA(cudaMemcpyAsync(P.pinned, P.norm.p, sizeof(double), cudaMemcpyDeviceToHost,
-                                    P.c.stream));
-            PD_CUDA(cudaStreamSynchronize(P.c.stream));
-            return std::sqrt(*P.pinned);
+            return std::sqrt(pd::read_scalar(P, P.norm.p));
         };
-        double r = resid();
-        if (!std::isfinite(r)) throw pd::SolverError("non-finite initial residual", -1);
-        const double thr = std::max(tol_abs, tol_rel * r);
-        double lowest = r;
-        int it = 0, conv = 0, div = 0;
-        if (hist) hist[0] = r;
-        while (true) {
-            if (r <= thr) { conv = 1; break; }
-            if (it >= max_sweeps) { div = 1; break; }
+        // the residual of resid() is still in B[0]: the sweep's V-cycle starts from it
+        auto step = [&]() {
             if (!pd::vcycle(P, 0, x)) {
                 pd::launch(pd::k_pf_axpy, P.c.grid_for(P.len[0], pd::PFB, 8), pd::PFB, 0,
                            P.c.stream, P.len[0], P.omega_t, (const double*)P.E[0].p, x);
                 PD_LAUNCH_CHECK();
             }
-            ++it;
-            r = resid();
-            if (hist) hist[it] = r;
-            if (!std::isfinite(r)) throw pd::SolverError("non-finite residual in P-fast sweep", it);
-            lowest = std::min(lowest, r);
-            if (r > 10.0 * lowest) { div = 1; break; }
-        }
-        rep->iterations = it;
-        rep->converged = conv;
-        rep->diverged = div;
-        rep->hist_len = hist ? it + 1 : 0;
+        };
+        pd::iterate(resid, step, tol_rel, tol_abs, max_sweeps, rep, hist);
     });
-}
-
-int pd_pfast_set_halo(void* plan, const double* halo) {
-    return guarded_pf([&] { static_cast<pd::PfastPlan*>(plan)->halo = halo; });
 }
 
 int pd_pfast_destroy(void* plan) {
     return guarded_pf([&] { delete static_cast<pd::PfastPlan*>(plan); });
+}
+
+/* ---- space-time multigrid around the smoother ---- */
+int pd_pfast_st_create(void* ctx, int dim, int bc_periodic, double kappa, int M, const double* Kq,
+                       const double* Mq, const double* l0, int nlevels, const int64_t* nt,
+                       const int64_t* n, const double* dt, const int* space_levels,
+                       const double* P1, const double* P2, const double* E, const int* half,
+                       int nu_t, int coarse_t_sweeps, int nu, int coarse_sweeps, double omega_s,
+                       double omega_t, void** out) {
+    return guarded_pf([&] {
+        auto& c = *static_cast<pd::Ctx*>(ctx);
+        if (nlevels < 1 || nu_t < 1 || coarse_t_sweeps < 1)
+            throw pd::ConfigError("P-fast STMG needs nlevels, nu_t and coarse_t_sweeps >= 1");
+        auto S = std::make_unique<pd::PfastSt>(c);
+        S->M = M;
+        S->dim = dim;
+        S->periodic = bc_periodic != 0;
+        S->nu_t = nu_t;
+        S->coarse_t_sweeps = coarse_t_sweeps;
+        if (M < 1 || M > pd::kPfMaxM) throw pd::ConfigError("P-fast supports 1..5 nodes");
+        for (int i = 0; i < M * M; ++i) {
+            S->T.P1[i] = P1[i];
+            S->T.P2[i] = P2[i];
+            S->T.E[i] = E[i];
+        }
+        for (int m = 0; m < M; ++m) S->T.half[m] = half[m];
+        S->X.resize(nlevels);
+        S->Bv.resize(nlevels);
+        for (int l = 0; l < nlevels; ++l) {
+            const bool last = l == nlevels - 1;
+            if (l > 0) {
+                if (nt[l] * 2 != nt[l - 1]) throw pd::ConfigError("time levels must halve the steps");
+                const int64_t nf = n[l - 1];
+                const int64_t nc = S->periodic ? nf / 2 : (nf - 1) / 2;
+                if (n[l] != nf && n[l] != nc) throw pd::ConfigError("bad space-time level grid");
+                S->space.push_back(n[l] != nf);
+            }
+            // the coarsest level sweeps undamped (exact after nt sweeps for exact blocks)
+            S->sm.push_back(pd::make_plan(c, dim, n[l], bc_periodic, kappa, M, nt[l], dt[l], Kq, Mq,
+                                          l0, space_levels[l], nu, coarse_sweeps, omega_s,
+                                          last ? 1.0 : omega_t));
+            if (l > 0) {
+                S->X[l].alloc(S->sm[l]->len[0]);
+                S->Bv[l].alloc(S->sm[l]->len[0]);
+            }
+        }
+        S->space.push_back(0);
+        *out = S.release();
+    });
+}
+
+int pd_pfast_st_destroy(void* st) {
+    return guarded_pf([&] { delete static_cast<pd::PfastSt*>(st); });
+}
+
+/* linearisation state on every space-time and spatial level (NULL u: linear) */
+int pd_pfast_st_set_state(void* st, const double* u, double gamma, int kind) {
+    return guarded_pf([&] {
+        auto& S = *static_cast<pd::PfastSt*>(st);
+        if (!u) {
+            for (auto& p : S.sm) p->nl = false;
+            return;
+        }
+        if (kind != 0 && kind != 1) throw pd::ConfigError("unknown reaction kind");
+        pd::PfastPlan& P = *S.sm[0];
+        pd::alloc_weights(P);
+        const double h = P.periodic ? 1.0 / P.n[0] : 1.0 / (P.n[0] + 1);
+        PD_CUDA(cudaMemsetAsync(P.wmax.p, 0, sizeof(unsigned long long), P.c.stream));
+        pd::launch(pd::k_pf_weights, P.c.grid_for(P.len[0], pd::PFB, 8), pd::PFB, 0, P.c.stream,
+                   P.len[0], gamma * P.dt * std::pow(h, P.dim), kind, u, P.W[0].p, P.wmax.p);
+        PD_LAUNCH_CHECK();
+        pd::st_weights_ready(S);
+    });
+}
+
+/* one V(nu_t, nu_t) space-time cycle on level 0 */
+int pd_pfast_st_cycle(void* st, const double* b, double* x) {
+    return guarded_pf([&] { pd::st_cycle(*static_cast<pd::PfastSt*>(st), 0, b, x); });
+}
+
+/* cycles until |b − J x| <= max(tol_abs, tol_rel |b − J x0|) (multigrid.py:275-305) */
+int pd_pfast_st_solve(void* st, const double* b, double* x, double tol_rel, double tol_abs,
+                      int max_cycles, pd_solve_report* rep, double* hist) {
+    return guarded_pf([&] {
+        auto& S = *static_cast<pd::PfastSt*>(st);
+        pd::PfastPlan& P = *S.sm[0];
+        auto resid = [&]() {
+            pd::pick(P)(P, 0, 3, x, b, P.B[0].p, nullptr);
+            pd::norm2(P, P.B[0].p, P.len[0], P.norm.p);
+            return std::sqrt(pd::read_scalar(P, P.norm.p));
+        };
+        pd::iterate(resid, [&]() { pd::st_cycle(S, 0, b, x); }, tol_rel, tol_abs, max_cycles, rep,
+                    hist);
+    });
+}
+
+/* Level primitives for the time-slab sharded cycle (driven by pfast.py): b / x NULL
+ * select the level's own vectors (levels >= 1). */
+int pd_pfast_st_level_plan(void* st, int level, void** plan_out) { /* borrowed smoother */
+    return guarded_pf([&] {
+        auto& S = *static_cast<pd::PfastSt*>(st);
+        if (level < 0 || level >= (int)S.sm.size()) throw pd::ConfigError("bad level");
+        *plan_out = S.sm[level].get();
+    });
+}
+
+int pd_pfast_st_level_sweep(void* st, int level, const double* b, double* x, const double* halo) {
+    return guarded_pf([&] {
+        auto& S = *static_cast<pd::PfastSt*>(st);
+        if (level < 0 || level >= (int)S.sm.size()) throw pd::ConfigError("bad level");
+        if (level == 0 && (!b || !x)) throw pd::ConfigError("level 0 vectors are the caller's");
+        pd::sweep(*S.sm[level], b ? b : S.Bv[level].p, x ? x : S.X[level].p, halo);
+    });
+}
+
+/* residual of the level into the smoother's B[0], restricted into level+1's right-hand
+ * side; level+1's iterate is zeroed */
+int pd_pfast_st_level_restrict(void* st, int level, const double* b, const double* x,
+                               const double* halo) {
+    return guarded_pf([&] {
+        auto& S = *static_cast<pd::PfastSt*>(st);
+        if (level < 0 || level + 1 >= (int)S.sm.size()) throw pd::ConfigError("bad level");
+        if (level == 0 && (!b || !x)) throw pd::ConfigError("level 0 vectors are the caller's");
+        pd::PfastPlan& P = *S.sm[level];
+        pd::pick(P)(P, 0, 3, x ? x : S.X[level].p, b ? b : S.Bv[level].p, P.B[0].p, halo);
+        pd::st_restrict(S, level, S.Bv[level + 1].p);
+        PD_CUDA(cudaMemsetAsync(S.X[level + 1].p, 0, S.sm[level + 1]->len[0] * sizeof(double),
+                                S.c.stream));
+    });
+}
+
+int pd_pfast_st_level_prolong(void* st, int level, double* x) {
+    return guarded_pf([&] {
+        auto& S = *static_cast<pd::PfastSt*>(st);
+        if (level < 0 || level + 1 >= (int)S.sm.size()) throw pd::ConfigError("bad level");
+        if (level == 0 && !x) throw pd::ConfigError("level 0 vectors are the caller's");
+        pd::st_prolong(S, level, S.X[level + 1].p, x ? x : S.X[level].p);
+    });
+}
+
+/* copy the last node of the level's iterate (n_l^d doubles) into out (device) */
+int pd_pfast_st_level_last(void* st, int level, const double* x, double* out) {
+    return guarded_pf([&] {
+        auto& S = *static_cast<pd::PfastSt*>(st);
+        if (level < 0 || level >= (int)S.sm.size()) throw pd::ConfigError("bad level");
+        if (level == 0 && !x) throw pd::ConfigError("level 0 vectors are the caller's");
+        pd::PfastPlan& P = *S.sm[level];
+        const double* src = (x ? x : S.X[level].p) + P.len[0] - P.S(0);
+        PD_CUDA(cudaMemcpyAsync(out, src, P.S(0) * sizeof(double), cudaMemcpyDeviceToDevice,
+                                S.c.stream));
+    });
 }
 
 }  // extern "C"
