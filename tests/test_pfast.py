@@ -486,3 +486,32 @@ def test_gpu_stmg_slabs_equal_serial_device():
     assert conv and rep.converged and its == rep.iterations
     x = np.concatenate([N.to_host(s.solution()) for s in slabs])
     assert np.linalg.norm(x - x_ser) <= 1e-12 * np.linalg.norm(x_ser)
+
+
+@pytest.mark.gpu
+def test_gpu_stmg_cycle_count_flat_in_nt_and_c5_newton():
+    """Device STMG at config 5's μ = κ·dt/h²: the cycle count to 1e-8 does not grow from
+    32 to 256 steps (block-Jacobi alone grows with Nt), and the cubic Newton solve
+    converges."""
+    from paper_2006_12883_b200 import _native as N
+    from paper_2006_12883_b200.pfast import PfastSolver, PfastStmg, pfast_rhs
+
+    spec = PB.StencilSpec(3, 32, "periodic", 0.1)
+    dt = 6.5536 * spec.h ** 2 / 0.1
+    u0 = np.random.default_rng(0).uniform(-1, 1, spec.ndof)
+    counts = []
+    for Nt in (32, 256):
+        b = N.to_device(pfast_rhs(spec, 3, Nt, u0))
+        _, rep = PfastStmg(spec, 3, Nt, dt).solve(b, tol_rel=1e-8)
+        assert rep.converged
+        counts.append(rep.iterations)
+    assert abs(counts[0] - counts[1]) <= 1 and counts[1] <= 20, counts
+    b = N.to_device(pfast_rhs(spec, 3, 64, u0))
+    _, bj = PfastSolver(spec, 3, 64, dt).solve(b, tol_rel=1e-8, max_sweeps=400)
+    assert bj.iterations > 3 * counts[1]
+    s = PfastStmg(spec, 3, 32, 1e-3)
+    b = N.to_device(pfast_rhs(spec, 3, 32, u0))
+    u, rep = s.newton(b, 1.0, "cubic", tol=1e-8)
+    assert rep.converged and rep.newton_iterations >= 1 and not rep.diverged
+    _, res = s.nl_residual(u, b, 1.0, "cubic")
+    assert res <= 1e-8
