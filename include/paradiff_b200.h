@@ -93,12 +93,37 @@ int pd_dense_lu_create(void *ctx, void *csr, void **lu_out); /* synchronising */
 int pd_dense_lu_solve(void *ctx, void *lu, const double *b, double *x);
 int pd_dense_lu_destroy(void *lu);
 
+/* ---- banded LU with partial pivoting: the direct solves of spacetime.py:154-195
+ *      (_element_solve, solve_sequential, solve_direct call SuperLU there).  csr is
+ *      the matrix with its unknowns already reordered so that it is banded (kl sub-,
+ *      ku super-diagonals); perm_host (n int32, may be NULL) maps band row i to the
+ *      caller's unknown perm[i] for b and x of pd_band_lu_solve.  A singular matrix
+ *      is PD_ERR_SOLVER (SuperLU: "Factor is exactly singular").  Synchronising. */
+int pd_band_lu_create(void *ctx, void *csr, int kl, int ku, const int32_t *perm_host,
+                      void **lu_out);
+int pd_band_lu_solve(void *ctx, void *lu, const double *b, double *x);
+int pd_band_lu_destroy(void *lu);
+
 /* ---- GMRES (linalg.py:215-311 gmres); ilu may be NULL (no preconditioner),
  *      x0 may be NULL (zero start).  hist (host, hist_cap doubles) receives
  *      SolveReport.residual_history.  Synchronising. ------------------------ */
 int pd_gmres(void *ctx, void *A, void *ilu, const double *b, const double *x0, double *x,
              double tol_rel, double tol_abs, int restart, int max_it,
              pd_solve_report *rep, double *hist, int hist_cap);
+
+/* The same solve when the operator and/or the preconditioner is a host callable
+ * (linalg.py:233-237: "A is a matrix or a callable matvec; precond needs a solve
+ * method (or is callable)").  Exactly one of A (CSR handle) / matvec, at most one of
+ * ilu / psolve.  A callable reads its argument from cb_in and writes its result to
+ * cb_out (device vectors of n doubles owned by the caller; the stream is idle while it
+ * runs) and returns 0, or nonzero to abort the solve.  The Krylov vectors, the
+ * orthogonalisation and the Givens recurrence stay on the device.  Synchronising. */
+typedef int (*pd_apply_cb)(void *user);
+int pd_gmres_callable(void *ctx, int64_t n, void *A, pd_apply_cb matvec, void *ilu,
+                      pd_apply_cb psolve, void *user, double *cb_in, double *cb_out,
+                      const double *b, const double *x0, double *x, double tol_rel,
+                      double tol_abs, int restart, int max_it, pd_solve_report *rep,
+                      double *hist, int hist_cap);
 
 /* ---- space-time multigrid (multigrid.py:197-305 MultigridHierarchy).
  *      Takes ownership of the level matrices mats[0..L) (Galerkin products,

@@ -118,7 +118,14 @@ _SIGNATURES = {
     "pd_spread": (_int, [_vp, _vp, _vp, _vp, _int, _int, _i64]),
     "pd_terminal": (_int, [_vp, _vp, _vp, _int, _int, _i64]),
     "pd_scale": (_int, [_vp, _vp, _vp, _dbl, _i64]),
+    "pd_band_lu_create": (_int, [_vp, _vp, _int, _int, _vp, ctypes.POINTER(_vp)]),
+    "pd_band_lu_solve": (_int, [_vp, _vp, _vp, _vp]),
+    "pd_band_lu_destroy": (_int, [_vp]),
+    "pd_gmres_callable": (_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl,
+                                 _dbl, _int, _int, ctypes.POINTER(SolveReportC), _vp, _int]),
 }
+
+APPLY_CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p)
 
 _lock = threading.Lock()
 _LIB = None

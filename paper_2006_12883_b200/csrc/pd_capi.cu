@@ -165,6 +165,21 @@ int pd_dense_lu_destroy(void* lu) {
     return guarded([&] { delete static_cast<pd::DenseLU*>(lu); });
 }
 
+int pd_band_lu_create(void* ctx, void* csr, int kl, int ku, const int32_t* perm_host, void** out) {
+    return guarded([&] {
+        *out = pd::band_lu_create(*C(ctx), *H<pd::Csr>(csr, "matrix"), kl, ku, perm_host);
+    });
+}
+int pd_band_lu_solve(void* ctx, void* lu, const double* b, double* x) {
+    return guarded([&] {
+        if (!lu) throw pd::ConfigError("null banded LU handle");
+        pd::band_lu_solve(*C(ctx), *static_cast<pd::BandLU*>(lu), b, x);
+    });
+}
+int pd_band_lu_destroy(void* lu) {
+    return guarded([&] { pd::band_lu_destroy(static_cast<pd::BandLU*>(lu)); });
+}
+
 int pd_gmres(void* ctx, void* A, void* ilu, const double* b, const double* x0, double* x,
              double tol_rel, double tol_abs, int restart, int max_it, pd_solve_report* rep,
              double* hist, int hist_cap) {
@@ -173,6 +188,45 @@ int pd_gmres(void* ctx, void* A, void* ilu, const double* b, const double* x0, d
         pd::Csr& M = *H<pd::Csr>(A, "matrix");
         auto r = pd::gmres_run(c, M, static_cast<pd::Ilu0*>(ilu), b, x0, x, tol_rel, tol_abs,
                                restart, max_it);
+        fill_report(rep, r.iterations, r.converged, r.diverged, r.hist, hist, hist_cap);
+    });
+}
+
+int pd_gmres_callable(void* ctx, int64_t n, void* A, pd_apply_cb matvec, void* ilu,
+                      pd_apply_cb psolve, void* user, double* cb_in, double* cb_out,
+                      const double* b, const double* x0, double* x, double tol_rel, double tol_abs,
+                      int restart, int max_it, pd_solve_report* rep, double* hist, int hist_cap) {
+    return guarded([&] {
+        pd::Ctx& c = *C(ctx);
+        if ((A == nullptr) == (matvec == nullptr))
+            throw pd::ConfigError("give the operator either as a matrix or as a callable");
+        if (ilu && psolve) throw pd::ConfigError("give one preconditioner, not two");
+        if ((matvec || psolve) && (!cb_in || !cb_out))
+            throw pd::ConfigError("callables need the two exchange vectors");
+        pd::Csr* M = A ? H<pd::Csr>(A, "matrix") : nullptr;
+        if (M && (M->nrows != n || M->ncols != n)) throw pd::ConfigError("matrix size differs from n");
+        pd::Ilu0* P = static_cast<pd::Ilu0*>(ilu);
+        // a host callable reads cb_in and writes cb_out (device vectors the caller owns);
+        // a nonzero return aborts the solve (the caller keeps the exception)
+        auto through = [&](pd_apply_cb fn, const char* what) {
+            return [&c, fn, user, cb_in, cb_out, n, what](const double* xin, double* yout) {
+                pd::vec_copy(c, cb_in, xin, n);
+                PD_CUDA(cudaStreamSynchronize(c.stream));
+                if (fn(user) != 0) throw pd::SolverError(std::string(what) + " callable failed");
+                pd::vec_copy(c, yout, cb_out, n);
+            };
+        };
+        pd::Gmres::ApplyFn fa, fm;
+        if (matvec) fa = through(matvec, "matvec");
+        else fa = [&c, M](const double* xin, double* yout) {
+            pd::csr_spmv(c, *M, xin, yout, pd::SPMV_SET, nullptr, nullptr, 0, nullptr, nullptr);
+        };
+        if (psolve) fm = through(psolve, "preconditioner");
+        else if (P) fm = [&c, P](const double* xin, double* yout) {
+            pd::ilu0_solve(c, *P, xin, yout, nullptr, 0);
+        };
+        auto r = pd::gmres_run_callables(c, n, fa, (psolve || P) ? &fm : nullptr, b, x0, x, tol_rel,
+                                         tol_abs, restart, max_it);
         fill_report(rep, r.iterations, r.converged, r.diverged, r.hist, hist, hist_cap);
     });
 }

@@ -187,6 +187,14 @@ struct DenseLU {
     DevBuf<int32_t> piv; // LAPACK-style row interchanges (0-based)
 };
 
+// Banded LU with partial pivoting (pd_band.cu): the device counterpart of the SuperLU
+// solves in spacetime.py:154-195.  A is the (already permuted) matrix; perm_host (may be
+// null) maps band row i to the caller's unknown perm[i] for the solve's vectors.
+struct BandLU;
+BandLU* band_lu_create(Ctx& c, const Csr& A, int kl, int ku, const int32_t* perm_host);
+void band_lu_solve(Ctx& c, BandLU& f, const double* b, double* x);
+void band_lu_destroy(BandLU* f);
+
 // ------------------------------------------------------------------ kernels (host wrappers)
 // vector ops
 void vec_fill(Ctx& c, double* x, int64_t n, double v);

@@ -329,6 +329,56 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
     PD_LAUNCH_CHECK();
 }
 
+// r = b - t (one rounding per entry, as numpy's b - matvec(x))
+__global__ void k_gm_sub(double* r, const double* b, const double* t, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        r[i] = sub(b[i], t[i]);
+}
+
+void Gmres::slot_with_callables(int slot, int mgs_passes, const double* b, const ApplyFn& fa,
+                                const ApplyFn* fm) {
+    const int g = c.grid_for(n, KB, 8);
+    const int gr = std::min(c.grid_for(n, KB, 4), kReduceMaxBlocks);
+    launch(k_gm_start_vec, g, KB, 0, c.stream, st.p, r0, rg.p, V.p, vcur.p, n);
+    launch(k_gm_start, 1, 1, 0, c.stream, st.p);
+    PD_LAUNCH_CHECK();
+    const GmDev& s = read_state();  // synchronising: the callables run on the host's clock
+    if (s.phase == GM_RUN) {
+        const double* zin = vcur.p;
+        if (fm) {
+            (*fm)(vcur.p, z.p);
+            zin = z.p;
+        }
+        fa(zin, w.p);
+    }
+    const int passes = std::min(mgs_passes, restart + 1);
+    for (int i = 0; i < passes; ++i)
+        launch(k_gm_mgs, gr, KB, 0, c.stream, st.p, i, w.p, V.p, n, c.red_partials.p,
+               c.red_counter.p);
+    launch(k_gm_arnoldi, 1, 1, 0, c.stream, st.p, slot, hist.p);
+    launch(k_gm_newvec, g, KB, 0, c.stream, st.p, slot, w.p, V.p, vcur.p, n);
+    launch(k_gm_finish_y, 1, 1, 0, c.stream, st.p);
+    launch(k_gm_combine, g, KB, 0, c.stream, st.p, V.p, u.p, n);
+    PD_LAUNCH_CHECK();
+    read_state();
+    if (s.phase != GM_FINISH) return;
+    const double* du = u.p;
+    if (fm) {
+        (*fm)(u.p, z.p);
+        du = z.p;
+    }
+    launch(k_gm_update_x, g, KB, 0, c.stream, st.p, xg.p, du, n);
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    if (s.final_res == GM_FINISH) {
+        fa(xg.p, w.p);
+        launch(k_gm_sub, g, KB, 0, c.stream, rg.p, b, (const double*)w.p, n);
+        vec_dot(c, rg.p, rg.p, n, norm2.p);
+    }
+    launch(k_gm_restart, 1, 1, 0, c.stream, st.p, norm2.p, hist.p);
+    PD_LAUNCH_CHECK();
+}
+
 const GmDev& Gmres::read_state() {
     // the host mirrors only the scalar header (phase, j, counters, flags)
     if (!host_st) host_st = std::make_unique<GmDev>();
@@ -393,6 +443,53 @@ GmresResult gmres_run(Ctx& c, const Csr& A, Ilu0* M, const double* b, const doub
     } else {
         if (x0) vec_copy(c, x, x0, n);
         else vec_fill(c, x, n, 0.0);
+    }
+    GmresResult r;
+    r.hist = g.history(s.total);
+    r.iterations = s.total;
+    r.converged = s.converged != 0;
+    r.diverged = s.diverged != 0;
+    return r;
+}
+
+GmresResult gmres_run_callables(Ctx& c, int64_t n, const Gmres::ApplyFn& fa,
+                                const Gmres::ApplyFn* fm, const double* b, const double* x0,
+                                double* x, double tol_rel, double tol_abs, int restart,
+                                int max_it) {
+    if (n < 0) throw ConfigError("GMRES needs a nonnegative size");
+    if (max_it < 0) throw ConfigError("max_it must be nonnegative");
+    Gmres g(c, nullptr, nullptr, n, restart, std::max(max_it, 1));
+    const int64_t n1 = std::max<int64_t>(n, 1);
+    DevBuf<double> r0(n1), t(n1), zero;
+    const double* xs = x0;
+    if (!xs) {
+        zero.alloc(n1);
+        vec_fill(c, zero.p, n, 0.0);
+        xs = zero.p;
+    }
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    fa(xs, t.p);  // r0 = b - matvec(x0), also for a zero start (linalg.py:243)
+    launch(k_gm_sub, c.grid_for(n, KB, 8), KB, 0, c.stream, r0.p, b, (const double*)t.p, n);
+    vec_dot(c, r0.p, r0.p, n, c.scalars.p + 16);
+    g.enqueue_init(r0.p, c.scalars.p + 16, tol_rel, tol_abs, x0);
+    const GmDev& s = g.read_state();
+    int slot = 0;
+    while (s.phase != GM_DONE && s.total < std::max(max_it, 1)) {
+        const int j_eff = (s.phase == GM_START) ? 0 : s.j;
+        g.slot_with_callables(slot++, j_eff + 2, b, fa, fm);
+        g.read_state();
+    }
+    if (s.err == 1) throw SolverError("non-finite initial residual in GMRES");
+    if (s.err == 2) throw SolverError("non-finite residual in GMRES iteration");
+    if (s.err == 3) throw SolverError("non-finite residual in GMRES restart");
+    if (s.cycles > 0) {
+        vec_copy(c, x, g.x(), n);
+    } else {
+        if (x0) {
+            if (x != x0) vec_copy(c, x, x0, n);
+        } else {
+            vec_fill(c, x, n, 0.0);
+        }
     }
     GmresResult r;
     r.hist = g.history(s.total);

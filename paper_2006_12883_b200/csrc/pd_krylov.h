@@ -4,6 +4,8 @@
 // smoother pass (multigrid.py:243-256) needs no host synchronisation.
 #pragma once
 
+#include <functional>
+
 #include "pd_internal.h"
 #include "pd_stencil.h"
 
@@ -34,6 +36,12 @@ class Gmres {
     // one Arnoldi step slot (mgs_passes = max j + 2 this slot can need) plus
     // the guarded cycle-finish block; `b` = the GMRES right-hand side
     void enqueue_slot(int slot, int mgs_passes, const double* b);
+    // the same Arnoldi step slot with the operator / preconditioner applications made
+    // by host callables on device vectors (linalg.py:233-237 accepts any callable);
+    // the vector work stays on the device, the host syncs around each callable
+    using ApplyFn = std::function<void(const double* x, double* y)>;
+    void slot_with_callables(int slot, int mgs_passes, const double* b, const ApplyFn& fa,
+                             const ApplyFn* fm);
     const GmDev& read_state();  // synchronising; scalar header only (host mirror)
     double* x() { return xg.p; }
     int64_t size() const { return n; }
@@ -64,6 +72,12 @@ struct GmresResult {
 };
 GmresResult gmres_run(Ctx& c, const Csr& A, Ilu0* M, const double* b, const double* x0, double* x,
                       double tol_rel, double tol_abs, int restart, int max_it);
+// The same solve with A and/or the preconditioner given as host callables on device
+// vectors of length n (fm == nullptr: no preconditioner).
+GmresResult gmres_run_callables(Ctx& c, int64_t n, const Gmres::ApplyFn& fa,
+                                const Gmres::ApplyFn* fm, const double* b, const double* x0,
+                                double* x, double tol_rel, double tol_abs, int restart,
+                                int max_it);
 
 // Enqueue x += GMRES(A, b - A x) with ILU/block-Jacobi right preconditioning,
 // restart=min(nu,restart), max_it=nu, tol_rel=1e-13, tol_abs=0: exactly one

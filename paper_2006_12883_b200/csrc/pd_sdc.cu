@@ -1362,12 +1362,9 @@ int pd_sdc_level_create(void* ctx, void* Kh, const double* mh_host, int M, const
             // nothing to factor: the inverse is applied spectrally
         } else {
             for (int m = 0; m < M; ++m) L->dlu.push_back(pd::dense_lu_from_csr(c, *L->Am[m]));
-            static bool attr = false;
-            if (!attr) {
-                PD_CUDA(cudaFuncSetAttribute(pd::k_lu_solve_batched,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-                attr = true;
-            }
+            // per-device attribute: set for every level built on this context's device
+            PD_CUDA(cudaFuncSetAttribute(pd::k_lu_solve_batched,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
         }
         const int64_t W = max_workers;
         for (auto* b : {&L->fi_old, &L->fe_old, &L->f_tot, &L->base, &L->fi_new, &L->fe_new})

@@ -783,57 +783,160 @@ __global__ void k_csr_to_dense_colmajor(int64_t n, const int64_t* rp, const int3
         for (int64_t p = rp[i]; p < rp[i + 1]; ++p) A[i + (int64_t)ci[p] * n] += v[p];
 }
 
-// pivot search (first max |a_ik|, like idamax), full-row interchange and
-// column scaling by the reciprocal pivot (dgetf2).
-__global__ void k_lu_pivot(double* A, int64_t n, int64_t k, int32_t* piv, int* info) {
-    __shared__ double sv[1024];
-    __shared__ int64_t si[1024];
-    double best = -1.0;
-    int64_t bi = k;
-    for (int64_t i = k + threadIdx.x; i < n; i += blockDim.x) {
-        double a = fabs(A[i + k * n]);
-        if (a > best) { best = a; bi = i; }
-    }
-    sv[threadIdx.x] = best;
-    si[threadIdx.x] = bi;
-    __syncthreads();
-    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-        if (threadIdx.x < s) {
-            double o = sv[threadIdx.x + s];
-            int64_t oi = si[threadIdx.x + s];
-            if (o > sv[threadIdx.x] || (o == sv[threadIdx.x] && oi < si[threadIdx.x])) {
-                sv[threadIdx.x] = o;
-                si[threadIdx.x] = oi;
+// Blocked right-looking LU with partial pivoting (dgetrf structure, panels of kLuNB
+// columns): three launches per panel instead of two per column.  Every entry still
+// receives its rank-1 updates one pivot column at a time, in pivot order, as
+// a = fma(-l_ik, u_kj, a) — the operation sequence of the unblocked dgetf2 loop — so
+// the factors are bitwise those of the column-by-column elimination.
+constexpr int kLuNB = 32;
+
+// Panel [k0, k0+nb): per column the pivot search (first max |a_ik|, like idamax), the
+// interchange inside the panel, the column scaling by the reciprocal pivot and the
+// rank-1 update of the panel's remaining columns.  One CTA.
+__global__ void __launch_bounds__(1024) k_lu_panel(double* A, int64_t n, int64_t k0, int nb,
+                                                   int32_t* piv, int* info) {
+    __shared__ double sv[32];
+    __shared__ int64_t si[32];
+    __shared__ double urow[kLuNB];
+    __shared__ int64_t sp;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int c = 0; c < nb; ++c) {
+        const int64_t k = k0 + c;
+        double best = -1.0;
+        int64_t bi = k;
+        for (int64_t i = k + threadIdx.x; i < n; i += blockDim.x) {
+            const double a = fabs(A[i + k * n]);
+            if (a > best) { best = a; bi = i; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ob = __shfl_down_sync(0xffffffffu, best, o);
+            const int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) { sv[wid] = best; si[wid] = bi; }
+        __syncthreads();
+        if (wid == 0) {
+            best = sv[lane];
+            bi = si[lane];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ob = __shfl_down_sync(0xffffffffu, best, o);
+                const int64_t oi = __shfl_down_sync(0xffffffffu, bi, o);
+                if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+            }
+            if (lane == 0) { sp = bi; piv[k] = (int32_t)bi; }
+        }
+        __syncthreads();
+        const int64_t p = sp;
+        // interchange rows k and p inside the panel; keep the pivot row's tail
+        if (threadIdx.x < nb) {
+            const int64_t j = k0 + threadIdx.x;
+            const double t = A[p + j * n];
+            if (p != k) {
+                A[p + j * n] = A[k + j * n];
+                A[k + j * n] = t;
+            }
+            urow[threadIdx.x] = t;
+        }
+        __syncthreads();
+        const double akk = urow[c];
+        if (akk == 0.0) {
+            if (threadIdx.x == 0 && *info == 0) *info = (int)(k + 1);
+            continue;  // dgetf2 skips the elimination of a zero pivot column
+        }
+        const double r = 1.0 / akk;
+        for (int64_t i = k + 1 + threadIdx.x; i < n; i += blockDim.x) {
+            const double l = A[i + k * n] * r;
+            A[i + k * n] = l;
+            for (int cc = c + 1; cc < nb; ++cc) {
+                double* a = A + i + (k0 + cc) * n;
+                *a = fma(-l, urow[cc], *a);
             }
         }
         __syncthreads();
     }
-    const int64_t p = si[0];
-    if (threadIdx.x == 0) piv[k] = (int32_t)p;
-    if (p != k)
-        for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-            double t = A[k + j * n];
-            A[k + j * n] = A[p + j * n];
-            A[p + j * n] = t;
-        }
-    __syncthreads();
-    const double akk = A[k + k * n];
-    if (akk == 0.0) {
-        if (threadIdx.x == 0 && *info == 0) *info = (int)(k + 1);
-        return;
-    }
-    const double r = 1.0 / akk;
-    for (int64_t i = k + 1 + threadIdx.x; i < n; i += blockDim.x) A[i + k * n] *= r;
 }
 
-__global__ void k_lu_update(double* A, int64_t n, int64_t k) {
-    const int64_t m = n - k - 1;
-    const int64_t tot = m * m;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = k + 1 + t % m, j = k + 1 + t / m;
-        A[i + j * n] -= A[i + k * n] * A[k + j * n];
+// Columns outside the panel, one thread each: the panel's row interchanges, and for
+// columns to its right the unit-lower solve U12 = L11^{-1} A12 (row k of the block
+// after rows k' < k, i.e. the rank-1 order).
+__global__ void k_lu_cols(double* A, int64_t n, int64_t k0, int nb, const int32_t* piv) {
+    __shared__ double L11[kLuNB * kLuNB];
+    __shared__ int32_t sp[kLuNB];
+    for (int t = threadIdx.x; t < nb * nb; t += blockDim.x) {
+        const int i = t % nb, k = t / nb;
+        L11[i * kLuNB + k] = A[(k0 + i) + (k0 + k) * n];
     }
+    if (threadIdx.x < nb) sp[threadIdx.x] = piv[k0 + threadIdx.x];
+    __syncthreads();
+    int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j >= n - nb) return;
+    if (j >= k0) j += nb;
+    double* col = A + j * n;
+    for (int c = 0; c < nb; ++c) {
+        const int64_t p = sp[c];
+        if (p != k0 + c) {
+            const double t = col[k0 + c];
+            col[k0 + c] = col[p];
+            col[p] = t;
+        }
+    }
+    if (j < k0) return;
+    double u[kLuNB];
+#pragma unroll
+    for (int i = 0; i < kLuNB; ++i) u[i] = i < nb ? col[k0 + i] : 0.0;
+#pragma unroll
+    for (int k = 0; k < kLuNB; ++k)
+#pragma unroll
+        for (int i = k + 1; i < kLuNB; ++i)
+            if (i < nb) u[i] = fma(-L11[i * kLuNB + k], u[k], u[i]);
+#pragma unroll
+    for (int i = 0; i < kLuNB; ++i)
+        if (i < nb) col[k0 + i] = u[i];
+}
+
+// Trailing update A22 -= L21 U12: 64 x 64 tiles, 4 x 4 per thread, k in pivot order.
+__global__ void __launch_bounds__(256) k_lu_trailing(double* A, int64_t n, int64_t k0, int nb) {
+    __shared__ double Ls[kLuNB][64];
+    __shared__ double Us[kLuNB][65];
+    const int64_t r0 = k0 + nb + (int64_t)blockIdx.x * 64, c0 = k0 + nb + (int64_t)blockIdx.y * 64;
+    for (int t = threadIdx.x; t < nb * 64; t += 256) {
+        const int i = t & 63, k = t >> 6;
+        Ls[k][i] = r0 + i < n ? A[(r0 + i) + (k0 + k) * n] : 0.0;
+    }
+    for (int t = threadIdx.x; t < nb * 64; t += 256) {
+        const int k = t % nb, j = t / nb;
+        Us[k][j] = c0 + j < n ? A[(k0 + k) + (c0 + j) * n] : 0.0;
+    }
+    __syncthreads();
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    double acc[4][4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int64_t i = r0 + tx + 16 * r, j = c0 + ty + 16 * s;
+            acc[s][r] = (i < n && j < n) ? A[i + j * n] : 0.0;
+        }
+    for (int k = 0; k < nb; ++k) {
+        double l[4], u[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) l[r] = Ls[k][tx + 16 * r];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) u[s] = Us[k][ty + 16 * s];
+#pragma unroll
+        for (int s = 0; s < 4; ++s)
+#pragma unroll
+            for (int r = 0; r < 4; ++r) acc[s][r] = fma(-l[r], u[s], acc[s][r]);
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int64_t i = r0 + tx + 16 * r, j = c0 + ty + 16 * s;
+            if (i < n && j < n) A[i + j * n] = acc[s][r];
+        }
 }
 
 std::unique_ptr<DenseLU> dense_lu_from_csr(Ctx& c, const Csr& A) {
@@ -849,10 +952,17 @@ std::unique_ptr<DenseLU> dense_lu_from_csr(Ctx& c, const Csr& A) {
                                                                     A.val.p, f->lu.p);
     DevBuf<int> info(1);
     PD_CUDA(cudaMemsetAsync(info.p, 0, sizeof(int), c.stream));
-    for (int64_t k = 0; k < n; ++k) {
-        launch(k_lu_pivot, 1, 1024, 0, c.stream, f->lu.p, n, k, f->piv.p, info.p);
-        const int64_t m = n - k - 1;
-        if (m > 0) launch(k_lu_update, c.grid_for(m * m, BS, 16), BS, 0, c.stream, f->lu.p, n, k);
+    for (int64_t k0 = 0; k0 < n; k0 += kLuNB) {
+        const int nb = (int)std::min<int64_t>(kLuNB, n - k0);
+        launch(k_lu_panel, 1, 1024, 0, c.stream, f->lu.p, n, k0, nb, f->piv.p, info.p);
+        if (n > nb)
+            launch(k_lu_cols, (int)((n - nb + 127) / 128), 128, 0, c.stream, f->lu.p, n, k0, nb,
+                   (const int32_t*)f->piv.p);
+        const int64_t m = n - k0 - nb;
+        if (m > 0) {
+            const unsigned t = (unsigned)((m + 63) / 64);
+            launch(k_lu_trailing, dim3(t, t), 256, 0, c.stream, f->lu.p, n, k0, nb);
+        }
     }
     PD_LAUNCH_CHECK();
     PD_CUDA(cudaStreamSynchronize(c.stream));
@@ -895,12 +1005,10 @@ void dense_lu_solve(Ctx& c, const DenseLU& f, const double* b, double* x) {
     const int64_t n = f.n;
     if (n == 0) return;
     size_t sm = n * sizeof(double);
-    static bool attr_set = false;
-    if (!attr_set) {
+    // per-device attribute (and cheap): set before every launch that needs it
+    if (sm > 48 * 1024)
         PD_CUDA(cudaFuncSetAttribute(k_lu_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      227 * 1024));
-        attr_set = true;
-    }
     if (sm > 227 * 1024) throw ConfigError("coarsest level too large for the dense solve");
     launch(k_lu_solve, 1, 1024, sm, c.stream, f.lu.p, f.piv.p, n, b, x);
     PD_LAUNCH_CHECK();
@@ -962,12 +1070,9 @@ DevBuf<double> dense_inverse(Ctx& c, const DenseLU& f) {
     const int64_t n = f.n;
     DevBuf<double> inv(std::max<int64_t>(n * n, 1));
     if (n == 0) return inv;
-    static bool attr = false;
-    if (!attr) {
+    if (n * sizeof(double) > 48 * 1024)  // per-device attribute: set whenever it is needed
         PD_CUDA(cudaFuncSetAttribute(k_lu_inverse_cols, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      227 * 1024));
-        attr = true;
-    }
     launch(k_lu_inverse_cols, (unsigned)n, 256, n * sizeof(double), c.stream, f.lu.p, f.piv.p, n,
            inv.p);
     PD_LAUNCH_CHECK();

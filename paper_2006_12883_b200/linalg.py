@@ -254,34 +254,152 @@ class DenseLU:
             pass
 
 
+class BandedLU:
+    """Banded LU with partial pivoting, factored and solved on the device
+    (pd_band.cu) — the drop-in for the SuperLU solves of spacetime.py:154-195.
+
+    ``order`` (optional permutation, band row i = unknown order[i]) reorders the
+    unknowns so that the matrix is banded; vectors passed to ``solve`` stay in the
+    caller's order.  A singular matrix raises SolverError.
+    """
+
+    def __init__(self, A, order=None):
+        self.ctx = N.context()
+        A = as_csr(A)
+        if A.shape[0] != A.shape[1]:
+            raise ConfigurationError("banded LU needs a square matrix")
+        self.n = A.shape[0]
+        perm = None
+        if order is not None:
+            perm = np.ascontiguousarray(order, dtype=np.int32)
+            if perm.shape != (self.n,) or not np.array_equal(np.sort(perm), np.arange(self.n)):
+                raise ConfigurationError("order must be a permutation of the unknowns")
+            A = as_csr(A[perm][:, perm])
+        coo = A.tocoo()
+        off = coo.row.astype(np.int64) - coo.col.astype(np.int64)
+        self.kl = int(max(off.max(), 0)) if off.size else 0
+        self.ku = int(max(-off.min(), 0)) if off.size else 0
+        self._A = DeviceCsr(A, self.ctx)
+        h = ctypes.c_void_p()
+        N.call("pd_band_lu_create", self.ctx.handle, self._A.handle, self.kl, self.ku,
+               perm.ctypes.data_as(ctypes.c_void_p) if perm is not None else None,
+               ctypes.byref(h))
+        self.handle = h
+        self._A = None  # the band copy is all the solve needs
+
+    def solve(self, b):
+        self.ctx.sync_stream()
+        bd = N.to_device(b, self.ctx)
+        if bd.numel() != self.n:
+            raise ConfigurationError(f"right-hand side has {bd.numel()} entries, expected {self.n}")
+        out = N.empty(self.n, self.ctx)
+        N.call("pd_band_lu_solve", self.ctx.handle, self.handle, N.ptr(bd.contiguous()),
+               N.ptr(out))
+        return N.like_input(out, b)
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                N.load_library().pd_band_lu_destroy(self.handle)
+        except Exception:
+            pass
+
+
 def _report_from(rep: N.SolveReportC, hist: np.ndarray) -> SolveReport:
     return SolveReport(iterations=int(rep.iterations), converged=bool(rep.converged),
                        diverged=bool(rep.diverged),
                        residual_history=[float(v) for v in hist[: rep.hist_len]])
 
 
+def _is_device_operator(A) -> bool:
+    return isinstance(A, DeviceCsr) or sp.issparse(A) or isinstance(A, np.ndarray)
+
+
 def gmres(A, b, precond=None, x0=None, tol_rel: float = 1e-9, tol_abs: float = 1e-9,
           restart: int = 30, max_it: int = 1000):
     """Restarted right-preconditioned GMRES on the GPU (linalg.py:215-311).
 
-    ``A``: scipy sparse matrix or DeviceCsr; ``precond``: Ilu0 /
-    BlockJacobiPrecond / None.  Arbitrary Python callables are not accepted
-    (their work could not run on the device).
+    ``A``: scipy sparse matrix / DeviceCsr, or — as in the reference
+    (linalg.py:233-237) — any object with ``.dot`` or a callable matvec;
+    ``precond``: Ilu0 / BlockJacobiPrecond / None, or any object with
+    ``.solve`` or a callable.  Matrices and device factorizations are applied
+    by the device kernels; other callables are invoked from the device GMRES
+    engine through a host callback (numpy in, numpy out — or CUDA tensors when
+    ``b`` is one), with the Krylov vectors and orthogonalisation kept in HBM.
     """
-    if callable(A) and not hasattr(A, "dot"):
-        raise ConfigurationError("device GMRES needs a sparse matrix, not a callable")
-    if precond is not None and not isinstance(precond, Ilu0):
-        raise ConfigurationError("device GMRES preconditioner must be Ilu0/BlockJacobiPrecond")
-    Ad = device_csr(A)
-    ctx = Ad.ctx
+    native_A = _is_device_operator(A)
+    native_M = precond is None or isinstance(precond, Ilu0)
+    if native_A and native_M:
+        Ad = device_csr(A if not isinstance(A, np.ndarray) else sp.csr_matrix(A))
+        ctx = Ad.ctx
+        ctx.sync_stream()
+        bd = N.to_device(b, ctx)
+        n = bd.numel()
+        x0d = N.to_device(x0, ctx) if x0 is not None else None
+        out = N.empty(n, ctx)
+        rep = N.SolveReportC()
+        hist = np.zeros(int(max(max_it, 1)) + 2)
+        N.call("pd_gmres", ctx.handle, Ad.handle, precond.handle if precond is not None else None,
+               N.ptr(bd), N.ptr(x0d), N.ptr(out), float(tol_rel), float(tol_abs), int(restart),
+               int(max_it), ctypes.byref(rep), hist.ctypes.data_as(ctypes.c_void_p), hist.size)
+        return N.like_input(out, b), _report_from(rep, hist)
+    return _gmres_callables(A, b, precond, x0, tol_rel, tol_abs, restart, max_it, native_A,
+                            native_M)
+
+
+def _gmres_callables(A, b, precond, x0, tol_rel, tol_abs, restart, max_it, native_A, native_M):
+    """GMRES whose operator and/or preconditioner is a host callable
+    (pd_gmres_callable): each application hands the callable the engine's
+    current vector and takes its result back through two exchange vectors."""
+    Ad = None
+    if native_A:
+        Ad = device_csr(A if not isinstance(A, np.ndarray) else sp.csr_matrix(A))
+        ctx = Ad.ctx
+    else:
+        ctx = precond.ctx if isinstance(precond, Ilu0) else N.context()
     ctx.sync_stream()
     bd = N.to_device(b, ctx)
     n = bd.numel()
     x0d = N.to_device(x0, ctx) if x0 is not None else None
     out = N.empty(n, ctx)
+    cb_in, cb_out = N.empty(max(n, 1), ctx), N.empty(max(n, 1), ctx)
+    on_device = N.is_tensor(b) and b.is_cuda
+    failure: list[BaseException] = []
+
+    def through(fn):
+        def run(_user):
+            try:
+                arg = cb_in[:n].clone() if on_device else N.to_host(cb_in[:n])
+                res = fn(arg)
+                rd = N.to_device(res if N.is_tensor(res) else np.asarray(res, dtype=np.float64),
+                                 ctx)
+                if rd.numel() != n:
+                    raise ConfigurationError(
+                        f"callable returned {rd.numel()} values for a vector of {n}")
+                cb_out[:n].copy_(rd.reshape(-1))
+                ctx.sync_stream()
+                N.torch_mod().cuda.current_stream().synchronize()
+                return 0
+            except BaseException as exc:  # noqa: BLE001 - re-raised after the C call returns
+                failure.append(exc)
+                return 1
+        return N.APPLY_CB(run)
+
+    matvec_cb = psolve_cb = None
+    if not native_A:
+        matvec_cb = through(A.dot if hasattr(A, "dot") else A)
+    if not native_M:
+        psolve_cb = through(precond.solve if hasattr(precond, "solve") else precond)
     rep = N.SolveReportC()
     hist = np.zeros(int(max(max_it, 1)) + 2)
-    N.call("pd_gmres", ctx.handle, Ad.handle, precond.handle if precond is not None else None,
-           N.ptr(bd), N.ptr(x0d), N.ptr(out), float(tol_rel), float(tol_abs), int(restart),
-           int(max_it), ctypes.byref(rep), hist.ctypes.data_as(ctypes.c_void_p), hist.size)
+    try:
+        N.call("pd_gmres_callable", ctx.handle, int(n), Ad.handle if Ad is not None else None,
+               matvec_cb, precond.handle if (native_M and precond is not None) else None,
+               psolve_cb, None, N.ptr(cb_in), N.ptr(cb_out), N.ptr(bd), N.ptr(x0d), N.ptr(out),
+               float(tol_rel), float(tol_abs), int(restart), int(max_it), ctypes.byref(rep),
+               hist.ctypes.data_as(ctypes.c_void_p), hist.size)
+    except Exception:
+        if failure:
+            raise failure[0]
+        raise
     return N.like_input(out, b), _report_from(rep, hist)

@@ -1,6 +1,6 @@
 """P-fast STMG probes on the device: cycle counts vs Nt, and config 5 (cubic Newton) at size.
 
-    python scripts/pfast_stmg_probe.py flat  [n]        # linear solves, Nt = 32..256 on n^3
+    python scripts/pfast_stmg_probe.py flat  [n] [nu_t] # linear solves, Nt = 32..256 on n^3
     python scripts/pfast_stmg_probe.py c5    [n] [Nt]   # Newton + STMG on the C5 problem
 """
 import sys
@@ -33,8 +33,9 @@ if mode == "flat":
     # keep mu = kappa dt / h^2 of config 5 (6.55) on the n^3 grid
     spec = StencilSpec(3, n, "periodic", 0.1)
     dt = 6.5536 * spec.h ** 2 / 0.1
+    nu_t = int(sys.argv[3]) if len(sys.argv) > 3 else 1
     for Nt in (32, 64, 128, 256):
-        s = PfastStmg(spec, 3, Nt, dt)
+        s = PfastStmg(spec, 3, Nt, dt, nu_t=nu_t)
         b = rhs_for(spec, 3, Nt)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -43,7 +44,7 @@ if mode == "flat":
         t = time.perf_counter() - t0
         line = f"Nt={Nt} levels={[(a, sp.n) for a, sp, _, _ in s.sched]} cycles={rep.iterations} conv={rep.converged} {t:.2f}s"
         del s
-        if Nt <= 64:
+        if Nt <= 64 and nu_t == 1:
             bj = PfastSolver(spec, 3, Nt, dt)
             _, r2 = bj.solve(b, tol_rel=1e-8, max_sweeps=400)
             line += f" | block-Jacobi alone: {r2.iterations} sweeps"

@@ -136,3 +136,67 @@ def test_dense_lu_matches_numpy_and_accepts_dense():
     np.testing.assert_allclose(pd.DenseLU(Ad).solve(b), np.linalg.solve(Ad, b), rtol=1e-12)
     np.testing.assert_allclose(pd.DenseLU(sp.csr_matrix(Ad)).solve(b), np.linalg.solve(Ad, b),
                                rtol=1e-12)
+
+
+def test_gmres_accepts_callables_like_the_reference():
+    """linalg.py:233-237 (test_linalg.py test_matvec_callable_accepted): A may be a
+    callable matvec or any object with .dot, precond any callable / .solve object."""
+    D = np.diag([2.0, 3.0, 4.0])
+    x, rep = pd.gmres(lambda v: D @ v, np.array([2.0, 3.0, 4.0]))
+    assert rep.converged
+    np.testing.assert_allclose(x, 1.0, atol=1e-10)
+
+    # callable operator + callable preconditioner vs the oracle's GMRES on the same pair:
+    # equal iteration counts and histories
+    A = _random_spd(80, 0.06, 5)
+    b = np.cos(np.arange(80.0))
+    dinv = 1.0 / A.diagonal()
+    calls = {"A": 0, "M": 0}
+
+    def mv(v):
+        calls["A"] += 1
+        return A @ v
+
+    def ps(v):
+        calls["M"] += 1
+        return dinv * v
+
+    x, rep = pd.gmres(mv, b, precond=ps, tol_rel=1e-11, tol_abs=0.0, restart=10)
+    xo, repo = O.gmres(A, b, ps, tol_rel=1e-11, tol_abs=0.0, restart=10)
+    assert rep.converged and rep.iterations == repo.iterations
+    assert calls["A"] > rep.iterations and calls["M"] >= rep.iterations
+    np.testing.assert_allclose(rep.residual_history, repo.residual_history, rtol=1e-6, atol=1e-13)
+    assert np.linalg.norm(x - xo) <= 1e-10 * np.linalg.norm(xo)
+
+    # mixed: device matrix with a callable preconditioner; callable operator with device ILU(0)
+    x1, rep1 = pd.gmres(A, b, precond=ps, tol_rel=1e-11, tol_abs=0.0, restart=10)
+    assert rep1.iterations == repo.iterations and np.linalg.norm(x1 - xo) <= 1e-10 * np.linalg.norm(xo)
+    ilu = pd.Ilu0(A)
+    x2, rep2 = pd.gmres(mv, b, precond=ilu, tol_rel=1e-11, tol_abs=0.0)
+    x3, rep3 = pd.gmres(A, b, precond=ilu, tol_rel=1e-11, tol_abs=0.0)
+    assert rep2.iterations == rep3.iterations
+    assert np.linalg.norm(x2 - x3) <= 1e-12 * np.linalg.norm(x3)
+
+    # an object with .dot / .solve (e.g. a LinearOperator-like wrapper)
+    class Op:
+        def dot(self, v):
+            return A @ v
+
+    class Pre:
+        def solve(self, v):
+            return dinv * v
+
+    x4, rep4 = pd.gmres(Op(), b, precond=Pre(), x0=np.ones(80), tol_rel=1e-11, tol_abs=0.0)
+    xo4, repo4 = O.gmres(A, b, ps, x0=np.ones(80), tol_rel=1e-11, tol_abs=0.0)
+    assert rep4.iterations == repo4.iterations
+    assert np.linalg.norm(x4 - xo4) <= 1e-10 * np.linalg.norm(xo4)
+
+    # an exception inside the callable surfaces unchanged
+    def bad(v):
+        raise ValueError("user matvec failed")
+
+    with pytest.raises(ValueError, match="user matvec failed"):
+        pd.gmres(bad, b)
+    # a wrong-sized result is a configuration error
+    with pytest.raises(pd.ConfigurationError):
+        pd.gmres(lambda v: np.zeros(3), b)
