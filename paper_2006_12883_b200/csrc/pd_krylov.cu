@@ -156,7 +156,9 @@ __global__ void k_gm_arnoldi(GmDev* s, int slot, double* hist) {
     s->total += 1;
     s->last_res = res;
     if (hist) hist[s->total] = res;
-    if (res <= s->thr || happy || s->total >= s->max_it) {
+    // the cycle ends on convergence, breakdown, the iteration cap — or when the inner
+    // loop `for j in range(restart)` (linalg.py:264) runs out
+    if (res <= s->thr || happy || s->total >= s->max_it || j + 1 >= R) {
         s->k = j + 1;
         s->phase = GM_FINISH;
         // the closing true residual decides restarts and the report; a smoother
@@ -388,6 +390,32 @@ const GmDev& Gmres::read_state() {
     return *host_st;
 }
 
+void Gmres::debug_dump(int slot) {
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    auto full = std::make_unique<GmDev>();
+    PD_CUDA(cudaMemcpy(full.get(), st.p, sizeof(GmDev), cudaMemcpyDeviceToHost));
+    const GmDev& s = *full;
+    fprintf(stderr, "[gm] slot %d phase %d j %d k %d total %d cycles %d final_res %d beta %.6g hn %.6g\n",
+            slot, s.phase, s.j, s.k, s.total, s.cycles, s.final_res, s.beta, s.hn);
+    fprintf(stderr, "     g %.6g %.6g %.6g  y %.6g %.6g  H00 %.6g H10 %.6g dots %.6g %.6g %.6g\n", s.g[0],
+            s.g[1], s.g[2], s.y[0], s.y[1], s.H[0], s.H[s.restart], s.dots[0], s.dots[1], s.dots[2]);
+    const int m = (int)std::min<int64_t>(n, 6);
+    auto show = [&](const char* name, const double* p) {
+        double h[6] = {0};
+        PD_CUDA(cudaMemcpy(h, p, m * sizeof(double), cudaMemcpyDeviceToHost));
+        fprintf(stderr, "     %-5s", name);
+        for (int i = 0; i < m; ++i) fprintf(stderr, " %.6g", h[i]);
+        fprintf(stderr, "\n");
+    };
+    show("V0", V.p);
+    show("V1", V.p + n);
+    show("vcur", vcur.p);
+    show("w", w.p);
+    show("u", u.p);
+    show("xg", xg.p);
+    show("rg", rg.p);
+}
+
 std::vector<double> Gmres::history(int total) {
     std::vector<double> h(total + 1);
     PD_CUDA(cudaMemcpyAsync(h.data(), hist.p, (total + 1) * sizeof(double), cudaMemcpyDeviceToHost,
@@ -433,6 +461,7 @@ GmresResult gmres_run(Ctx& c, const Csr& A, Ilu0* M, const double* b, const doub
         const int j_eff = (s.phase == GM_START) ? 0 : s.j;
         g.enqueue_slot(slot++, j_eff + 2, b);
         g.read_state();
+        if (getenv("PD_GM_DEBUG")) g.debug_dump(slot - 1);
     }
     if (s.err == 1) throw SolverError("non-finite initial residual in GMRES");
     if (s.err == 2) throw SolverError("non-finite residual in GMRES iteration");

@@ -48,6 +48,7 @@ class Gmres {
     GmDev* dev() { return st.p; }
     void set_operator(const StOp* o) { op = o; }
     std::vector<double> history(int total);
+    void debug_dump(int slot);  // PD_GM_DEBUG: state and leading vector entries to stderr
 
    private:
     Ctx& c;

@@ -56,6 +56,8 @@ def test_gmres_matches_reference(golden):
                         restart=5, max_it=200)
     assert rep2.iterations == int(g["gm2_its"])
     assert rel_l2(x2, g["gm2_x"]) < 1e-10
+    # restart=5 over 16 iterations: every cycle's estimates match the reference's
+    np.testing.assert_allclose(rep2.residual_history[:-1], g["gm2_hist"][:-1], rtol=1e-5)
 
 
 def test_gmres_x0_and_unpreconditioned():
