@@ -195,7 +195,8 @@ int pd_sdc_chain(void *lvl, double *U, double *U0, const double *tau, int W, con
 int pd_sdc_residual(void *lvl, const double *U, const double *U0, const double *tau, int W,
                     double *res_dev);                            /* :107-115, per worker */
 int pd_sdc_coll_op(void *lvl, const double *U, double *out, int W); /* C(u) = u - dt Q F(u) */
-int pd_sdc_errors(void *lvl, int *host_out);                        /* synchronising */
+int pd_sdc_errors(void *lvl, int *host_out); /* synchronising; host_out[0] = failure
+ * kinds (0 none), host_out[1] = lowest failing worker of the batch (-1 none); clears */
 int pd_node_mix(void *ctx, const double *in, double *out, int W, int Min, int Mout, int64_t S,
                 const double *N_host, int accumulate);           /* node transfer :262-266 */
 int pd_csr_spmm(void *ctx, void *A, const double *x, int64_t xs, double *y, int64_t ys,

@@ -222,13 +222,22 @@ __global__ void k_add_to(double* out, const double* a, const double* b, int64_t 
         out[i] = add(a[i], b[i]);
 }
 
+// Error word of an SDC level: err[0] = OR of failure kinds (1 non-finite values, 2 zero
+// pivot, 4 node solve failed, 8 node solve at its iteration cap), err[1] = the lowest
+// worker that failed (the window driver needs it: pfasst.py:471-507 counts an iteration
+// only for workers that finished it), err[2] = index of the batch's first worker.
+__device__ __forceinline__ void flag_err(int* err, int bit, int w) {
+    atomicOr(err, bit);
+    atomicMin(err + 1, w + err[2]);
+}
+__global__ void k_err_base(int* err, int base) { err[2] = base; }
+
 // base[w][m] = U0[w] + dt*(sum_j A[m][j] f1[w][j] + sum_j B[m][j] f2[w][j]) (+ tau)
 // (pfasst.py:170-178); f2 may be null (non-IMEX).  Flags non-finite entries.
 __global__ void k_sdc_base(const double* U0, const double* f1, const double* f2,
                            const double* tau, double* base, int W, int M, int64_t S, double dt,
                            Small A, Small B, int* err) {
     const int64_t tot = (int64_t)W * M * S;
-    bool bad = false;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = t % S;
@@ -247,9 +256,8 @@ __global__ void k_sdc_base(const double* U0, const double* f1, const double* f2,
         double v = add(U0[w * S + s], mul(dt, acc));
         if (tau) v = add(v, tau[t]);
         base[t] = v;
-        if (!isfinite(v)) bad = true;
+        if (!isfinite(v)) flag_err(err, 1, (int)w);
     }
-    if (bad) atomicOr(err, 1);
 }
 
 // b[w] = mh * (base[w][m] + sum_{j<m} dt*qdi[m][j]*fi[w][j] (+ dt*qde[m][j]*fe[w][j]))
@@ -458,7 +466,7 @@ __global__ void k_refine_check(const double* rn, const double* bn, double* beta0
         beta0[w] = beta;
         if (!isfinite(beta)) {
             done[w] = 1;
-            atomicOr(err, 4);
+            flag_err(err, 4, w);
             return;
         }
         const double t = fmax(mul(tol, fmax(1.0, bn[w])), mul(tol, beta));
@@ -470,7 +478,7 @@ __global__ void k_refine_check(const double* rn, const double* bn, double* beta0
     if (done[w]) return;
     if (!isfinite(beta) || beta > mul(10.0, lowest[w])) {
         done[w] = 1;
-        atomicOr(err, 4);
+        flag_err(err, 4, w);
         return;
     }
     lowest[w] = fmin(lowest[w], beta);
@@ -493,7 +501,7 @@ __global__ void k_count_open(const int* done, int W, int* count) {
 
 __global__ void k_any_open(const int* done, int W, int* err) {
     const int w = blockIdx.x * blockDim.x + threadIdx.x;
-    if (w < W && !done[w]) atomicOr(err, 8);
+    if (w < W && !done[w]) flag_err(err, 8, w);
 }
 
 // collocation residual / C(u):  R = U - U0 - dt*Q*F - tau ;  C = U - dt*Q*F
@@ -576,7 +584,8 @@ __device__ void node_newton_tri_worker(const int64_t* __restrict__ rp,
                                        const double* __restrict__ mh, int64_t S, double q,
                                        double gamma, int kind, const double* __restrict__ b,
                                        double* x, double* gbuf, double* lbuf, double* ubuf, int w,
-                                       int* err) {
+                                       int* err, int wflag = -1) {
+    if (wflag < 0) wflag = w;
     const double* bw = b + (int64_t)w * S;
     double* u = x + (int64_t)w * S;
     double* g = gbuf + (int64_t)w * S;
@@ -596,7 +605,7 @@ __device__ void node_newton_tri_worker(const int64_t* __restrict__ rp,
             gn = fma(gj, gj, gn);
         }
         if (!(sqrt(gn) > mul(1e-12, scale))) {
-            if (!isfinite(gn)) atomicOr(err, 4);
+            if (!isfinite(gn)) flag_err(err, 4, wflag);
             return;
         }
         // Thomas on J delta = -g (J tridiagonal; entries rebuilt per row)
@@ -628,7 +637,7 @@ __device__ void node_newton_tri_worker(const int64_t* __restrict__ rp,
             u[j] = add(u[j], xn);
         }
     }
-    atomicOr(err, 4);
+    flag_err(err, 4, wflag);
 }
 
 __global__ void k_node_newton_tri(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
@@ -948,7 +957,7 @@ __device__ void fused_sweep_worker(const FusedSweep& F, double* U, const double*
         bas[idx] = v;
         if (!isfinite(v)) bad = true;
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(F.err, 1);
+    if (__any_sync(0xffffffffu, bad) && lane == 0) flag_err(F.err, 1, w);
     __syncwarp();
     for (int m = 0; m < M; ++m) {
         for (int64_t j = lane; j < S; j += 32) {
@@ -964,7 +973,7 @@ __device__ void fused_sweep_worker(const FusedSweep& F, double* U, const double*
         if (F.gamma != 0.0 && !imex) {
             if (lane == 0)
                 node_newton_tri_worker(F.krp, F.kci, F.kv, F.mh, S, mul(F.dt, F.QDI.a[m * M + m]),
-                                       F.gamma, F.kind, b, x, r, fio, feo, 0, F.err);
+                                       F.gamma, F.kind, b, x, r, fio, feo, 0, F.err, w);
             __syncwarp();
         } else {
             const double* am = F.av + (int64_t)m * F.annz;
@@ -1013,14 +1022,14 @@ __device__ void fused_sweep_worker(const FusedSweep& F, double* U, const double*
                 }
                 beta = sqrt(warp_sum(beta));
                 if (!isfinite(beta) || beta > mul(10.0, lowest)) {
-                    if (lane == 0) atomicOr(F.err, 4);
+                    if (lane == 0) flag_err(F.err, 4, w);
                     done = true;
                     break;
                 }
                 lowest = fmin(lowest, beta);
                 done = !(beta > thr);
             }
-            if (!done && lane == 0) atomicOr(F.err, 8);
+            if (!done && lane == 0) flag_err(F.err, 8, w);
             __syncwarp();
         }
         // U[m] = x ; f of the new node value
@@ -1345,8 +1354,11 @@ int pd_sdc_level_create(void* ctx, void* Kh, const double* mh_host, int M, const
         for (int m = 0; m < M; ++m)
             PD_CUDA(cudaMemcpy(L->Aval.p + (int64_t)m * K->nnz, L->Am[m]->val.p,
                                K->nnz * sizeof(double), cudaMemcpyDeviceToDevice));
-        L->err.alloc(1);
-        PD_CUDA(cudaMemset(L->err.p, 0, sizeof(int)));
+        L->err.alloc(3);
+        {
+            const int init[3] = {0, INT_MAX, 0};
+            PD_CUDA(cudaMemcpy(L->err.p, init, sizeof(init), cudaMemcpyHostToDevice));
+        }
         L->open_count.alloc(1);
         if (tri) {
             L->tl.alloc(M * S);
@@ -1410,10 +1422,12 @@ int pd_sdc_chain(void* lvl, double* U, double* U0, const double* tau, int W, con
                 const double* src = w == 0 ? u0c : U + (int64_t)(w - 1) * MS + (L.M - 1) * S;
                 PD_CUDA(cudaMemcpyAsync(U0 + (int64_t)w * S, src, S * sizeof(double),
                                         cudaMemcpyDeviceToDevice, c.stream));
+                pd::launch(pd::k_err_base, 1, 1, 0, c.stream, L.err.p, w);
                 for (int k = 0; k < nu; ++k)
                     pd::sdc_sweep(L, U + w * MS, U0 + (int64_t)w * S,
                                   tau ? tau + w * MS : nullptr, 1);
             }
+            pd::launch(pd::k_err_base, 1, 1, 0, c.stream, L.err.p, 0);
         };
         // The chain is W sequential one-worker sweeps of ~100 small launches each:
         // launch-bound.  Without host synchronisation inside (spectral / dense /
@@ -1493,9 +1507,14 @@ int pd_sdc_coll_op(void* lvl, const double* U, double* out, int W) {
 int pd_sdc_errors(void* lvl, int* host_out) {
     return guarded_sdc([&] {
         auto& L = *static_cast<pd::SdcLevelDev*>(lvl);
-        PD_CUDA(cudaMemcpyAsync(host_out, L.err.p, sizeof(int), cudaMemcpyDeviceToHost, L.c.stream));
+        int h[2] = {0, 0};
+        PD_CUDA(cudaMemcpyAsync(h, L.err.p, sizeof(h), cudaMemcpyDeviceToHost, L.c.stream));
         PD_CUDA(cudaStreamSynchronize(L.c.stream));
-        PD_CUDA(cudaMemsetAsync(L.err.p, 0, sizeof(int), L.c.stream));
+        host_out[0] = h[0];
+        host_out[1] = h[0] ? h[1] : -1;
+        const int init[2] = {0, INT_MAX};
+        PD_CUDA(cudaMemcpyAsync(L.err.p, init, sizeof(init), cudaMemcpyHostToDevice, L.c.stream));
+        PD_CUDA(cudaStreamSynchronize(L.c.stream));
     });
 }
 

@@ -149,11 +149,16 @@ class SdcLevel:
             pass
 
     def check_errors(self):
-        e = ctypes.c_int()
-        N.call("pd_sdc_errors", self._dev, ctypes.byref(e))
-        if e.value:
-            bit = next(b for b in (1, 2, 4, 8) if e.value & b)
-            raise SolverError(_ERR_TEXT[bit])
+        """Raise the device-side failure of this level, if any; the exception's `worker`
+        is the lowest failing worker of the batch (the window driver counts an
+        iteration only for the workers before it, pfasst.py:471-507)."""
+        e = (ctypes.c_int * 2)()
+        N.call("pd_sdc_errors", self._dev, e)
+        if e[0]:
+            bit = next(b for b in (1, 2, 4, 8) if e[0] & b)
+            err = SolverError(_ERR_TEXT[bit])
+            err.worker = int(e[1])
+            raise err
 
     # ---- batched device primitives (W workers) --------------------------------
     def sweep_dev(self, U, U0, tau, W: int, w_off: int = 0):
@@ -565,8 +570,16 @@ class GpuPfasstEngine:
             self._c("pd_scale", _vp(self.halo_out[l]), _vp(self.msgs[l], (self.W - 1) * S), 1.0, S)
         lv[0].residual_dev(self.U[0], self.U0[0], None, self.W, self.res)
         r = self.res.cpu().numpy()
-        for lev in lv:
-            lev.check_errors()
+        first = None
+        for lev in lv:  # read (and clear) every level's flags; report the lowest worker
+            try:
+                lev.check_errors()
+            except SolverError as e:
+                if first is None or getattr(e, "worker", 0) < getattr(first, "worker", 0):
+                    first = e
+        if first is not None:
+            first.worker = self.w0 + max(getattr(first, "worker", 0), 0)
+            raise first
         return r
 
     def store_window(self, start):

@@ -162,6 +162,9 @@ def run_windows(engine, comm, Nt: int, P: int, tol_rel: float, tol_abs: float,
                         return fn(*a)
                     except SolverError as e:
                         state["failed"] = True
+                        # global index of the first failing worker (0 when unknown)
+                        state["worker"] = min(state.get("worker", 1 << 30),
+                                              max(int(getattr(e, "worker", 0)), 0))
                         if os.environ.get("PD_PFASST_VERBOSE"):
                             print(f"[pfasst] window iteration {k}: {fn.__name__}: {e}",
                                   file=sys.stderr, flush=True)
@@ -192,8 +195,12 @@ def run_windows(engine, comm, Nt: int, P: int, tol_rel: float, tol_abs: float,
                 red = comm.allreduce_max([
                     float(np.max(res)) if np.all(np.isfinite(res)) else np.inf,
                     1.0 if (state["failed"] or bad.any()) else 0.0,
-                    1.0 if np.any(~(res <= threshold)) else 0.0])
-                iters = k
+                    1.0 if np.any(~(res <= threshold)) else 0.0,
+                    -float(state["worker"]) if state["failed"] else -np.inf])
+                # pfasst.py:471-507: a worker counts iteration k once it has published;
+                # after a SolverError in worker f the workers before f still finish k,
+                # f and its successors (stranded in the coarse chain) stay at k - 1
+                iters = k if (red[3] == -np.inf or -red[3] > 0) else k - 1
                 res_max = float(red[0])
                 if red[1] > 0:
                     diverged = True
