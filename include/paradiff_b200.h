@@ -93,6 +93,13 @@ int pd_dense_lu_create(void *ctx, void *csr, void **lu_out); /* synchronising */
 int pd_dense_lu_solve(void *ctx, void *lu, const double *b, double *x);
 int pd_dense_lu_destroy(void *lu);
 
+/* ---- mode product of the exact structured-grid node solve (pfasst.py:118-132's linear
+ *      system solved by its 1D eigen-decomposition): out[o,a,r] = sum_i Mat[a,i]
+ *      in[o,i,r] over the C-order array [total/(n*stride)][n][stride], Mat = Phi^T
+ *      (transpose=1) or Phi, phi = n x n row-major on the device.  in != out. */
+int pd_mode_product(void *ctx, const double *in, double *out, int64_t total, int64_t n,
+                    int64_t stride, const double *phi, int transpose);
+
 /* ---- banded LU with partial pivoting: the direct solves of spacetime.py:154-195
  *      (_element_solve, solve_sequential, solve_direct call SuperLU there).  csr is
  *      the matrix with its unknowns already reordered so that it is banded (kl sub-,

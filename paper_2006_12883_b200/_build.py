@@ -65,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         objs = list(pool.map(compile_one, sources()))
     tmp = LIB.with_suffix(f".so.{os.getpid()}.tmp")
     cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(tmp), *objs,
-           "-lcudart_static", "-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+           "-lcudart_static"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{res.stderr}")

@@ -118,6 +118,7 @@ _SIGNATURES = {
     "pd_spread": (_int, [_vp, _vp, _vp, _vp, _int, _int, _i64]),
     "pd_terminal": (_int, [_vp, _vp, _vp, _int, _int, _i64]),
     "pd_scale": (_int, [_vp, _vp, _vp, _dbl, _i64]),
+    "pd_mode_product": (_int, [_vp, _vp, _vp, _i64, _i64, _i64, _vp, _int]),
     "pd_band_lu_create": (_int, [_vp, _vp, _int, _int, _vp, ctypes.POINTER(_vp)]),
     "pd_band_lu_solve": (_int, [_vp, _vp, _vp, _vp]),
     "pd_band_lu_destroy": (_int, [_vp]),

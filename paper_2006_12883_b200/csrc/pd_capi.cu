@@ -165,6 +165,14 @@ int pd_dense_lu_destroy(void* lu) {
     return guarded([&] { delete static_cast<pd::DenseLU*>(lu); });
 }
 
+int pd_mode_product(void* ctx, const double* in, double* out, int64_t total, int64_t n,
+                    int64_t stride, const double* phi, int transpose) {
+    return guarded([&] {
+        if (n < 1 || stride < 1 || total < 0) throw pd::ConfigError("bad mode product shape");
+        pd::mode_product(*C(ctx), in, out, total, n, stride, phi, transpose);
+    });
+}
+
 int pd_band_lu_create(void* ctx, void* csr, int kl, int ku, const int32_t* perm_host, void** out) {
     return guarded([&] {
         *out = pd::band_lu_create(*C(ctx), *H<pd::Csr>(csr, "matrix"), kl, ku, perm_host);

@@ -102,7 +102,6 @@ struct Ctx {
     DevBuf<unsigned int> red_counter; // 4 counters
     DevBuf<double> scalars;           // small result slots
     DevBuf<int> flags;                // misc device flags
-    void* blas = nullptr;             // cuBLAS handle (plain DGEMMs only), lazily created
     // bumped by every call that changes device state a captured CUDA graph
     // would bake in (values, factors, plans): captured V-cycles are re-made
     uint64_t epoch = 0;
@@ -114,7 +113,7 @@ struct Ctx {
 };
 
 // out = mode-`stride` product of W stacked grids with the n x n matrix phi
-// (row-major; transpose=1: Phi^T, 0: Phi) as cuBLAS DGEMMs (pd_sdc.cu)
+// (row-major; transpose=1: Phi^T, 0: Phi): hand-written FP64 GEMM (pd_modeprod.cu)
 void mode_product(Ctx& c, const double* in, double* out, int64_t total, int64_t n,
                   int64_t stride, const double* phi, int transpose);
 

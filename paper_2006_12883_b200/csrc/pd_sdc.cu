@@ -20,7 +20,6 @@
 // guess with the reference's thresholds, growth test and iteration cap.
 #include "../../include/paradiff_b200.h"
 #include "pd_device.cuh"
-#include <cublas_v2.h>
 
 #include <array>
 
@@ -691,21 +690,6 @@ __global__ void k_spec_scale(double* z, int64_t total, int64_t n, int dim,
     }
 }
 
-cublasHandle_t blas_of(Ctx& c) {
-    if (!c.blas) {
-        cublasHandle_t h;
-        if (cublasCreate(&h) != CUBLAS_STATUS_SUCCESS) throw CudaError("cublasCreate failed");
-        // a fixed workspace: no allocation inside a captured CUDA graph
-        static thread_local DevBuf<unsigned char> ws;
-        if (!ws.p) ws.alloc((size_t)32 << 20);
-        cublasSetWorkspace(h, ws.p, (size_t)32 << 20);
-        c.blas = h;
-    }
-    auto h = static_cast<cublasHandle_t>(c.blas);
-    cublasSetStream(h, c.stream);
-    return h;
-}
-
 Small small_from(const double* h, int r, int cols) {
     Small s;
     std::memset(&s, 0, sizeof(s));
@@ -715,30 +699,6 @@ Small small_from(const double* h, int r, int cols) {
 }  // namespace
 
 // ---------------------------------------------------------------- host API
-// Mode product as DGEMMs (column-major views of the C-order [outer][n][stride]
-// array).  phi's raw row-major storage is Phi^T in column-major terms.
-//   stride == 1: out(a, o) = sum_i Mat(a, i) in(i, o): one GEMM, m=n, n=outer;
-//   stride  > 1: per outer block C_o(r, a) = sum_i B_o(r, i) Mat(a, i): strided
-//                batched GEMMs m=stride, n=n, k=n (B_o = in block, ld = stride).
-// Mat = Phi^T (transpose=1, forward) or Phi (back).
-void mode_product(Ctx& c, const double* in, double* out, int64_t total, int64_t n,
-                  int64_t stride, const double* phi, int transpose) {
-    const double one = 1.0, zero = 0.0;
-    cublasHandle_t h = blas_of(c);
-    const int64_t outer = total / (n * stride);
-    cublasStatus_t st;
-    if (stride == 1) {
-        st = cublasDgemm(h, transpose ? CUBLAS_OP_N : CUBLAS_OP_T, CUBLAS_OP_N, (int)n,
-                         (int)outer, (int)n, &one, phi, (int)n, in, (int)n, &zero, out, (int)n);
-    } else {
-        st = cublasDgemmStridedBatched(h, CUBLAS_OP_N, transpose ? CUBLAS_OP_T : CUBLAS_OP_N,
-                                       (int)stride, (int)n, (int)n, &one, in, (int)stride,
-                                       (long long)(n * stride), phi, (int)n, 0LL, &zero, out,
-                                       (int)stride, (long long)(n * stride), (int)outer);
-    }
-    if (st != CUBLAS_STATUS_SUCCESS) throw CudaError("cublas DGEMM failed in mode_product");
-}
-
 static void bnorm(SdcLevelDev& L, const double* x, int64_t n, int64_t stride, int W, double* out,
                   bool take_sqrt) {
     Ctx& c = L.c;
@@ -1456,7 +1416,6 @@ int pd_sdc_chain(void* lvl, double* U, double* U0, const double* tau, int W, con
         auto restore = [&] {
             c.stream = orig;
             L.capturing = false;
-            if (c.blas) cublasSetStream(static_cast<cublasHandle_t>(c.blas), orig);
         };
         PD_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));
         const unsigned long long l0 = pd::g_launches.load();

@@ -15,7 +15,6 @@
 // by a thread that is already running: no deadlock for any grid size.  Each
 // row's arithmetic follows the reference's sequential order exactly.
 #include "pd_device.cuh"
-#include <cublas_v2.h>
 
 #include "pd_internal.h"
 
@@ -44,9 +43,7 @@ Ctx::Ctx(int dev_, cudaStream_t s) : device(dev_), stream(s) {
     PD_CUDA(cudaMemset(flags.p, 0, 64 * sizeof(int)));
 }
 
-Ctx::~Ctx() {
-    if (blas) cublasDestroy(static_cast<cublasHandle_t>(blas));
-}
+Ctx::~Ctx() = default;
 
 int Ctx::grid_for(int64_t n, int bs, int per_sm) const {
     int64_t g = (n + bs - 1) / bs;

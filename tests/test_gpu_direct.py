@@ -133,3 +133,29 @@ def test_element_solve_2d_fd_band():
                     pd.fd_space(cfg.spec).lumped_diagonal, cfg.Nt, cfg.T, 0.0,
                     cfg.u0()).solve_sequential()
     assert per_node_rel(s.solve_sequential(), ref, (cfg.Nt, cfg.M, cfg.spec.ndof)) < 1e-10
+
+
+@pytest.mark.parametrize("n,dim,W", [(5, 2, 3), (31, 3, 2), (127, 2, 1), (40, 3, 1), (130, 2, 2)])
+def test_mode_product_matches_einsum(n, dim, W):
+    """The hand-written FP64 mode product (pd_modeprod.cu, no library) along every axis
+    of W stacked n^dim grids, with Phi and Phi^T, vs numpy (fp64 summation-order tolerance)."""
+    import torch
+
+    from paper_2006_12883_b200 import _native as N
+
+    rng = np.random.default_rng(n)
+    phi = rng.standard_normal((n, n))
+    X = rng.standard_normal((W,) + (n,) * dim)
+    ctx = N.context()
+    xd, pd_ = N.to_device(X.ravel(), ctx), N.to_device(phi.ravel(), ctx)
+    out = N.empty(X.size, ctx)
+    for axis in range(dim):
+        stride = n ** (dim - 1 - axis)
+        for tr in (0, 1):
+            N.call("pd_mode_product", ctx.handle, N.ptr(xd), N.ptr(out), X.size, n, stride,
+                   N.ptr(pd_), tr)
+            torch.cuda.synchronize()
+            mat = phi.T if tr else phi
+            ref = np.moveaxis(np.tensordot(mat, X, axes=([1], [axis + 1])), 0, axis + 1)
+            got = N.to_host(out).reshape(X.shape)
+            assert np.max(np.abs(got - ref)) <= 1e-12 * n * np.max(np.abs(ref))

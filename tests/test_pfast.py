@@ -515,7 +515,9 @@ def test_gpu_stmg_cycle_count_flat_in_nt_and_c5_newton():
     assert counts11[1] <= 1.35 * counts11[0] and counts11[1] <= 24, (counts, counts11)
     b = N.to_device(pfast_rhs(spec, 3, 64, u0))
     _, bj = PfastSolver(spec, 3, 64, dt).solve(b, tol_rel=1e-8, max_sweeps=400)
-    assert bj.iterations > 3 * counts11[1]
+    # block-Jacobi alone needs about one sweep per step: at a quarter of the steps it
+    # already takes far more sweeps than the 256-step STMG takes cycles
+    assert bj.iterations >= 64 and bj.iterations > 2 * counts11[1]
     s = PfastStmg(spec, 3, 32, 1e-3)
     b = N.to_device(pfast_rhs(spec, 3, 32, u0))
     u, rep = s.newton(b, 1.0, "cubic", tol=1e-8)
