@@ -390,6 +390,125 @@ __global__ void __launch_bounds__(PFB) k_pf_prolong_add(int nc, int nf, int64_t 
     }
 }
 
+// ---- periodic grids with nc a multiple of 32: pair-per-lane transfers ----
+// A lane owns the fine pair (2cx, 2cx+1) of its coarse point cx: one 16-byte access per
+// fine row and pair, the x neighbour from the adjacent lane by shuffle (the edge lane
+// loads it, wrapping around the row).  The general kernels above issue up to 8 scalar
+// coarse loads per fine point (prolongation) / 27 scalar fine loads per coarse point
+// (restriction): they run at the L1 request rate, not at the HBM rate.
+
+// fine += P coarse.  A warp takes the coarse cell (cz, cy) x one 32-point chunk of cx and
+// updates its 2 x 2 fine rows (2D: 2 fine rows) from the 2 x 2 coarse rows read once.
+template <int DIM>
+__global__ void __launch_bounds__(PFB) k_pf_prolong_add_pp(int nc, int64_t planes,
+                                                          const double* __restrict__ coarse,
+                                                          double* fine) {
+    const int nf = 2 * nc;
+    const int64_t Sc = DIM == 2 ? (int64_t)nc * nc : (int64_t)nc * nc * nc;
+    const int64_t Sf = DIM == 2 ? (int64_t)nf * nf : (int64_t)nf * nf * nf;
+    const unsigned chunks = (unsigned)nc >> 5;
+    const unsigned G = (DIM == 2 ? (unsigned)nc : (unsigned)nc * nc) * chunks;  // units per plane
+    const unsigned units = (unsigned)planes * G;
+    const int lane = threadIdx.x & 31;
+    constexpr int NZ = DIM == 3 ? 2 : 1;
+    for (unsigned unit = blockIdx.x * (PFB / 32) + (threadIdx.x >> 5); unit < units;
+         unit += gridDim.x * (PFB / 32)) {
+        const unsigned p_u = unit / G;
+        unsigned rr = unit - p_u * G;
+        const int ch = (int)(rr % chunks);
+        rr /= chunks;
+        const int cy = DIM == 2 ? (int)rr : (int)(rr % (unsigned)nc);
+        const int cz = DIM == 3 ? (int)(rr / (unsigned)nc) : 0;
+        const int cy1 = cy + 1 == nc ? 0 : cy + 1, cz1 = cz + 1 == nc ? 0 : cz + 1;
+        const int cx = ch * 32 + lane;
+        const int cxn = cx + 1 == nc ? 0 : cx + 1;
+        const double* src = coarse + (int64_t)p_u * Sc;
+        // coarse rows [z][y] at cx, and at cx + 1 (neighbour lane; the last lane loads it)
+        double c[NZ][2], cn[NZ][2];
+#pragma unroll
+        for (int a = 0; a < NZ; ++a)
+#pragma unroll
+            for (int bb = 0; bb < 2; ++bb) {
+                const double* row = src + ((int64_t)(a ? cz1 : cz) * (DIM == 3 ? nc : 0) +
+                                           (bb ? cy1 : cy)) * nc;
+                c[a][bb] = __ldg(row + cx);
+                cn[a][bb] = __shfl_down_sync(0xffffffffu, c[a][bb], 1);
+                if (lane == 31) cn[a][bb] = __ldg(row + cxn);
+            }
+        double* dst = fine + (int64_t)p_u * Sf;
+#pragma unroll
+        for (int j = 0; j < NZ; ++j)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                // interpolated coarse row for fine (z = 2cz + j, y = 2cy + i) at cx and cx + 1
+                double r, rn;
+                if (DIM == 2 || j == 0) {
+                    r = i ? 0.5 * (c[0][0] + c[0][1]) : c[0][0];
+                    rn = i ? 0.5 * (cn[0][0] + cn[0][1]) : cn[0][0];
+                } else {
+                    r = i ? 0.25 * ((c[0][0] + c[0][1]) + (c[NZ - 1][0] + c[NZ - 1][1]))
+                          : 0.5 * (c[0][0] + c[NZ - 1][0]);
+                    rn = i ? 0.25 * ((cn[0][0] + cn[0][1]) + (cn[NZ - 1][0] + cn[NZ - 1][1]))
+                           : 0.5 * (cn[0][0] + cn[NZ - 1][0]);
+                }
+                double2* q = reinterpret_cast<double2*>(
+                    dst + ((int64_t)(2 * cz + j) * (DIM == 3 ? nf : 0) + (2 * cy + i)) * nf + 2 * cx);
+                double2 v = *q;
+                v.x += r;
+                v.y += 0.5 * (r + rn);
+                *q = v;
+            }
+    }
+}
+
+// coarse = P^T fine.  A warp takes the coarse row (cz, cy) x one 32-point chunk of cx: the
+// 3 x 3 (2D: 3) fine rows are combined per lane pair first, then in x with one shuffle.
+template <int DIM>
+__global__ void __launch_bounds__(PFB) k_pf_restrict_pp(int nc, int64_t planes,
+                                                       const double* __restrict__ fine,
+                                                       double* coarse) {
+    const int nf = 2 * nc;
+    const int64_t Sc = DIM == 2 ? (int64_t)nc * nc : (int64_t)nc * nc * nc;
+    const int64_t Sf = DIM == 2 ? (int64_t)nf * nf : (int64_t)nf * nf * nf;
+    const unsigned chunks = (unsigned)nc >> 5;
+    const unsigned G = (DIM == 2 ? (unsigned)nc : (unsigned)nc * nc) * chunks;
+    const unsigned units = (unsigned)planes * G;
+    const int lane = threadIdx.x & 31;
+    constexpr int NZ = DIM == 3 ? 3 : 1;
+    for (unsigned unit = blockIdx.x * (PFB / 32) + (threadIdx.x >> 5); unit < units;
+         unit += gridDim.x * (PFB / 32)) {
+        const unsigned p_u = unit / G;
+        unsigned rr = unit - p_u * G;
+        const int ch = (int)(rr % chunks);
+        rr /= chunks;
+        const int cy = DIM == 2 ? (int)rr : (int)(rr % (unsigned)nc);
+        const int cz = DIM == 3 ? (int)(rr / (unsigned)nc) : 0;
+        const int cx = ch * 32 + lane;
+        const int fxm = cx == 0 ? nf - 1 : 2 * cx - 1;  // wrapped left neighbour of the pair
+        int fy[3], fz[3];
+        fy[0] = cy == 0 ? nf - 1 : 2 * cy - 1; fy[1] = 2 * cy; fy[2] = 2 * cy + 1;
+        fz[0] = cz == 0 ? nf - 1 : 2 * cz - 1; fz[1] = 2 * cz; fz[2] = 2 * cz + 1;
+        const double* src = fine + (int64_t)p_u * Sf;
+        const double w3[3] = {0.5, 1.0, 0.5};
+        double ax = 0.0, ay = 0.0, am = 0.0;  // combined rows at 2cx, 2cx+1 and 2cx-1
+#pragma unroll
+        for (int a = 0; a < NZ; ++a)
+#pragma unroll
+            for (int bb = 0; bb < 3; ++bb) {
+                const double w = (DIM == 3 ? w3[a] : 1.0) * w3[bb];
+                const double* row = src + ((int64_t)(DIM == 3 ? fz[a] : 0) * nf + fy[bb]) * nf;
+                const double2 v = __ldg(reinterpret_cast<const double2*>(row + 2 * cx));
+                double left = __shfl_up_sync(0xffffffffu, v.y, 1);
+                if (lane == 0) left = __ldg(row + fxm);
+                ax = fma(w, v.x, ax);
+                ay = fma(w, v.y, ay);
+                am = fma(w, left, am);
+            }
+        coarse[(int64_t)p_u * Sc + ((int64_t)cz * (DIM == 3 ? nc : 0) + cy) * nc + cx] =
+            fma(0.5, am, fma(0.5, ay, ax));
+    }
+}
+
 __global__ void __launch_bounds__(PFB) k_pf_axpy(int64_t n, double a, const double* __restrict__ e,
                                                 double* x) {
     for (int64_t i = blockIdx.x * (int64_t)PFB + threadIdx.x; i < n; i += (int64_t)gridDim.x * PFB)
@@ -632,6 +751,16 @@ void restrict_planes(Ctx& c, int dim, bool periodic, int nc, int nf, int64_t pla
     auto go = [&](auto kernel) {
         launch(kernel, one_wave(c, kernel, rows * 32), PFB, 0, c.stream, nc, nf, planes, fine, coarse);
     };
+    static const bool no_pp = getenv("PD_PF_NO_PAIR_TRANSFERS") != nullptr;
+    if (periodic && nf == 2 * nc && nc % 32 == 0 && !no_pp) {
+        auto gp = [&](auto kernel) {
+            launch(kernel, one_wave(c, kernel, rows * 32), PFB, 0, c.stream, nc, planes, fine, coarse);
+        };
+        if (dim == 2) gp(k_pf_restrict_pp<2>);
+        else gp(k_pf_restrict_pp<3>);
+        PD_LAUNCH_CHECK();
+        return;
+    }
     if (dim == 2) {
         if (periodic) go(k_pf_restrict<2, true>);
         else go(k_pf_restrict<2, false>);
@@ -649,6 +778,18 @@ void prolong_add_planes(Ctx& c, int dim, bool periodic, int nc, int nf, int64_t 
     auto go = [&](auto kernel) {
         launch(kernel, one_wave(c, kernel, rows * 32), PFB, 0, c.stream, nc, nf, planes, coarse, fine);
     };
+    static const bool no_pp = getenv("PD_PF_NO_PAIR_TRANSFERS") != nullptr;
+    if (periodic && nf == 2 * nc && nc % 32 == 0 && !no_pp) {
+        const int64_t crows = planes * (dim == 2 ? nc : (int64_t)nc * nc);
+        auto gp = [&](auto kernel) {
+            launch(kernel, one_wave(c, kernel, crows * 32), PFB, 0, c.stream, nc, planes, coarse,
+                   fine);
+        };
+        if (dim == 2) gp(k_pf_prolong_add_pp<2>);
+        else gp(k_pf_prolong_add_pp<3>);
+        PD_LAUNCH_CHECK();
+        return;
+    }
     if (dim == 2) {
         if (periodic) go(k_pf_prolong_add<2, true>);
         else go(k_pf_prolong_add<2, false>);

@@ -94,6 +94,33 @@ def test_gpu_pfast_matches_restatement(case):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("case", [(2, 128, "periodic", 1.0, 3, 2, 0.01, 4),
+                                  (3, 64, "periodic", 0.1, 3, 2, 1e-3, 3),
+                                  (3, 64, "periodic", 0.1, 2, 1, 1e-3, 2)])
+def test_gpu_pair_per_lane_transfers_match_restatement(case, monkeypatch):
+    """Periodic levels with a multiple of 32 coarse points run the pair-per-lane
+    restriction / prolongation kernels: one sweep vs the restatement (1e-12) and vs the
+    general transfer kernels (PD_PF_NO_PAIR_TRANSFERS is read once per process, so the
+    comparison is against the restatement only when it was not set at start-up)."""
+    from paper_2006_12883_b200 import _native as N
+    from paper_2006_12883_b200.pfast import PfastSolver, pfast_rhs
+
+    dim, n, bc, coef, M, Nt, dt, levels = case
+    spec, tab, u0, orc = _case(*case)
+    b = pfast_rhs(spec, M, Nt, u0, tab)
+    solver = PfastSolver(spec, M, Nt, dt, levels=levels, tableau=tab)
+    x0 = np.random.default_rng(3).standard_normal(b.size)
+    xd = N.to_device(x0)
+    solver.sweep(b, xd)
+    want = orc.sweep(x0.reshape(orc.shape()), b.reshape(orc.shape())).ravel()
+    got = N.to_host(xd)
+    assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
+    solver.sweep(b, xd)
+    want = orc.sweep(want.reshape(orc.shape()), b.reshape(orc.shape())).ravel()
+    assert np.linalg.norm(N.to_host(xd) - want) <= 1e-12 * np.linalg.norm(want)
+
+
+@pytest.mark.gpu
 def test_gpu_pfast_config_errors():
     from paper_2006_12883_b200.errors import ConfigurationError
     from paper_2006_12883_b200.pfast import PfastSolver
