@@ -135,10 +135,12 @@ def test_element_solve_2d_fd_band():
     assert per_node_rel(s.solve_sequential(), ref, (cfg.Nt, cfg.M, cfg.spec.ndof)) < 1e-10
 
 
-@pytest.mark.parametrize("n,dim,W", [(5, 2, 3), (31, 3, 2), (127, 2, 1), (40, 3, 1), (130, 2, 2)])
+@pytest.mark.parametrize("n,dim,W", [(5, 2, 3), (31, 3, 2), (127, 2, 1), (40, 3, 1), (130, 2, 2),
+                                     (65, 3, 5), (100, 3, 2), (63, 3, 8), (33, 3, 40)])
 def test_mode_product_matches_einsum(n, dim, W):
     """The hand-written FP64 mode product (pd_modeprod.cu, no library) along every axis
-    of W stacked n^dim grids, with Phi and Phi^T, vs numpy (fp64 summation-order tolerance)."""
+    of W stacked n^dim grids, with Phi and Phi^T, vs numpy (fp64 summation-order
+    tolerance).  The last four shapes are wide enough for the DMMA (tensor) kernels."""
     import torch
 
     from paper_2006_12883_b200 import _native as N
