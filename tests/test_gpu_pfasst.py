@@ -222,3 +222,33 @@ def test_pfasst_implicit_newton_general_kh_matches_oracle():
     assert rep.converged and ro.converged
     assert rep.iterations == ro.iterations and rep.inner_iterations == ro.inner_iterations
     assert per_node_rel(x, xo, (cfg.Nt, 3, cfg.spec.ndof)) < 1e-9
+
+
+def test_lu_trick_qdelta_matches_reference(golden):
+    """the "lu-trick" Q_delta (collocation.py:119-123) through the device
+    sweeps — one sweep, a single-step SDC solve, PFASST on the heat problem and IMEX
+    PFASST on the monodomain problem vs runs of the real reference
+    (tests/golden/make_golden_lutrick.py)."""
+    g = golden("lutrick")
+    heat = pd.heat_problem()
+    mesh = pd.SpaceMesh(32, heat.X)
+    u0 = heat.u0(mesh.vertices)
+    hier = PF.build_pfasst_hierarchy(3, mesh, pd.TimeGrid(8, heat.T), 0.0, L=2, nu=1,
+                                     qdelta="lu-trick")
+    np.testing.assert_allclose(hier.fine.sweep(PF.spread_state(u0, 3)).U, g["heat_sweep1"],
+                               rtol=0, atol=1e-12)
+    st, rep = PF.sdc_solve_step(u0, hier.fine, tol_rel=1e-11, tol_abs=1e-12)
+    assert rep.iterations == int(g["heat_step_its"])
+    np.testing.assert_allclose(st.U, g["heat_step_U"], rtol=0, atol=1e-10)
+    x, rp = PF.pfasst_run(hier, u0, 8, 4, tol_rel=1e-10, tol_abs=1e-10)
+    assert rp.converged == bool(g["heat_conv"])
+    assert rp.inner_iterations == g["heat_its"].tolist()
+    assert per_node_rel(x, g["heat_U"], (8, 3, 33)) < 1e-10
+    mono = pd.monodomain_problem()
+    mesh2 = pd.SpaceMesh(64, mono.X)
+    hier2 = PF.build_pfasst_hierarchy(3, mesh2, pd.TimeGrid(8, 0.5), mono.gamma, L=2, nu=1,
+                                      mode="imex", qdelta="lu-trick")
+    x2, r2 = PF.pfasst_run(hier2, mono.u0(mesh2.vertices), 8, 2, tol_rel=1e-9, tol_abs=1e-9)
+    assert r2.converged == bool(g["mono_conv"])
+    assert r2.inner_iterations == g["mono_its"].tolist()
+    assert per_node_rel(x2, g["mono_U"], (8, 3, 65)) < 1e-9
