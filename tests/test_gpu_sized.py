@@ -2,7 +2,8 @@
 
 The reference was run here on the benchmarked configuration itself (BASELINE C2:
 255^2 x 64 steps x M=3, SMG L=7, P=8) and on the survey's reduced sizes of the other
-configs (Appendix A): STMG 63^2 x 64 (L=6, P=8), C3 128^2 x 32 periodic Fisher
+configs (Appendix A): STMG 63^2 x 64 (L=6, P=8) and STMG on C2 itself (40 cycles, stagnating),
+C3 128^2 x 32 periodic Fisher
 (Newton + SMG and PFASST IMEX over 4 windows), C4 31^3 x 16 (PFASST M=5/3 at P=4/8
 and tol 1e-9/1e-10, multi-window; SMG), C5 16^3 x 8 periodic cubic (Newton + STMG).
 
@@ -72,6 +73,22 @@ def test_c2_full_size_smg_matches_reference(golden, c2_system):
     assert rep.converged and rep.iterations == int(g["smg_its"]) == 3
     assert_history(rep, g, "smg")
     compare(x, g, "smg", (cfg.Nt, 3, cfg.spec.ndof))
+
+
+def test_stmg_on_c2_stagnates_like_the_reference(golden, c2_system):
+    """Why the bench solves C2 with SMG: the reference's STMG (L=7, P=8) on the full C2
+    system stagnates near 1.4e-4 (40 cycles, flagged diverged at the cap); the device
+    path follows the same residual history."""
+    g = golden("sized_stmg_c2")
+    cfg, s = c2_system
+    h = pd.build_hierarchy(s, "STMG", 7, 3, partitions=8)
+    cap = int(g["max_cycles"])
+    x, rep = h.solve(s.rhs(), tol_rel=1e-10, tol_abs=1e-10, max_cycles=cap)
+    assert rep.iterations == int(g["stmg_its"]) == cap
+    assert rep.converged == bool(g["stmg_conv"]) and rep.diverged == bool(g["stmg_div"])
+    assert not rep.converged
+    assert_history(rep, g, "stmg", rel=1e-4)
+    assert rep.residual_history[-1] > 1e-2 * rep.residual_history[0]
 
 
 def test_stmg_63_matches_reference(golden):
