@@ -167,6 +167,7 @@ int pd_st_residual_csr(void *ctx, void *L, void *MR, double gamma, int kind, con
 int pd_reaction(void *ctx, int kind, int deriv, const double *u, double *out, int64_t n);
 int pd_axpy_to(void *ctx, double *y, const double *x, const double *d, double s, int64_t n);
 int pd_norm(void *ctx, const double *x, int64_t n, double *host_out); /* synchronising */
+int pd_dot(void *ctx, const double *x, const double *y, int64_t n, double *host_out); /* x.y, synchronising */
 int pd_scale(void *ctx, double *y, const double *x, double s, int64_t n);
 
 /* ---- K1: matrix-free space-time operator (spacetime.py:77-80,117-142).

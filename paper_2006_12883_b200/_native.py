@@ -104,6 +104,7 @@ _SIGNATURES = {
     "pd_reaction": (_int, [_vp, _int, _int, _vp, _vp, _i64]),
     "pd_axpy_to": (_int, [_vp, _vp, _vp, _vp, _dbl, _i64]),
     "pd_norm": (_int, [_vp, _vp, _i64, ctypes.POINTER(_dbl)]),
+    "pd_dot": (_int, [_vp, _vp, _vp, _i64, ctypes.POINTER(_dbl)]),
     "pd_sdc_level_create": (_int, [_vp, _vp, _vp, _int, _vp, _vp, _vp, _dbl, _dbl, _int, _int,
                                    _int, _vp, _vp, _int, _i64, _dbl, ctypes.POINTER(_vp)]),
     "pd_sdc_level_destroy": (_int, [_vp]),
@@ -376,6 +377,14 @@ def norm(x, ctx: Context | None = None) -> float:
     ctx = ctx or context()
     out = _dbl()
     call("pd_norm", ctx.handle, ptr(x), int(x.numel()), ctypes.byref(out))
+    return float(out.value)
+
+
+def dot(x, y, ctx: Context | None = None) -> float:
+    """x . y of two CUDA tensors via the native deterministic reduction."""
+    ctx = ctx or context()
+    out = _dbl()
+    call("pd_dot", ctx.handle, ptr(x), ptr(y), int(x.numel()), ctypes.byref(out))
     return float(out.value)
 
 

@@ -117,6 +117,21 @@ int pd_norm(void* ctx, const double* x, int64_t n, double* host_out) {
     });
 }
 
+// host_out = x . y (the same deterministic two-stage reduction; synchronising)
+int pd_dot(void* ctx, const double* x, const double* y, int64_t n, double* host_out) {
+    return guarded_vec([&] {
+        auto& c = *static_cast<pd::Ctx*>(ctx);
+        double h = 0.0;
+        if (n > 0) {
+            pd::vec_dot(c, x, y, n, c.scalars.p);
+            PD_CUDA(cudaMemcpyAsync(&h, c.scalars.p, sizeof(double), cudaMemcpyDeviceToHost,
+                                    c.stream));
+            PD_CUDA(cudaStreamSynchronize(c.stream));
+        }
+        *host_out = h;
+    });
+}
+
 // y = s * x
 int pd_scale(void* ctx, double* y, const double* x, double s, int64_t n) {
     return guarded_vec([&] {

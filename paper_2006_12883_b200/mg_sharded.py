@@ -182,7 +182,8 @@ class DeviceEngine:
         return lu.solve(b)
 
     def dot(self, a, b) -> float:
-        return float(a.dot(b).item())
+        # the library's own deterministic reduction (no torch / cuBLAS ddot on the path)
+        return self.N.dot(a.contiguous(), b.contiguous(), self.ctx)
 
     def size(self, a) -> int:
         return int(a.numel())
