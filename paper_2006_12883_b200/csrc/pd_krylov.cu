@@ -69,16 +69,13 @@ __global__ void k_gm_init(GmDev* s, const double* norm2, double tol_rel, double 
 
 // V0 = r / beta (first cycle reads the initial residual r0, restarts read rg)
 __global__ void k_gm_start_vec(const GmDev* s, const double* r0, const double* rg, double* V,
-                               double* vcur, int64_t n) {
+                               int64_t n) {
     if (vphase(s) != GM_START) return;
     const double beta = s->beta;
     const double* src = s->cycles == 0 ? r0 : rg;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const double v = src[i] / beta;
-        V[i] = v;
-        vcur[i] = v;
-    }
+         i += (int64_t)gridDim.x * blockDim.x)
+        V[i] = src[i] / beta;
 }
 
 __global__ void k_gm_start(GmDev* s) {
@@ -170,29 +167,16 @@ __global__ void k_gm_arnoldi(GmDev* s, int slot, double* hist) {
 #undef HH
 }
 
-// V[j+1] = w / hn (and the preconditioner input buffer)
-__global__ void k_gm_newvec(const GmDev* s, int slot, const double* w, double* V, double* vcur,
-                            int64_t n) {
+// V[j+1] = w / hn (the next step's preconditioner / operator input is read from V[j+1])
+__global__ void k_gm_newvec(const GmDev* s, int slot, const double* w, double* V, int64_t n) {
     if (s->vec_slot != slot || s->vec_idx < 0) return;
     const int ph = vphase(s);
     if (ph != GM_RUN && ph != GM_FINISH) return;
     const double hn = s->hn;
     double* dst = V + (int64_t)s->vec_idx * n;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const double v = w[i] / hn;
-        dst[i] = v;
-        vcur[i] = v;
-    }
-}
-
-// Z[j] = z = M^{-1} V[j]  (kept so the cycle update needs no extra ILU apply)
-__global__ void k_gm_store_z(const GmDev* s, const double* z, double* Z, int64_t n) {
-    if (vphase(s) != GM_RUN) return;
-    double* dst = Z + (int64_t)s->j * n;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = z[i];
+        dst[i] = w[i] / hn;
 }
 
 // y = H[:k,:k]^{-1} g[:k]  (column-oriented back substitution, dtrsm order)
@@ -218,6 +202,20 @@ __global__ void k_gm_combine(const GmDev* s, const double* V, double* u, int64_t
         double acc = 0.0;
         for (int l = 0; l < k; ++l) acc = add(acc, mul(s->y[l], V[(int64_t)l * n + i]));
         u[i] = acc;
+    }
+}
+
+// xg (+)= V[:k]^T y in one pass (no preconditioner apply between the two: the smoother's
+// stored Z_j, or an unpreconditioned solve); the same sums as k_gm_combine + k_gm_update_x
+__global__ void k_gm_combine_update(const GmDev* s, const double* V, double* xg, int64_t n) {
+    if (vphase(s) != GM_FINISH) return;
+    const int k = s->k;
+    const bool first = s->cycles == 0 && !s->has_x0;  // x = 0 + du exactly
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int l = 0; l < k; ++l) acc = add(acc, mul(s->y[l], V[(int64_t)l * n + i]));
+        xg[i] = first ? acc : add(xg[i], acc);
     }
 }
 
@@ -281,7 +279,6 @@ Gmres::Gmres(Ctx& c_, const Csr* A_, Ilu0* M_, int64_t n_, int restart_, int max
     u.alloc(std::max<int64_t>(n, 1));
     rg.alloc(std::max<int64_t>(n, 1));
     xg.alloc(std::max<int64_t>(n, 1));
-    vcur.alloc(std::max<int64_t>(n, 1));
     if (store_z) Z.alloc((size_t)restart * std::max<int64_t>(n, 1));
     norm2.alloc(1);
     hist.alloc(std::max(max_it, 1) + 2);
@@ -300,13 +297,17 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
     const int g = c.grid_for(n, KB, 8);
     const int gr = std::min(c.grid_for(n, KB, 4), kReduceMaxBlocks);
     const int* ph = &st.p->phase;
-    launch(k_gm_start_vec, g, KB, 0, c.stream, st.p, r0, rg.p, V.p, vcur.p, n);
+    // the host knows this slot's Arnoldi index (callers pass j + 2 passes): the basis
+    // vector V[j] is the input of the step, and a stored Z_j is written in place
+    const int jh = std::max(0, std::min(mgs_passes - 2, restart - 1));
+    const double* vin = V.p + (int64_t)jh * n;
+    launch(k_gm_start_vec, g, KB, 0, c.stream, st.p, r0, rg.p, V.p, n);
     launch(k_gm_start, 1, 1, 0, c.stream, st.p);
-    const double* zin = vcur.p;
+    const double* zin = vin;
     if (M) {
-        ilu0_solve(c, *M, vcur.p, z.p, ph, GM_RUN);
-        zin = z.p;
-        if (store_z) launch(k_gm_store_z, g, KB, 0, c.stream, st.p, (const double*)z.p, Z.p, n);
+        double* zout = store_z ? Z.p + (int64_t)jh * n : z.p;
+        ilu0_solve(c, *M, vin, zout, ph, GM_RUN);
+        zin = zout;
     }
     apply_A(c, *A, op, zin, w.p, SPMV_SET, nullptr, ph, GM_RUN);
     const int passes = std::min(mgs_passes, restart + 1);
@@ -314,18 +315,18 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
         launch(k_gm_mgs, gr, KB, 0, c.stream, st.p, i, w.p, V.p, n, c.red_partials.p,
                                           c.red_counter.p);
     launch(k_gm_arnoldi, 1, 1, 0, c.stream, st.p, slot, hist.p);
-    launch(k_gm_newvec, g, KB, 0, c.stream, st.p, slot, w.p, V.p, vcur.p, n);
+    launch(k_gm_newvec, g, KB, 0, c.stream, st.p, slot, w.p, V.p, n);
     // cycle finish (active only when this step ended the cycle)
     launch(k_gm_finish_y, 1, 1, 0, c.stream, st.p);
     // x += M^{-1}(V y) (linalg.py:297); with stored Z_j = M^{-1} V_j this is
     // sum_j y_j Z_j — the same linear map, one ILU apply fewer per cycle
-    launch(k_gm_combine, g, KB, 0, c.stream, st.p, store_z ? Z.p : V.p, u.p, n);
-    const double* du = u.p;
-    if (M && !store_z) {
+    if (!M || store_z) {
+        launch(k_gm_combine_update, g, KB, 0, c.stream, st.p, store_z ? Z.p : V.p, xg.p, n);
+    } else {
+        launch(k_gm_combine, g, KB, 0, c.stream, st.p, V.p, u.p, n);
         ilu0_solve(c, *M, u.p, z.p, ph, GM_FINISH);
-        du = z.p;
+        launch(k_gm_update_x, g, KB, 0, c.stream, st.p, xg.p, (const double*)z.p, n);
     }
-    launch(k_gm_update_x, g, KB, 0, c.stream, st.p, xg.p, du, n);
     apply_A(c, *A, op, xg.p, rg.p, SPMV_RESID, b, &st.p->final_res, GM_FINISH, norm2.p, nullptr);
     launch(k_gm_restart, 1, 1, 0, c.stream, st.p, norm2.p, hist.p);
     PD_LAUNCH_CHECK();
@@ -342,14 +343,15 @@ void Gmres::slot_with_callables(int slot, int mgs_passes, const double* b, const
                                 const ApplyFn* fm) {
     const int g = c.grid_for(n, KB, 8);
     const int gr = std::min(c.grid_for(n, KB, 4), kReduceMaxBlocks);
-    launch(k_gm_start_vec, g, KB, 0, c.stream, st.p, r0, rg.p, V.p, vcur.p, n);
+    launch(k_gm_start_vec, g, KB, 0, c.stream, st.p, r0, rg.p, V.p, n);
     launch(k_gm_start, 1, 1, 0, c.stream, st.p);
     PD_LAUNCH_CHECK();
     const GmDev& s = read_state();  // synchronising: the callables run on the host's clock
     if (s.phase == GM_RUN) {
-        const double* zin = vcur.p;
+        const double* vin = V.p + (int64_t)s.j * n;
+        const double* zin = vin;
         if (fm) {
-            (*fm)(vcur.p, z.p);
+            (*fm)(vin, z.p);
             zin = z.p;
         }
         fa(zin, w.p);
@@ -359,7 +361,7 @@ void Gmres::slot_with_callables(int slot, int mgs_passes, const double* b, const
         launch(k_gm_mgs, gr, KB, 0, c.stream, st.p, i, w.p, V.p, n, c.red_partials.p,
                c.red_counter.p);
     launch(k_gm_arnoldi, 1, 1, 0, c.stream, st.p, slot, hist.p);
-    launch(k_gm_newvec, g, KB, 0, c.stream, st.p, slot, w.p, V.p, vcur.p, n);
+    launch(k_gm_newvec, g, KB, 0, c.stream, st.p, slot, w.p, V.p, n);
     launch(k_gm_finish_y, 1, 1, 0, c.stream, st.p);
     launch(k_gm_combine, g, KB, 0, c.stream, st.p, V.p, u.p, n);
     PD_LAUNCH_CHECK();
@@ -409,7 +411,6 @@ void Gmres::debug_dump(int slot) {
     };
     show("V0", V.p);
     show("V1", V.p + n);
-    show("vcur", vcur.p);
     show("w", w.p);
     show("u", u.p);
     show("xg", xg.p);

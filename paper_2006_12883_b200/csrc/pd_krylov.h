@@ -60,7 +60,7 @@ class Gmres {
     DevBuf<GmDev> st;
     std::unique_ptr<GmDev> host_st;  // host mirror (the struct is ~0.5 MB: kept off the stack)
     bool store_z = false;
-    DevBuf<double> V, w, z, u, rg, xg, vcur, norm2, hist, Z;
+    DevBuf<double> V, w, z, u, rg, xg, norm2, hist, Z;
     const double* r0 = nullptr;
 };
 
