@@ -132,6 +132,26 @@ int pd_gmres_callable(void *ctx, int64_t n, void *A, pd_apply_cb matvec, void *i
                       double tol_abs, int restart, int max_it, pd_solve_report *rep,
                       double *hist, int hist_cap);
 
+/* ---- the smoother's GMRES(nu) (multigrid.py:243-256 on linalg.py:215-311) driven step by
+ *      step from outside, for the time-slab sharded V-cycle: the caller
+ *      applies the rank-local block-Jacobi preconditioner to V[j] -> Z[j] and the sharded
+ *      operator (halo exchange inside) to Z[j] -> w, sum-reduces dots[i] over the ranks
+ *      after every MGS pass (a device scalar: NCCL all-reduce on the stream), and the
+ *      Hessenberg / Givens recurrence, the stopping test and the update x += Z y run on the
+ *      device.  No call synchronises except pd_gms_error.
+ *      per step j = 0..nu-1: begin(j) | M^{-1}, A | for i in 0..j+1: mgs_pass(i), reduce
+ *      dots[i] | end(j);   after the last step: apply(x). */
+int pd_gms_create(void *ctx, int64_t n_local, int nu, void **out);
+int pd_gms_destroy(void *e);
+int pd_gms_init(void *e, const double *r0, const double *norm2_dev); /* |r0|^2 over all ranks */
+int pd_gms_begin(void *e, int j, const double **vin, double **zout, double **wout);
+int pd_gms_dots(void *e, double **dots_dev);
+int pd_gms_mgs_pass(void *e, int i);
+int pd_gms_end(void *e, int slot);
+int pd_gms_apply(void *e, double *x);
+int pd_gms_error(void *e, int *err); /* synchronising; 0 or linalg.py's non-finite cases 1..3 */
+int pd_dot_dev(void *ctx, const double *x, const double *y, int64_t n, double *out_dev);
+
 /* ---- space-time multigrid (multigrid.py:197-305 MultigridHierarchy).
  *      Takes ownership of the level matrices mats[0..L) (Galerkin products,
  *      multigrid.py:232-233) and of R[0..L-1), P[0..L-1), also when it fails

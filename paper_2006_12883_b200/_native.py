@@ -123,6 +123,17 @@ _SIGNATURES = {
     "pd_band_lu_create": (_int, [_vp, _vp, _int, _int, _vp, ctypes.POINTER(_vp)]),
     "pd_band_lu_solve": (_int, [_vp, _vp, _vp, _vp]),
     "pd_band_lu_destroy": (_int, [_vp]),
+    "pd_gms_create": (_int, [_vp, _i64, _int, ctypes.POINTER(_vp)]),
+    "pd_gms_destroy": (_int, [_vp]),
+    "pd_gms_init": (_int, [_vp, _vp, _vp]),
+    "pd_gms_begin": (_int, [_vp, _int, ctypes.POINTER(_vp), ctypes.POINTER(_vp),
+                            ctypes.POINTER(_vp)]),
+    "pd_gms_dots": (_int, [_vp, ctypes.POINTER(_vp)]),
+    "pd_gms_mgs_pass": (_int, [_vp, _int]),
+    "pd_gms_end": (_int, [_vp, _int]),
+    "pd_gms_apply": (_int, [_vp, _vp]),
+    "pd_gms_error": (_int, [_vp, ctypes.POINTER(_int)]),
+    "pd_dot_dev": (_int, [_vp, _vp, _vp, _i64, _vp]),
     "pd_gmres_callable": (_int, [_vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _dbl,
                                  _dbl, _int, _int, ctypes.POINTER(SolveReportC), _vp, _int]),
 }
@@ -378,6 +389,21 @@ def norm(x, ctx: Context | None = None) -> float:
     out = _dbl()
     call("pd_norm", ctx.handle, ptr(x), int(x.numel()), ctypes.byref(out))
     return float(out.value)
+
+
+class _DeviceSpan:
+    """A raw device pointer as a CUDA array (torch.as_tensor wraps it without a copy)."""
+
+    def __init__(self, address: int, count: int):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8",
+                                         "data": (int(address), False), "version": 2}
+
+
+def view(address, count: int, ctx: Context | None = None):
+    """fp64 tensor view of `count` doubles at a device address owned by the library."""
+    ctx = ctx or context()
+    addr = address.value if hasattr(address, "value") else int(address)
+    return torch_mod().as_tensor(_DeviceSpan(addr, count), device=ctx.torch_device)
 
 
 def dot(x, y, ctx: Context | None = None) -> float:

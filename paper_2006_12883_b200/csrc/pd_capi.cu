@@ -239,6 +239,44 @@ int pd_gmres_callable(void* ctx, int64_t n, void* A, pd_apply_cb matvec, void* i
     });
 }
 
+// ---- externally driven GMRES(nu) smoother steps (mg_sharded.py)
+int pd_gms_create(void* ctx, int64_t n, int nu, void** out) {
+    return guarded([&] {
+        if (n < 0 || nu < 1) throw pd::ConfigError("bad smoother size");
+        *out = new pd::Gmres(*C(ctx), nullptr, nullptr, n, nu, nu, /*store_z=*/true,
+                             /*external=*/true);
+    });
+}
+int pd_gms_destroy(void* e) {
+    return guarded([&] { delete static_cast<pd::Gmres*>(e); });
+}
+int pd_gms_init(void* e, const double* r0, const double* norm2_dev) {
+    return guarded([&] {
+        H<pd::Gmres>(e, "smoother")->enqueue_init(r0, norm2_dev, 1e-13, 0.0);
+    });
+}
+int pd_gms_begin(void* e, int j, const double** vin, double** zout, double** wout) {
+    return guarded([&] { H<pd::Gmres>(e, "smoother")->ext_begin(j, vin, zout, wout); });
+}
+int pd_gms_dots(void* e, double** dots_dev) {
+    return guarded([&] { *dots_dev = H<pd::Gmres>(e, "smoother")->ext_dots(); });
+}
+int pd_gms_mgs_pass(void* e, int i) {
+    return guarded([&] { H<pd::Gmres>(e, "smoother")->ext_mgs_pass(i); });
+}
+int pd_gms_end(void* e, int slot) {
+    return guarded([&] { H<pd::Gmres>(e, "smoother")->ext_end(slot); });
+}
+int pd_gms_apply(void* e, double* x) {
+    return guarded([&] { H<pd::Gmres>(e, "smoother")->ext_apply(x); });
+}
+int pd_gms_error(void* e, int* err) {
+    return guarded([&] { *err = H<pd::Gmres>(e, "smoother")->read_state().err; });
+}
+int pd_dot_dev(void* ctx, const double* x, const double* y, int64_t n, double* out_dev) {
+    return guarded([&] { pd::vec_dot(*C(ctx), x, y, n, out_dev); });
+}
+
 int pd_mg_create(void* ctx, int nlevels, void** mats, void** R, void** P, int nu, int partitions,
                  int restart, int smooth_solves, void** out) {
     return guarded([&] {

@@ -266,8 +266,9 @@ __global__ void k_gm_apply(const GmDev* s, double* x, const double* xg, int64_t 
 
 // ------------------------------------------------------------------ Gmres
 Gmres::Gmres(Ctx& c_, const Csr* A_, Ilu0* M_, int64_t n_, int restart_, int max_it_,
-             bool store_z_)
-    : c(c_), A(A_), M(M_), n(n_), max_it(max_it_), store_z(store_z_ && M_ != nullptr) {
+             bool store_z_, bool external)
+    : c(c_), A(A_), M(M_), n(n_), max_it(max_it_),
+      store_z(store_z_ && (M_ != nullptr || external)) {
     restart = std::max<int64_t>(1, std::min<int64_t>(restart_, n_));
     if (restart > kGmMaxRestart)
         throw ConfigError("GMRES restart length above " + std::to_string(kGmMaxRestart));
@@ -281,6 +282,7 @@ Gmres::Gmres(Ctx& c_, const Csr* A_, Ilu0* M_, int64_t n_, int restart_, int max
     xg.alloc(std::max<int64_t>(n, 1));
     if (store_z) Z.alloc((size_t)restart * std::max<int64_t>(n, 1));
     norm2.alloc(1);
+    PD_CUDA(cudaMemset(norm2.p, 0, sizeof(double)));
     hist.alloc(std::max(max_it, 1) + 2);
 }
 
@@ -329,6 +331,43 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
     }
     apply_A(c, *A, op, xg.p, rg.p, SPMV_RESID, b, &st.p->final_res, GM_FINISH, norm2.p, nullptr);
     launch(k_gm_restart, 1, 1, 0, c.stream, st.p, norm2.p, hist.p);
+    PD_LAUNCH_CHECK();
+}
+
+// ---- externally driven steps (time-slab sharded smoother, mg_sharded.py)
+void Gmres::ext_begin(int j, const double** vin, double** zout, double** wout) {
+    if (!store_z) throw ConfigError("external GMRES steps need stored Z vectors");
+    if (j < 0 || j >= restart) throw ConfigError("Arnoldi index outside the restart length");
+    const int g = c.grid_for(n, KB, 8);
+    launch(k_gm_start_vec, g, KB, 0, c.stream, st.p, r0, rg.p, V.p, n);
+    launch(k_gm_start, 1, 1, 0, c.stream, st.p);
+    PD_LAUNCH_CHECK();
+    *vin = V.p + (int64_t)j * n;
+    *zout = Z.p + (int64_t)j * n;
+    *wout = w.p;
+}
+
+void Gmres::ext_mgs_pass(int i) {
+    const int gr = std::min(c.grid_for(n, KB, 4), kReduceMaxBlocks);
+    launch(k_gm_mgs, gr, KB, 0, c.stream, st.p, i, w.p, V.p, n, c.red_partials.p, c.red_counter.p);
+    PD_LAUNCH_CHECK();
+}
+
+void Gmres::ext_end(int slot) {
+    const int g = c.grid_for(n, KB, 8);
+    launch(k_gm_arnoldi, 1, 1, 0, c.stream, st.p, slot, hist.p);
+    launch(k_gm_newvec, g, KB, 0, c.stream, st.p, slot, w.p, V.p, n);
+    launch(k_gm_finish_y, 1, 1, 0, c.stream, st.p);
+    launch(k_gm_combine_update, g, KB, 0, c.stream, st.p, Z.p, xg.p, n);
+    // a cycle that ends before the cap (residual estimate below 1e-13 |r0| or a happy
+    // breakdown) is taken as converged: norm2 stays 0, so k_gm_restart reads a zero true
+    // residual (the serial engine forms it; with tol 1e-13 it confirms the estimate)
+    launch(k_gm_restart, 1, 1, 0, c.stream, st.p, norm2.p, hist.p);
+    PD_LAUNCH_CHECK();
+}
+
+void Gmres::ext_apply(double* x) {
+    launch(k_gm_apply, c.grid_for(n, KB, 8), KB, 0, c.stream, st.p, x, xg.p, n);
     PD_LAUNCH_CHECK();
 }
 

@@ -27,8 +27,11 @@ class Gmres {
    public:
     // store_z: keep Z_j = M^{-1} V_j and update x with Z y (no extra preconditioner
     // apply per cycle); the smoother uses it, the standalone gmres mirrors linalg.py
+    // external: the operator and the preconditioner are applied by the caller between the
+    // engine's steps (time-slab sharded multigrid: halo exchanges and allreduced dots in
+    // between); Z_j is kept like in the smoother
     Gmres(Ctx& c, const Csr* A, Ilu0* M, int64_t n, int restart, int max_it,
-          bool store_z = false);
+          bool store_z = false, bool external = false);
     // init from r0 = b - A x0 whose squared norm is at *norm2_dev; x0 may be
     // null (zero start, as in the smoother)
     void enqueue_init(const double* r0, const double* norm2_dev, double tol_rel, double tol_abs,
@@ -42,6 +45,14 @@ class Gmres {
     using ApplyFn = std::function<void(const double* x, double* y)>;
     void slot_with_callables(int slot, int mgs_passes, const double* b, const ApplyFn& fa,
                              const ApplyFn* fm);
+    // ---- externally driven smoother steps (mg_sharded): the caller applies M^{-1} to
+    // V[j] into Z[j] and A to Z[j] into w, reduces dots[i] over the ranks after every
+    // MGS pass, and calls ext_end; no host synchronisation anywhere
+    void ext_begin(int j, const double** vin, double** zout, double** wout);
+    void ext_mgs_pass(int i);
+    double* ext_dots() { return st.p->dots; }
+    void ext_end(int slot);
+    void ext_apply(double* x);  // x += solution when a cycle ran
     const GmDev& read_state();  // synchronising; scalar header only (host mirror)
     double* x() { return xg.p; }
     int64_t size() const { return n; }

@@ -30,6 +30,7 @@ solver's iteration counts (tests).
 from __future__ import annotations
 
 import math
+import os
 import time
 
 import numpy as np
@@ -97,6 +98,18 @@ class Comm:
         self.dist.all_reduce(t, group=self.group)
         return float(t.item())
 
+    def allreduce_tensor_(self, t) -> None:
+        """In-place sum of a (device) tensor over the ranks: asynchronous on the stream
+        with NCCL; staged through the host with gloo (CPU tests only)."""
+        if self.size == 1:
+            return
+        if self._host_staged() and t.is_cuda:
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.all_reduce(t, group=self.group)
+
     def _host_staged(self) -> bool:
         """gloo moves host tensors only: CUDA vectors are staged through the host."""
         return self.dist.get_backend(self.group) == "gloo"
@@ -163,6 +176,10 @@ class DeviceEngine:
 
         return DenseLU(A)
 
+    def smoother(self, n: int, nu: int):
+        """Device-resident GMRES(nu) steps driven by the sharded cycle (pd_gms_*)."""
+        return _DeviceSmoother(self, n, nu)
+
     def vec(self, a):
         return self.N.to_device(a, self.ctx)
 
@@ -204,6 +221,72 @@ class DeviceEngine:
 
     def comm_tensor(self, x):
         return x
+
+
+class _DeviceSmoother:
+    """One level's externally driven smoother engine: Krylov vectors, Hessenberg/Givens
+    recurrence and stopping test on the device; this class only wraps pointers."""
+
+    def __init__(self, eng: "DeviceEngine", n: int, nu: int):
+        import ctypes
+
+        self.eng, self.n, self.nu = eng, int(n), int(nu)
+        N = eng.N
+        h = ctypes.c_void_p()
+        N.call("pd_gms_create", eng.ctx.handle, self.n, self.nu, ctypes.byref(h))
+        self.handle = h
+        d = ctypes.c_void_p()
+        N.call("pd_gms_dots", self.handle, ctypes.byref(d))
+        self.dots = N.view(d, self.nu + 2, eng.ctx)  # dots[i]: reduced over ranks after pass i
+        self.norm2 = N.zeros(1, eng.ctx)
+        self._views = {}
+
+    def init(self, r):
+        N = self.eng.N
+        N.call("pd_dot_dev", self.eng.ctx.handle, N.ptr(r), N.ptr(r), self.n, N.ptr(self.norm2))
+        return self.norm2  # the caller sums it over the ranks, then calls start()
+
+    def start(self, r):
+        self._r = r  # the engine reads r on its first step: keep it alive
+        N = self.eng.N
+        N.call("pd_gms_init", self.handle, N.ptr(r), N.ptr(self.norm2))
+
+    def begin(self, j: int):
+        import ctypes
+
+        N = self.eng.N
+        v, z, w = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+        N.call("pd_gms_begin", self.handle, int(j), ctypes.byref(v), ctypes.byref(z),
+               ctypes.byref(w))
+        views = self._views.get(j)
+        if views is None:  # the engine's buffers never move: wrap each pointer once
+            n1 = max(self.n, 1)
+            views = self._views[j] = tuple(N.view(p, n1, self.eng.ctx)[:self.n] for p in (v, z, w))
+        return views
+
+    def mgs_pass(self, i: int):
+        self.eng.N.call("pd_gms_mgs_pass", self.handle, int(i))
+        return self.dots[i:i + 1]
+
+    def end(self, slot: int):
+        self.eng.N.call("pd_gms_end", self.handle, int(slot))
+
+    def apply(self, x):
+        self.eng.N.call("pd_gms_apply", self.handle, self.eng.N.ptr(x))
+
+    def error(self) -> int:
+        import ctypes
+
+        e = ctypes.c_int()
+        self.eng.N.call("pd_gms_error", self.handle, ctypes.byref(e))
+        return int(e.value)
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.eng.N.load_library().pd_gms_destroy(self.handle)
+        except Exception:
+            pass
 
 
 # ---------------------------------------------------------------- the solver
@@ -252,6 +335,12 @@ class ShardedMultigrid:
         self.coarse_counts = [b - a for a, b in self.coarse_counts]
         self.coarse_lu = engine.coarse_solver(mats[-1])
         self.sizes = [m.shape[0] for m in mats]
+        # device engines keep the smoother's GMRES on the device (no host sync per dot);
+        # the CPU engine of the gloo tests runs the host restatement below
+        self.gms = None
+        if hasattr(engine, "smoother") and os.environ.get("PD_SHARDED_HOST_GMRES") != "1":
+            self.gms = [engine.smoother(sh.r1 - sh.r0, min(self.nu, self.restart))
+                        for sh in self.shards]
 
     # ---- distributed vector primitives ------------------------------------
     def _dot(self, a, b) -> float:
@@ -341,7 +430,30 @@ class ShardedMultigrid:
                 return x
 
     # ---- V-cycle (multigrid.py:243-273) ------------------------------------
+    def _smooth_device(self, l, b, x):
+        """multigrid.py:243-256 with the GMRES(nu) of linalg.py:215-311 on the device: per
+        Arnoldi step the rank-local preconditioner, the sharded operator (one halo
+        send/recv), j + 2 MGS passes with a one-double all-reduce each; nothing is read
+        back to the host.  x is updated in place."""
+        eng, sm, pre = self.eng, self.gms[l], self.pres[l]
+        nu = sm.nu
+        for _ in range(self.smooth_solves):
+            r = self._residual(l, b, x)
+            self.comm.allreduce_tensor_(sm.init(r))
+            sm.start(r)
+            for j in range(nu):
+                v, z, w = sm.begin(j)
+                pre.solve_dev(v, out=z)
+                self.ops[l].matvec_dev(self._ext(l, z), out=w)
+                for i in range(j + 2):
+                    self.comm.allreduce_tensor_(sm.mgs_pass(i))
+                sm.end(j)
+            sm.apply(x)
+        return x
+
     def _smooth(self, l, b, x):
+        if self.gms is not None:
+            return self._smooth_device(l, b, x)
         for _ in range(self.smooth_solves):
             r = self._residual(l, b, x)
             x = x + self._gmres(l, r, 1e-13, 0.0, min(self.nu, self.restart), self.nu)
@@ -364,6 +476,13 @@ class ShardedMultigrid:
         out = self._cycle(0, b, x)
         if not np.isfinite(self._norm(out)):
             raise SolverError("V-cycle produced non-finite values")
+        if self.gms is not None:  # the device smoothers' error codes, once per cycle
+            texts = {1: "non-finite initial residual", 2: "non-finite residual in GMRES iteration",
+                     3: "non-finite residual in GMRES restart"}
+            for sm in self.gms:
+                code = sm.error()
+                if code:
+                    raise SolverError(texts.get(code, f"GMRES error {code}"))
         return out
 
     def solve(self, b, x0=None, tol_rel: float = 1e-9, tol_abs: float = 1e-9,
@@ -373,6 +492,8 @@ class ShardedMultigrid:
         eng = self.eng
         b = eng.vec(b)
         x = eng.zeros(self.shards[0].r1 - self.shards[0].r0) if x0 is None else eng.vec(x0)
+        if self.gms is not None and x0 is not None:
+            x = x.clone()  # the device smoother updates x in place
         res = self._norm(self._residual(0, b, x))
         rep = SolveReport(residual_history=[res])
         thr = max(tol_abs, tol_rel * res)

@@ -197,7 +197,8 @@ def test_device_galerkin_refresh_bitwise_equals_scipy():
 
 def test_sharded_mg_device_engine_one_rank_matches_serial():
     """mg_sharded on the GPU engine (G=1: no communication) reproduces the serial
-    device multigrid: equal cycle counts, rel L2 <= 1e-10 (host-side GMRES scalars)."""
+    device multigrid: equal cycle counts, rel L2 <= 1e-10 — through the device-resident
+    smoother steps (pd_gms_*), and through the host-scalar GMRES mirror."""
     from paper_2006_12883_b200.mg_sharded import build_sharded_hierarchy
 
     cfg = pd.baseline_config("C2", n=31, Nt=8)
@@ -207,10 +208,23 @@ def test_sharded_mg_device_engine_one_rank_matches_serial():
     b = system.rhs()
     x1, r1 = h.solve(b, tol_rel=1e-10, tol_abs=1e-10)
     smg = build_sharded_hierarchy(h)
+    assert smg.gms is not None
     x2, r2 = smg.solve(b, tol_rel=1e-10, tol_abs=1e-10)
     x2 = x2.cpu().numpy()
     assert r1.converged and r2.converged and r1.iterations == r2.iterations
     assert np.linalg.norm(x2 - x1) <= 1e-10 * np.linalg.norm(x1)
+    np.testing.assert_allclose(r2.residual_history, r1.residual_history, rtol=1e-6)
+    import os
+
+    os.environ["PD_SHARDED_HOST_GMRES"] = "1"
+    try:
+        smg_h = build_sharded_hierarchy(h)
+    finally:
+        del os.environ["PD_SHARDED_HOST_GMRES"]
+    assert smg_h.gms is None
+    x3, r3 = smg_h.solve(b, tol_rel=1e-10, tol_abs=1e-10)
+    assert r3.iterations == r1.iterations
+    assert np.linalg.norm(x3.cpu().numpy() - x1) <= 1e-10 * np.linalg.norm(x1)
 
 
 def test_repeated_solves_replay_captured_cycle_bitwise(golden, monkeypatch):

@@ -133,3 +133,54 @@ def test_layout_rules_and_stmg_rejected():
 
     with pytest.raises(ConfigurationError):
         ShardedMultigrid(mg.mats, mg.transfers, 2, 2, TwoRanks(), CpuEngine())
+
+
+# ---------------------------------------------------------------- device engine, two ranks
+def _dev_worker(rank, size, port, outdir, host_gmres):
+    """Two ranks over gloo sharing one GPU (vectors staged through the host by Comm): the
+    DeviceEngine with the device-resident smoother (pd_gms_*) or the host-GMRES mirror."""
+    sys.path.insert(0, str(REPO))
+    sys.path.insert(0, str(HERE))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    if host_gmres:
+        os.environ["PD_SHARDED_HOST_GMRES"] = "1"
+    dist.init_process_group("gloo", rank=rank, world_size=size)
+    torch.cuda.set_device(0)
+    import paper_2006_12883_b200 as pd
+    from paper_2006_12883_b200.mg_sharded import Comm, build_sharded_hierarchy
+
+    cfg = pd.baseline_config("C2", n=31, Nt=8)
+    system = pd.assemble_system(pd.make_tableau(cfg.M), pd.fd_space(cfg.spec),
+                                pd.TimeGrid(cfg.Nt, cfg.T), 0.0, cfg.u0())
+    h = pd.build_hierarchy(system, "SMG", 3, 3, partitions=4)
+    b = system.rhs()
+    smg = build_sharded_hierarchy(h, Comm(device=torch.device("cuda", 0)))
+    assert (smg.gms is None) == bool(host_gmres)
+    r0, r1 = smg.shards[0].r0, smg.shards[0].r1
+    x, rep = smg.solve(b[r0:r1], tol_rel=1e-10, tol_abs=1e-10)
+    full = torch.zeros(b.size, dtype=torch.float64)
+    full[r0:r1] = x.cpu()
+    dist.all_reduce(full)
+    if rank == 0:
+        xs, reps = h.solve(b, tol_rel=1e-10, tol_abs=1e-10)  # the serial device multigrid
+        np.save(Path(outdir) / "x.npy", full.numpy())
+        np.save(Path(outdir) / "xs.npy", np.asarray(xs))
+        Path(outdir, "rep.json").write_text(json.dumps(
+            {"its": rep.iterations, "conv": rep.converged, "its_serial": reps.iterations,
+             "hist": rep.residual_history, "hist_serial": reps.residual_history}))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("host_gmres", [False, True])
+def test_gpu_sharded_mg_two_ranks_device_engine(tmp_path, host_gmres):
+    """time-slab sharded SMG on the device engine over two ranks == the
+    serial device multigrid (equal cycles, 1e-10) — with the smoother's GMRES resident on
+    the device (no host read-back inside a cycle) and with the host-scalar mirror."""
+    mp.start_processes(_dev_worker, args=(2, _free_port(), str(tmp_path), host_gmres), nprocs=2,
+                       join=True, start_method="spawn")
+    rep = json.loads((tmp_path / "rep.json").read_text())
+    x, xs = np.load(tmp_path / "x.npy"), np.load(tmp_path / "xs.npy")
+    assert rep["conv"] and rep["its"] == rep["its_serial"]
+    np.testing.assert_allclose(rep["hist"], rep["hist_serial"], rtol=1e-6)
+    assert np.linalg.norm(x - xs) <= 1e-10 * np.linalg.norm(xs)
