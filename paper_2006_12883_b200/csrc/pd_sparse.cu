@@ -358,6 +358,14 @@ __global__ void k_fill_int(int* x, int64_t n, int v) {
         x[i] = v;
 }
 
+__global__ void k_max_rowlen(int64_t n, const int64_t* rp, int* out) {
+    int m = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, (int)min((int64_t)INT_MAX, rp[i + 1] - rp[i]));
+    if (m > 0) atomicMax(out, m);
+}
+
 __global__ void k_max_int(const int* x, int64_t n, int* out) {
     int m = 0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -370,6 +378,92 @@ __global__ void k_max_int(const int* x, int64_t n, int* out) {
 // Per row, exactly linalg.py:73-96: for each lower entry k (ascending):
 // l_ik = a_ik / u_kk; a_ij -= l_ik * u_kj over the intersection of row k's
 // upper pattern with row i (two-pointer merge instead of the position map).
+// Warp-per-row ILU(0) factorization (IKJ order, linalg.py:78-98): the row lives in shared
+// memory; for each lower neighbour k in column order the multiplier l_ik = a_ik / u_kk is
+// formed and the lanes sweep row k's upper entries, each finding its column in row i by
+// binary search and applying a_ij -= l_ik * u_kj (separately rounded).  The updates of one
+// k are independent, so the factors are bitwise those of the row-serial loop; a row costs
+// ~nnz_lower dependent L2 round trips instead of ~nnz^2 (the thread-per-row kernel below
+// took 0.6 ms per 35-entry row: with the ~2,300 small levels of a periodic 64^2 x 16
+// Galerkin level that is 1.4 s per factorization).  Rows are taken in level order, eight
+// per 256-thread batch; kFacMaxRow bounds the shared-memory row.
+constexpr int kFacMaxRow = 256;
+
+__global__ void __launch_bounds__(BS) k_ilu0_factor_warp(
+    int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, double* fac,
+    int64_t* diag, const int32_t* __restrict__ order, int* flag, const int* ep,
+    unsigned long long* counter, unsigned long long* bad) {
+    __shared__ int32_t scol[BS / 32][kFacMaxRow];
+    __shared__ double sval[BS / 32][kFacMaxRow];
+    __shared__ long long sbase;
+    const int epoch = *((volatile const int*)ep);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t* col = scol[wid];
+    double* val = sval[wid];
+    for (;;) {
+        if (threadIdx.x == 0) sbase = (long long)atomicAdd(counter, (unsigned long long)(BS / 32));
+        __syncthreads();
+        const int64_t t = sbase + wid;
+        __syncthreads();
+        if (sbase >= n) return;
+        if (t >= n) continue;
+        const int64_t i = order[t];
+        const int64_t a = rp[i];
+        const int len = (int)(rp[i + 1] - a);
+        for (int l = lane; l < len; l += 32) {
+            col[l] = ci[a + l];
+            val[l] = fac[a + l];
+        }
+        __syncwarp();
+        // diagonal position and number of lower entries (columns sorted)
+        int d = -1, pl = 0;
+        for (int l = lane; l < len; l += 32) {
+            if (col[l] == i) d = l;
+            if (col[l] < i) ++pl;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            d = max(d, __shfl_xor_sync(0xffffffffu, d, o));
+            pl += __shfl_xor_sync(0xffffffffu, pl, o);
+        }
+        // every lower neighbour must be fully factored first
+        for (int l = lane; l < pl; l += 32) wait_flag(flag + col[l], epoch);
+        __syncwarp();
+        unsigned long long mybad = ~0ull;
+        for (int pk = 0; pk < pl; ++pk) {
+            const int64_t k = col[pk];
+            const int64_t dk = ldcg(diag + k);
+            const double ukk = ldcg(fac + dk);
+            if (ukk == 0.0 && mybad == ~0ull) mybad = (unsigned long long)k;
+            const double lik = val[pk] / ukk;
+            const int64_t ke = rp[k + 1];
+            __syncwarp();
+            if (lane == 0) val[pk] = lik;
+            for (int64_t p = dk + 1 + lane; p < ke; p += 32) {
+                const int32_t cp = ci[p];
+                int lo = pk + 1, hi = len;  // first q in (pk, len) with col[q] >= cp
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (col[mid] < cp) lo = mid + 1;
+                    else hi = mid;
+                }
+                if (lo < len && col[lo] == cp) val[lo] = sub(val[lo], mul(lik, ldcg(fac + p)));
+            }
+            __syncwarp();
+        }
+        if (mybad == ~0ull && (d < 0 || val[d] == 0.0)) mybad = (unsigned long long)i;
+        for (int l = lane; l < len; l += 32) fac[a + l] = val[l];
+        if (lane == 0) {
+            if (mybad != ~0ull) atomicMin(bad, mybad);
+            diag[i] = d < 0 ? a : a + d;  // keep a valid index; error is reported
+        }
+        __threadfence();
+        __syncwarp();
+        // st.release orders the row's stores (fenced above) before the flag
+        if (lane == 0) st_release(flag + i, epoch);
+    }
+}
+
 __global__ void k_ilu0_factor(int64_t n, const int64_t* __restrict__ rp,
                               const int32_t* __restrict__ ci, double* fac, int64_t* diag,
                               const int32_t* __restrict__ order, int* flag, const int* ep,
@@ -379,7 +473,7 @@ __global__ void k_ilu0_factor(int64_t n, const int64_t* __restrict__ rp,
         int64_t base = fetch_batch(counter);
         if (base >= n) return;
         int64_t t = base + threadIdx.x;
-        if (t < n) {
+        if (t < n && order[t] >= 0) {
             const int64_t i = order[t];
             const int64_t a = rp[i], e = rp[i + 1];
             int64_t d = -1;
@@ -640,6 +734,14 @@ std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks) {
     if (n > 0) launch(k_fill_pending, c.grid_for(n, BS), BS, 0, c.stream, f->scratch.p, n);
     PD_CUDA(cudaMemsetAsync(f->flag.p, 0, std::max<int64_t>(n, 1) * sizeof(int), c.stream));
     PD_CUDA(cudaMemsetAsync(f->ep.p, 0, sizeof(int), c.stream));
+    if (n > 0) {  // longest row: the warp-per-row factorization keeps a row in shared memory
+        DevBuf<int> mx(1);
+        PD_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(int), c.stream));
+        launch(k_max_rowlen, c.grid_for(n, BS), BS, 0, c.stream, n, P.rowptr.p, mx.p);
+        PD_CUDA(cudaMemcpyAsync(&f->max_row_nnz, mx.p, sizeof(int), cudaMemcpyDeviceToHost,
+                                c.stream));
+        PD_CUDA(cudaStreamSynchronize(c.stream));
+    }
     if (n > 0) {
         DevBuf<int> level(n);
         int g = c.grid_for(n, BS, 8);
@@ -649,6 +751,30 @@ std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks) {
         launch(k_levels_lower, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, level.p, f->counter.p);
         PD_LAUNCH_CHECK();
         sort_by_level(c, level.p, n, f->order_lo, f->nlevels_lo);
+        // Small levels (periodic grids: a few dozen rows each): a batch of 256 consecutive
+        // rows of the level order then spans several levels and the factorization's
+        // per-row waits turn into chains inside one warp (C3 32^2 x 8: 458 ms per
+        // factorization of 24,576 rows).  Pad every level to whole warps for that kernel.
+        if (n / std::max(f->nlevels_lo, 1) < 4096 && n < (int64_t)1 << 30) {
+            std::vector<int> hl(n);
+            std::vector<int32_t> ho(n);
+            PD_CUDA(cudaMemcpy(hl.data(), level.p, n * sizeof(int), cudaMemcpyDeviceToHost));
+            PD_CUDA(cudaMemcpy(ho.data(), f->order_lo.p, n * sizeof(int32_t),
+                               cudaMemcpyDeviceToHost));
+            std::vector<int32_t> padded;
+            padded.reserve(n + 32 * (size_t)f->nlevels_lo);
+            for (int64_t t = 0; t < n;) {
+                const int lev = hl[ho[t]];
+                int64_t e = t;
+                while (e < n && hl[ho[e]] == lev) padded.push_back(ho[e++]);
+                while (padded.size() % 32) padded.push_back(-1);
+                t = e;
+            }
+            f->nfac = (int64_t)padded.size();
+            f->order_fac.alloc(padded.size());
+            PD_CUDA(cudaMemcpy(f->order_fac.p, padded.data(), padded.size() * sizeof(int32_t),
+                               cudaMemcpyHostToDevice));
+        }
 
         launch(k_fill_int, c.grid_for(n, BS), BS, 0, c.stream, level.p, n, -1);
         PD_CUDA(cudaMemsetAsync(f->counter.p, 0, sizeof(unsigned long long), c.stream));
@@ -712,9 +838,20 @@ void ilu0_refactor(Ctx& c, Ilu0& f) {
     DevBuf<unsigned long long> bad(1);
     PD_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), c.stream));
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, nullptr, 0);
-    launch(k_ilu0_factor, c.grid_for(n, BS, sweep_blocks_per_sm()), BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p,
-                                                              f.diag.p, f.order_lo.p, f.flag.p,
-                                                              f.ep.p, f.counter.p, bad.p);
+    static const bool thread_rows = getenv("PD_ILU_FACTOR_THREAD_ROWS") != nullptr;
+    if (f.max_row_nnz > 0 && f.max_row_nnz <= kFacMaxRow && !thread_rows) {
+        // a warp per row: eight rows per batch, resident CTAs stride over the level order
+        const int g = (int)std::min<int64_t>((n + BS / 32 - 1) / (BS / 32),
+                                             (int64_t)c.sms * sweep_blocks_per_sm());
+        launch(k_ilu0_factor_warp, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
+               (const int32_t*)f.order_lo.p, f.flag.p, f.ep.p, f.counter.p, bad.p);
+    } else {
+        // n = number of tasks: the padded task list when the levels are small
+        const int64_t ntask = f.nfac ? f.nfac : n;
+        launch(k_ilu0_factor, c.grid_for(ntask, BS, sweep_blocks_per_sm()), BS, 0, c.stream, ntask,
+               P.rowptr.p, P.col.p, f.fac.p, f.diag.p, f.nfac ? f.order_fac.p : f.order_lo.p,
+               f.flag.p, f.ep.p, f.counter.p, bad.p);
+    }
     PD_LAUNCH_CHECK();
     unsigned long long hbad = 0;
     PD_CUDA(cudaMemcpyAsync(&hbad, bad.p, sizeof(hbad), cudaMemcpyDeviceToHost, c.stream));
