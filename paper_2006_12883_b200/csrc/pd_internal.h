@@ -164,10 +164,9 @@ struct Ilu0 {
     DevBuf<double> fac;             // factor values on the pattern
     DevBuf<int64_t> diag;           // diagonal positions
     DevBuf<int32_t> order_lo;       // rows in lower-solve level order
-    // factorization tasks when the levels are small (periodic grids): order_lo with every
+    // order_lo / order_up hold nt_lo / nt_up tasks: the rows in level order with every
     // level padded to a multiple of 32 (-1 = idle lane), so a warp never waits on itself
-    DevBuf<int32_t> order_fac;
-    int64_t nfac = 0;
+    int64_t nt_lo = 0, nt_up = 0;
     int max_row_nnz = 0;            // longest row of the pattern (warp-per-row factorization)
     DevBuf<int32_t> order_up;       // rows in upper-solve level order
     DevBuf<int> flag;               // per-row completion epochs

@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(BS) k_ilu0_factor_warp(
         const int64_t t = sbase + wid;
         __syncthreads();
         if (sbase >= n) return;
-        if (t >= n) continue;
+        if (t >= n || order[t] < 0) continue;
         const int64_t i = order[t];
         const int64_t a = rp[i];
         const int len = (int)(rp[i + 1] - a);
@@ -572,7 +572,7 @@ __global__ void k_trsv_lower(int64_t n, const int64_t* __restrict__ lp,
         int64_t base = fetch_batch(counter);
         if (base >= n) return;
         int64_t t = base + threadIdx.x;
-        if (t < n) {
+        if (t < n && order[t] >= 0) {
             const int64_t i = order[t];
             const double s = accumulate_polling(b[i], lcol, lval, y, lp[t], lp[t + 1]);
             st_strong(y + i, s);
@@ -591,7 +591,7 @@ __global__ void k_trsv_upper(int64_t n, const int64_t* __restrict__ up,
         int64_t base = fetch_batch(counter);
         if (base >= n) return;
         int64_t t = base + threadIdx.x;
-        if (t < n) {
+        if (t < n && order[t] >= 0) {
             const int64_t i = order[t];
             const double yi = y[i];
             const double s = accumulate_polling(yi, ucol, uval, x, up[t], up[t + 1]);
@@ -608,6 +608,10 @@ __global__ void k_task_counts(int64_t n, const int64_t* rp, const int64_t* diag,
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = order[t];
+        if (i < 0) {  // padding task
+            cnt[t + 1] = 0;
+            continue;
+        }
         cnt[t + 1] = upper ? rp[i + 1] - diag[i] - 1 : diag[i] - rp[i];
     }
 }
@@ -618,6 +622,10 @@ __global__ void k_task_gather(int64_t n, const int64_t* rp, const int32_t* ci, c
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = order[t];
+        if (i < 0) {
+            if (upper) tdiag[t] = 1.0;
+            continue;
+        }
         const int64_t d = diag[i];
         const int64_t src = upper ? d + 1 : rp[i];
         const int64_t cnt = tp[t + 1] - tp[t];
@@ -662,6 +670,56 @@ __global__ void k_begin_sweep(int* ep, unsigned long long* c, const int* guard, 
     if (guard_off(guard, want)) return;
     *c = 0ull;
     *ep = *ep + 1;
+}
+
+__global__ void k_level_hist(int64_t n, const int* level, int* hist) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(hist + level[i], 1);
+}
+__global__ void k_pad_order(int64_t n, const int* level, const int32_t* order, const int64_t* start,
+                            const int64_t* pstart, int32_t* padded) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = order[t];
+        const int lev = level[i];
+        padded[pstart[lev] + (t - start[lev])] = i;
+    }
+}
+
+// Level order with every level padded to whole warps (-1 = idle lane): the tasks of one
+// warp then belong to one level, so no thread waits on a row of its own warp.  With small
+// levels (periodic grids: a few dozen rows per level) the unpadded order put several
+// levels into one warp and the per-row waits of the factorization and of the
+// level-scheduled sweeps ran as chains of divergent spin loops.
+static int64_t pad_levels(Ctx& c, const int* level, int64_t n, int nlev, DevBuf<int32_t>& order) {
+    DevBuf<int> hist((size_t)nlev);
+    PD_CUDA(cudaMemsetAsync(hist.p, 0, (size_t)nlev * sizeof(int), c.stream));
+    launch(k_level_hist, c.grid_for(n, BS), BS, 0, c.stream, n, level, hist.p);
+    std::vector<int> h((size_t)nlev);
+    PD_CUDA(cudaMemcpyAsync(h.data(), hist.p, (size_t)nlev * sizeof(int), cudaMemcpyDeviceToHost,
+                            c.stream));
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    std::vector<int64_t> start((size_t)nlev), pstart((size_t)nlev);
+    int64_t a = 0, b = 0;
+    for (int l = 0; l < nlev; ++l) {
+        start[l] = a;
+        pstart[l] = b;
+        a += h[l];
+        b += ((int64_t)h[l] + 31) & ~(int64_t)31;
+    }
+    if (b >= INT32_MAX) throw ConfigError("level order too long");
+    DevBuf<int64_t> ds((size_t)nlev), dp((size_t)nlev);
+    PD_CUDA(cudaMemcpyAsync(ds.p, start.data(), (size_t)nlev * 8, cudaMemcpyHostToDevice, c.stream));
+    PD_CUDA(cudaMemcpyAsync(dp.p, pstart.data(), (size_t)nlev * 8, cudaMemcpyHostToDevice, c.stream));
+    DevBuf<int32_t> padded((size_t)std::max<int64_t>(b, 1));
+    PD_CUDA(cudaMemsetAsync(padded.p, 0xff, (size_t)b * sizeof(int32_t), c.stream));  // -1
+    launch(k_pad_order, c.grid_for(n, BS), BS, 0, c.stream, n, level, (const int32_t*)order.p,
+           (const int64_t*)ds.p, (const int64_t*)dp.p, padded.p);
+    PD_LAUNCH_CHECK();
+    PD_CUDA(cudaStreamSynchronize(c.stream));
+    order = std::move(padded);
+    return b;
 }
 
 static void sort_by_level(Ctx& c, int* level, int64_t n, DevBuf<int32_t>& order, int& nlev) {
@@ -751,36 +809,14 @@ std::unique_ptr<Ilu0> ilu0_create(Ctx& c, const Csr& A, int nblocks) {
         launch(k_levels_lower, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, level.p, f->counter.p);
         PD_LAUNCH_CHECK();
         sort_by_level(c, level.p, n, f->order_lo, f->nlevels_lo);
-        // Small levels (periodic grids: a few dozen rows each): a batch of 256 consecutive
-        // rows of the level order then spans several levels and the factorization's
-        // per-row waits turn into chains inside one warp (C3 32^2 x 8: 458 ms per
-        // factorization of 24,576 rows).  Pad every level to whole warps for that kernel.
-        if (n / std::max(f->nlevels_lo, 1) < 4096 && n < (int64_t)1 << 30) {
-            std::vector<int> hl(n);
-            std::vector<int32_t> ho(n);
-            PD_CUDA(cudaMemcpy(hl.data(), level.p, n * sizeof(int), cudaMemcpyDeviceToHost));
-            PD_CUDA(cudaMemcpy(ho.data(), f->order_lo.p, n * sizeof(int32_t),
-                               cudaMemcpyDeviceToHost));
-            std::vector<int32_t> padded;
-            padded.reserve(n + 32 * (size_t)f->nlevels_lo);
-            for (int64_t t = 0; t < n;) {
-                const int lev = hl[ho[t]];
-                int64_t e = t;
-                while (e < n && hl[ho[e]] == lev) padded.push_back(ho[e++]);
-                while (padded.size() % 32) padded.push_back(-1);
-                t = e;
-            }
-            f->nfac = (int64_t)padded.size();
-            f->order_fac.alloc(padded.size());
-            PD_CUDA(cudaMemcpy(f->order_fac.p, padded.data(), padded.size() * sizeof(int32_t),
-                               cudaMemcpyHostToDevice));
-        }
+        f->nt_lo = pad_levels(c, level.p, n, f->nlevels_lo, f->order_lo);
 
         launch(k_fill_int, c.grid_for(n, BS), BS, 0, c.stream, level.p, n, -1);
         PD_CUDA(cudaMemsetAsync(f->counter.p, 0, sizeof(unsigned long long), c.stream));
         launch(k_levels_upper, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, level.p, f->counter.p);
         PD_LAUNCH_CHECK();
         sort_by_level(c, level.p, n, f->order_up, f->nlevels_up);
+        f->nt_up = pad_levels(c, level.p, n, f->nlevels_up, f->order_up);
 
     }
     ilu0_refactor(c, *f);
@@ -791,6 +827,7 @@ static void build_task_layout(Ctx& c, Ilu0& f) {
     const Csr& P = f.pat();
     const int64_t n = f.n;
     for (int upper = 0; upper < 2; ++upper) {
+        const int64_t n = upper ? f.nt_up : f.nt_lo;  // tasks (rows + level padding)
         DevBuf<int64_t>& tp = upper ? f.tp_up : f.tp_lo;
         DevBuf<int32_t>& tcol = upper ? f.tcol_up : f.tcol_lo;
         DevBuf<double>& tval = upper ? f.tval_up : f.tval_lo;
@@ -839,18 +876,17 @@ void ilu0_refactor(Ctx& c, Ilu0& f) {
     PD_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), c.stream));
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, nullptr, 0);
     static const bool thread_rows = getenv("PD_ILU_FACTOR_THREAD_ROWS") != nullptr;
+    const int64_t ntask = f.nt_lo;  // level order, levels padded to whole warps
     if (f.max_row_nnz > 0 && f.max_row_nnz <= kFacMaxRow && !thread_rows) {
-        // a warp per row: eight rows per batch, resident CTAs stride over the level order
-        const int g = (int)std::min<int64_t>((n + BS / 32 - 1) / (BS / 32),
+        // a warp per row: eight tasks per batch, resident CTAs stride over the level order
+        const int g = (int)std::min<int64_t>((ntask + BS / 32 - 1) / (BS / 32),
                                              (int64_t)c.sms * sweep_blocks_per_sm());
-        launch(k_ilu0_factor_warp, g, BS, 0, c.stream, n, P.rowptr.p, P.col.p, f.fac.p, f.diag.p,
-               (const int32_t*)f.order_lo.p, f.flag.p, f.ep.p, f.counter.p, bad.p);
+        launch(k_ilu0_factor_warp, g, BS, 0, c.stream, ntask, P.rowptr.p, P.col.p, f.fac.p,
+               f.diag.p, (const int32_t*)f.order_lo.p, f.flag.p, f.ep.p, f.counter.p, bad.p);
     } else {
-        // n = number of tasks: the padded task list when the levels are small
-        const int64_t ntask = f.nfac ? f.nfac : n;
         launch(k_ilu0_factor, c.grid_for(ntask, BS, sweep_blocks_per_sm()), BS, 0, c.stream, ntask,
-               P.rowptr.p, P.col.p, f.fac.p, f.diag.p, f.nfac ? f.order_fac.p : f.order_lo.p,
-               f.flag.p, f.ep.p, f.counter.p, bad.p);
+               P.rowptr.p, P.col.p, f.fac.p, f.diag.p, (const int32_t*)f.order_lo.p, f.flag.p,
+               f.ep.p, f.counter.p, bad.p);
     }
     PD_LAUNCH_CHECK();
     unsigned long long hbad = 0;
@@ -897,15 +933,17 @@ void ilu0_solve(Ctx& c, Ilu0& f, const double* b, double* x, const int* guard, i
         wf_solve(c, f, b, x, guard, want);
         return;
     }
-    const int g = c.grid_for(n, BS, sweep_blocks_per_sm());
+    // tasks = rows in level order, levels padded to whole warps (nt_lo / nt_up)
     arm_pending(c, f.scratch.p, n, guard, want);
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, guard, want);
-    launch(k_trsv_lower, g, BS, 0, c.stream, n, f.tp_lo.p, f.tcol_lo.p, f.tval_lo.p,
-           f.order_lo.p, b, f.scratch.p, f.counter.p, guard, want);
+    launch(k_trsv_lower, c.grid_for(f.nt_lo, BS, sweep_blocks_per_sm()), BS, 0, c.stream, f.nt_lo,
+           f.tp_lo.p, f.tcol_lo.p, f.tval_lo.p, f.order_lo.p, b, f.scratch.p, f.counter.p, guard,
+           want);
     arm_pending(c, x, n, guard, want);
     launch(k_begin_sweep, 1, 1, 0, c.stream, f.ep.p, f.counter.p, guard, want);
-    launch(k_trsv_upper, g, BS, 0, c.stream, n, f.tp_up.p, f.tcol_up.p, f.tval_up.p, f.tdiag.p,
-           f.order_up.p, f.scratch.p, x, f.counter.p, guard, want);
+    launch(k_trsv_upper, c.grid_for(f.nt_up, BS, sweep_blocks_per_sm()), BS, 0, c.stream, f.nt_up,
+           f.tp_up.p, f.tcol_up.p, f.tval_up.p, f.tdiag.p, f.order_up.p, f.scratch.p, x,
+           f.counter.p, guard, want);
     PD_LAUNCH_CHECK();
 }
 
