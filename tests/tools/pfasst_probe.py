@@ -1,7 +1,7 @@
 """PFASST timing on the GPU vs the CPU oracle for a few sizes."""
 import sys, time
 from pathlib import Path
-ROOT = Path(__file__).resolve().parent.parent
+ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 import numpy as np
 import torch
