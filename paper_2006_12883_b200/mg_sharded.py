@@ -176,6 +176,23 @@ class DeviceEngine:
 
         return DenseLU(A)
 
+    def slab_stencil(self, system, shard):
+        """K1 for the rank's rows of the fine operator when they are whole time steps that
+        couple to exactly the previous step's last node grid (SMG/SMMG level 0)."""
+        import os
+
+        S = system.space.mesh.ndof
+        per_step = system.tableau.M * S
+        rows = shard.r1 - shard.r0
+        if (os.environ.get("PD_SHARDED_NO_K1") == "1" or rows % per_step or shard.r0 % per_step
+                or shard.halo not in (0, S) or (shard.halo == 0) != (shard.r0 == 0)
+                or system.gamma != 0.0):
+            return None
+        try:
+            return _SlabStencilOp(system, rows // per_step, shard.halo, self.ctx)
+        except ConfigurationError:
+            return None
+
     def smoother(self, n: int, nu: int):
         """Device-resident GMRES(nu) steps driven by the sharded cycle (pd_gms_*)."""
         return _DeviceSmoother(self, n, nu)
@@ -221,6 +238,38 @@ class DeviceEngine:
 
     def comm_tensor(self, x):
         return x
+
+
+class _SlabStencilOp:
+    """Level 0 of a rank's time slab applied matrix-free (K1, pd_stop_apply): bitwise the
+    slab's CSR rows.  Takes the extended vector [halo | own] the CSR operator takes — the
+    halo (the previous slab's last node grid) is passed to the kernel by pointer."""
+
+    def __init__(self, system, steps: int, halo: int, ctx):
+        from . import _native as N
+
+        self.N, self.ctx, self.halo = N, ctx, int(halo)
+        self.handle = system.stencil_operator_handle(ctx, Nt=steps)
+        self.n = steps * system.tableau.M * system.space.mesh.ndof
+
+    def matvec_dev(self, x_ext, out=None, mode=0, b=None):
+        import ctypes
+
+        N = self.N
+        self.ctx.sync_stream()
+        out = N.empty(self.n, self.ctx) if out is None else out
+        own = x_ext[self.halo:] if self.halo else x_ext
+        N.call("pd_stop_apply", self.handle, N.ptr(own), N.ptr(out), int(mode),
+               N.ptr(b) if b is not None else ctypes.c_void_p(),
+               N.ptr(x_ext) if self.halo else ctypes.c_void_p())
+        return out
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                self.N.load_library().pd_stop_destroy(self.handle)
+        except Exception:
+            pass
 
 
 class _DeviceSmoother:
@@ -294,7 +343,8 @@ class ShardedMultigrid:
     """SMG/SMMG V-cycles over G ranks; same interface as MultigridHierarchy.solve."""
 
     def __init__(self, mats, transfers, nu: int, partitions: int, comm: Comm, engine,
-                 restart: int = 30, smooth_solves: int = 1, grids=None, node_counts=None):
+                 restart: int = 30, smooth_solves: int = 1, grids=None, node_counts=None,
+                 system=None):
         if nu < 1:
             raise ConfigurationError("need at least one smoothing iteration")
         if len(transfers) != len(mats) - 1:
@@ -314,7 +364,10 @@ class ShardedMultigrid:
             nxt = (LevelShard(mats[l], *spans[g + 1], r0).halo if g + 1 < G else 0)
             self.shards.append(sh)
             self.halo_send.append(nxt)
-            self.ops.append(engine.operator(sh.A_ext))
+            op = None
+            if l == 0 and system is not None and hasattr(engine, "slab_stencil"):
+                op = engine.slab_stencil(system, sh)  # matrix-free K1 on the slab, or None
+            self.ops.append(op if op is not None else engine.operator(sh.A_ext))
             grid = grids[l] if grids is not None else None
             m = node_counts[l] if node_counts is not None else 0
             self.pres.append(engine.preconditioner(sh.A_own, partitions // G, grid, m))
@@ -534,4 +587,5 @@ def build_sharded_hierarchy(hierarchy, comm: Comm | None = None, engine=None):
     nodes = [d.m for d in hierarchy.dims]
     return ShardedMultigrid(hierarchy.matrices, transfers, hierarchy.nu, hierarchy.partitions,
                             comm, engine, hierarchy.restart, hierarchy.smooth_solves,
-                            grids=grids, node_counts=nodes)
+                            grids=grids, node_counts=nodes,
+                            system=getattr(hierarchy, "_system", None))

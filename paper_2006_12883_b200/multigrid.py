@@ -226,6 +226,9 @@ class MultigridHierarchy:
             raise ConfigurationError(
                 f"matrix size {A.shape[0]} does not match level 1 size {self.dims[0].size}")
         mats = self._galerkin(A)
+        if getattr(self, "_system", None) is not None and hasattr(self, "_fine_installed"):
+            self._system = None  # a later fine matrix is not the attached system's operator
+        self._fine_installed = True
         if self._mg is not None and getattr(self, "_has_fine_op", False):
             # a new fine matrix (e.g. a Newton Jacobian) no longer matches the
             # matrix-free operator attached by build_hierarchy
@@ -303,6 +306,7 @@ class MultigridHierarchy:
     def set_fine_values_dev(self, vals) -> None:
         """New fine-level values on the existing pattern (CUDA tensor, nnz doubles):
         Galerkin products and all factorizations are recomputed on device."""
+        self._system = None
         if getattr(self, "_has_fine_op", False):
             N.call("pd_mg_set_fine_operator", self._mg, None)
             self._has_fine_op = False
@@ -318,6 +322,7 @@ class MultigridHierarchy:
         other use of A_1 (smoother GMRES, residuals, restriction input, the
         solve's stopping test) streams only vectors.
         """
+        self._system = system  # the sharded hierarchy builds its slab operators from it
         if self._mg is None:
             return
         op = system.stencil_operator_handle(self.ctx)

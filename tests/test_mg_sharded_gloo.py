@@ -156,6 +156,9 @@ def _dev_worker(rank, size, port, outdir, host_gmres):
     b = system.rhs()
     smg = build_sharded_hierarchy(h, Comm(device=torch.device("cuda", 0)))
     assert (smg.gms is None) == bool(host_gmres)
+    from paper_2006_12883_b200.mg_sharded import _SlabStencilOp
+
+    assert isinstance(smg.ops[0], _SlabStencilOp)  # level 0 matrix-free (K1 with a halo)
     r0, r1 = smg.shards[0].r0, smg.shards[0].r1
     x, rep = smg.solve(b[r0:r1], tol_rel=1e-10, tol_abs=1e-10)
     full = torch.zeros(b.size, dtype=torch.float64)
