@@ -23,7 +23,9 @@ struct StOp {
     // structured-grid mode (Dirichlet constant-coefficient stencil on n^dim)
     int grid_dim = 0, grid_n = 0;
     DevBuf<double> grid_tab;  // [m][m'][position] + step coupling per m
-    DevBuf<double> grid_partials;  // fused-norm per-block partials (kGridMaxBlocks)
+    std::vector<double> grid_tab_host;  // the same table on the host (kernel parameters)
+    DevBuf<double> grid_partials;  // fused-norm per-block partials (grid_blocks_max)
+    int64_t grid_blocks_max = 0;
     DevBuf<unsigned int> grid_counter;
     StOp(Ctx& c, int64_t Nt, int M, int64_t S, const double* Kq, const double* Mq,
          const double* l0, double dt, const Csr& Kh, const double* mh_host);
