@@ -295,6 +295,130 @@ __global__ void __launch_bounds__(SB, M <= 3 ? 3 : 2) k_st_grid(int64_t Nt, int 
     }
 }
 
+// ---- periodic 2D grids (BASELINE config 3) ----
+// The same kernel for the 5-point stencil with wrap-around neighbours.  Every point has
+// all five entries; what changes at the grid's edges is their COLUMN ORDER in the CSR
+// row (a wrapped neighbour's column sorts to the other end), and the sum must follow it
+// to stay bitwise scipy's.  Products are formed in the interior order (y-1, x-1, c, x+1,
+// y+1) and added in the order of the point's case: x interior / first / last column
+// times y interior / first / last line — nine fully unrolled variants, divergent only in
+// the warps that touch an edge.
+template <int XC, int YC>
+__device__ __forceinline__ double add_periodic5(double s, const double (&p)[5]) {
+    // x group in column order
+    auto xg = [&](double a) {
+        if (XC == 0) { a = add(a, p[1]); a = add(a, p[2]); a = add(a, p[3]); }        // x-1, c, x+1
+        else if (XC == 1) { a = add(a, p[2]); a = add(a, p[3]); a = add(a, p[1]); }   // x = 0
+        else { a = add(a, p[3]); a = add(a, p[1]); a = add(a, p[2]); }                // x = n-1
+        return a;
+    };
+    if (YC == 0) { s = add(s, p[0]); s = xg(s); s = add(s, p[4]); }        // y-1, X, y+1
+    else if (YC == 1) { s = xg(s); s = add(s, p[4]); s = add(s, p[0]); }   // y = 0: y-1 wraps last
+    else { s = add(s, p[4]); s = add(s, p[0]); s = xg(s); }                // y = n-1: y+1 wraps first
+    return s;
+}
+
+template <int M, int XC, int YC>
+__device__ __forceinline__ void rows_periodic(const double* c, const double (&v)[M][5], bool prev,
+                                              double vprev, double (&out)[M]) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        double sacc = 0.0;
+        if (prev && c[M * M * 5 + m] != 0.0) sacc = add(sacc, mul(c[M * M * 5 + m], vprev));
+#pragma unroll
+        for (int mp = 0; mp < M; ++mp) {
+            double p[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) p[k] = mul(c[(m * M + mp) * 5 + k], v[mp][k]);
+            sacc = add_periodic5<XC, YC>(sacc, p);
+        }
+        out[m] = sacc;
+    }
+}
+
+template <int M, bool REDUCE>
+__global__ void __launch_bounds__(SB, M <= 3 ? 3 : 2) k_st_grid_per(
+    int64_t Nt, int n, const __grid_constant__ GridTabP<2, M> T, const double* __restrict__ x,
+    const double* __restrict__ halo, double* y, int mode, const double* b, const int* guard,
+    int want, double* partials, unsigned int* counter, double* norm2, int* nonfinite) {
+    if (guard_off(guard, want)) return;
+    const double* c = T.c;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    const int xi = blockIdx.x * 32 + threadIdx.x;
+    const int yi = (int)blockIdx.y * 8 + threadIdx.y;
+    const bool inside = xi < n && yi < n;
+    const int Si = n * n;
+    const int64_t MS = (int64_t)M * Si;
+    const int j = yi * n + xi;
+    double acc2 = 0.0;
+    bool bad = false;
+    const int64_t step = blockIdx.z;
+    if (inside && step < Nt) {
+        const int xc = xi == 0 ? 1 : (xi == n - 1 ? 2 : 0), yc = yi == 0 ? 1 : (yi == n - 1 ? 2 : 0);
+        int off[5];
+        off[0] = yc == 1 ? (n - 1) * n : -n;
+        off[1] = xc == 1 ? n - 1 : -1;
+        off[2] = 0;
+        off[3] = xc == 2 ? -(n - 1) : 1;
+        off[4] = yc == 2 ? -(n - 1) * n : n;
+        const double* xs = x + step * MS + j;
+        double v[M][5];
+#pragma unroll
+        for (int mp = 0; mp < M; ++mp)
+#pragma unroll
+            for (int k = 0; k < 5; ++k) v[mp][k] = __ldg(xs + (mp * Si + off[k]));
+        const double* xp = step > 0 ? xs - MS + (M - 1) * Si : (halo ? halo + j : nullptr);
+        const double vprev = xp ? __ldg(xp) : 0.0;
+        double rows[M];
+        switch (yc * 3 + xc) {
+            case 0: rows_periodic<M, 0, 0>(c, v, xp != nullptr, vprev, rows); break;
+            case 1: rows_periodic<M, 1, 0>(c, v, xp != nullptr, vprev, rows); break;
+            case 2: rows_periodic<M, 2, 0>(c, v, xp != nullptr, vprev, rows); break;
+            case 3: rows_periodic<M, 0, 1>(c, v, xp != nullptr, vprev, rows); break;
+            case 4: rows_periodic<M, 1, 1>(c, v, xp != nullptr, vprev, rows); break;
+            case 5: rows_periodic<M, 2, 1>(c, v, xp != nullptr, vprev, rows); break;
+            case 6: rows_periodic<M, 0, 2>(c, v, xp != nullptr, vprev, rows); break;
+            case 7: rows_periodic<M, 1, 2>(c, v, xp != nullptr, vprev, rows); break;
+            default: rows_periodic<M, 2, 2>(c, v, xp != nullptr, vprev, rows); break;
+        }
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            const int64_t r = step * MS + j + m * Si;
+            double out = rows[m];
+            if (mode == 1) out = sub(b[r], rows[m]);
+            else if (mode == 2) out = add(b[r], rows[m]);
+            y[r] = out;
+            if (REDUCE) {
+                acc2 = fma(out, out, acc2);
+                if (nonfinite && !isfinite(v[m][2])) bad = true;
+            }
+        }
+    }
+    if (REDUCE) {
+        if (bad) atomicOr(nonfinite, 1);
+        __shared__ double sh[SB / 32];
+        __shared__ bool last;
+        double sblk = block_sum_flat<SB>(acc2, sh, tid);
+        const unsigned int bid = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        const unsigned int nb = gridDim.x * gridDim.y * gridDim.z;
+        if (tid == 0) {
+            partials[bid] = sblk;
+            __threadfence();
+            last = (atomicAdd(counter, 1u) == nb - 1);
+        }
+        __syncthreads();
+        if (!last) return;
+        __threadfence();
+        double t = 0.0;
+        for (unsigned int i = tid; i < nb; i += SB) t += __ldcg(partials + i);
+        t = block_sum_flat<SB>(t, sh, tid);
+        if (tid == 0) {
+            *norm2 = t;
+            *counter = 0u;
+        }
+    }
+}
+
 // the grid table from the coefficient table of one interior row (k_st_coef's
 // rounding) and the step coupling -fl(l0[m]*mh)
 __global__ void k_st_grid_tab(int M, int NP, int64_t nnzK, const int64_t* __restrict__ rp,
@@ -397,6 +521,40 @@ bool detect_dirichlet_stencil(const Csr& K, int& dim, int& n_out, double tv[7], 
     return false;
 }
 
+// Kh is exactly the periodic 5-point stencil on an n x n grid (n >= 3): every row has
+// its five wrapped neighbours, in sorted column order, with one value per position.
+// tv = values by position (y-1, x-1, c, x+1, y+1) of an interior row jc.
+static bool detect_periodic_stencil2d(const Csr& K, int& n_out, int64_t& jc_out) {
+    const int64_t S = K.nrows;
+    if (S < 9 || K.ncols != S || K.nnz != 5 * S || getenv("PD_NO_GRID_STENCIL")) return false;
+    const int64_t n = (int64_t)llround(std::sqrt((double)S));
+    if (n * n != S || n < 3 || S >= INT_MAX / 8) return false;
+    std::vector<int64_t> rp(S + 1);
+    std::vector<int32_t> ci(K.nnz);
+    std::vector<double> kv(K.nnz);
+    PD_CUDA(cudaMemcpy(rp.data(), K.rowptr.p, (S + 1) * 8, cudaMemcpyDeviceToHost));
+    PD_CUDA(cudaMemcpy(ci.data(), K.col.p, K.nnz * 4, cudaMemcpyDeviceToHost));
+    PD_CUDA(cudaMemcpy(kv.data(), K.val.p, K.nnz * 8, cudaMemcpyDeviceToHost));
+    const int64_t mid = n / 2, jc = mid * n + mid;
+    if (n < 5 || rp[jc + 1] - rp[jc] != 5) return false;
+    double tv[5];
+    for (int k = 0; k < 5; ++k) tv[k] = kv[rp[jc] + k];
+    for (int64_t j = 0; j < S; ++j) {
+        if (rp[j + 1] - rp[j] != 5) return false;
+        const int64_t xi = j % n, yi = j / n;
+        // (column, position) of the five wrapped neighbours, sorted by column
+        std::pair<int64_t, int> e[5] = {
+            {((yi + n - 1) % n) * n + xi, 0}, {yi * n + (xi + n - 1) % n, 1}, {j, 2},
+            {yi * n + (xi + 1) % n, 3}, {((yi + 1) % n) * n + xi, 4}};
+        std::sort(e, e + 5);
+        for (int k = 0; k < 5; ++k)
+            if (ci[rp[j] + k] != e[k].first || kv[rp[j] + k] != tv[e[k].second]) return false;
+    }
+    n_out = (int)n;
+    jc_out = jc;
+    return true;
+}
+
 // Structured K1 mode: Kh a Dirichlet constant-coefficient stencil, Mh constant,
 // and a kernel instantiated for M.
 void StOp::detect_grid(const std::vector<int64_t>& rp, const double* mh_host) {
@@ -408,7 +566,12 @@ void StOp::detect_grid(const std::vector<int64_t>& rp, const double* mh_host) {
     int d = 0, n = 0;
     double tv[7];
     int64_t jc = 0;
-    if (!detect_dirichlet_stencil(*Kh, d, n, tv, jc) || S * M >= INT_MAX) return;
+    if (S * M >= INT_MAX) return;
+    if (!detect_dirichlet_stencil(*Kh, d, n, tv, jc)) {
+        if (!detect_periodic_stencil2d(*Kh, n, jc)) return;
+        d = 2;
+        grid_periodic = true;
+    }
     grid_tab.alloc(kGridMaxTabHost);
     Tab T = make_tab_raw(Kq, Mq, l0, (int)M);
     launch(k_st_grid_tab, 1, 128, 0, c.stream, (int)M, 2 * d + 1, nnzK, Kh->rowptr.p, jc, coef.p,
@@ -463,6 +626,19 @@ static void launch_grid(const StOp& op, const double* x, double* y, int mode, co
     if (op.grid_tab_host.size() != sizeof(T.c) / sizeof(double))
         throw ConfigError("grid K1: coefficient table size mismatch");
     std::memcpy(T.c, op.grid_tab_host.data(), sizeof(T.c));
+    if constexpr (DIM == 2) {
+        if (op.grid_periodic) {
+            if (norm2_out)
+                launch(k_st_grid_per<MM, true>, grid, block, 0, c.stream, op.Nt, n, T, x, halo, y,
+                       mode, b, guard, want, op.grid_partials.p, op.grid_counter.p, norm2_out,
+                       nonfinite);
+            else
+                launch(k_st_grid_per<MM, false>, grid, block, 0, c.stream, op.Nt, n, T, x, halo, y,
+                       mode, b, guard, want, (double*)nullptr, (unsigned int*)nullptr,
+                       (double*)nullptr, (int*)nullptr);
+            return;
+        }
+    }
     if (norm2_out) {
         launch(k_st_grid<DIM, MM, true>, grid, block, 0, c.stream, op.Nt, n, gy, T, x,
                halo, y, mode, b, guard, want, op.grid_partials.p, op.grid_counter.p, norm2_out,

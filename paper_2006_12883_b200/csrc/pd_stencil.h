@@ -26,6 +26,7 @@ struct StOp {
     std::vector<double> grid_tab_host;  // the same table on the host (kernel parameters)
     DevBuf<double> grid_partials;  // fused-norm per-block partials (grid_blocks_max)
     int64_t grid_blocks_max = 0;
+    bool grid_periodic = false;  // 2D periodic 5-point stencil (wrapped neighbours)
     DevBuf<unsigned int> grid_counter;
     StOp(Ctx& c, int64_t Nt, int M, int64_t S, const double* Kq, const double* Mq,
          const double* l0, double dt, const Csr& Kh, const double* mh_host);
