@@ -114,6 +114,20 @@ __global__ void k_gm_mgs(GmDev* s, int i, double* w, const double* V, int64_t n,
     grid_sum_finish<KB>(acc, partials, counter, &s->dots[i]);
 }
 
+// y = H[:k,:k]^{-1} g[:k]  (column-oriented back substitution, dtrsm order); runs at the
+// end of the Arnoldi step that ends a cycle
+__device__ void gm_finish_y(GmDev* s) {
+    const int k = s->k, R = s->restart;
+    for (int i = 0; i < k; ++i) s->y[i] = s->g[i];
+    for (int c = k - 1; c >= 0; --c) {
+        if (s->y[c] != 0.0) {
+            s->y[c] = s->y[c] / s->H[c * R + c];
+            const double yc = s->y[c];
+            for (int i = 0; i < c; ++i) s->y[i] = sub(s->y[i], mul(yc, s->H[i * R + c]));
+        }
+    }
+}
+
 // Hessenberg column, Givens rotations, residual estimate, stop decision.
 __global__ void k_gm_arnoldi(GmDev* s, int slot, double* hist) {
     if (s->phase != GM_RUN) return;
@@ -161,6 +175,7 @@ __global__ void k_gm_arnoldi(GmDev* s, int slot, double* hist) {
         // the closing true residual decides restarts and the report; a smoother
         // at its iteration cap needs neither (multigrid.py:246-255 drops it)
         s->final_res = (s->skip_final && s->total >= s->max_it) ? -1 : GM_FINISH;
+        gm_finish_y(s);
     } else {
         s->j = j + 1;
     }
@@ -177,20 +192,6 @@ __global__ void k_gm_newvec(const GmDev* s, int slot, const double* w, double* V
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         dst[i] = w[i] / hn;
-}
-
-// y = H[:k,:k]^{-1} g[:k]  (column-oriented back substitution, dtrsm order)
-__global__ void k_gm_finish_y(GmDev* s) {
-    if (s->phase != GM_FINISH) return;
-    const int k = s->k, R = s->restart;
-    for (int i = 0; i < k; ++i) s->y[i] = s->g[i];
-    for (int c = k - 1; c >= 0; --c) {
-        if (s->y[c] != 0.0) {
-            s->y[c] = s->y[c] / s->H[c * R + c];
-            const double yc = s->y[c];
-            for (int i = 0; i < c; ++i) s->y[i] = sub(s->y[i], mul(yc, s->H[i * R + c]));
-        }
-    }
 }
 
 // u = V[:k]^T y
@@ -318,8 +319,7 @@ void Gmres::enqueue_slot(int slot, int mgs_passes, const double* b) {
                                           c.red_counter.p);
     launch(k_gm_arnoldi, 1, 1, 0, c.stream, st.p, slot, hist.p);
     launch(k_gm_newvec, g, KB, 0, c.stream, st.p, slot, w.p, V.p, n);
-    // cycle finish (active only when this step ended the cycle)
-    launch(k_gm_finish_y, 1, 1, 0, c.stream, st.p);
+    // cycle finish (active only when this step ended the cycle; y is formed by k_gm_arnoldi)
     // x += M^{-1}(V y) (linalg.py:297); with stored Z_j = M^{-1} V_j this is
     // sum_j y_j Z_j — the same linear map, one ILU apply fewer per cycle
     if (!M || store_z) {
@@ -357,7 +357,6 @@ void Gmres::ext_end(int slot) {
     const int g = c.grid_for(n, KB, 8);
     launch(k_gm_arnoldi, 1, 1, 0, c.stream, st.p, slot, hist.p);
     launch(k_gm_newvec, g, KB, 0, c.stream, st.p, slot, w.p, V.p, n);
-    launch(k_gm_finish_y, 1, 1, 0, c.stream, st.p);
     launch(k_gm_combine_update, g, KB, 0, c.stream, st.p, Z.p, xg.p, n);
     // a cycle that ends before the cap (residual estimate below 1e-13 |r0| or a happy
     // breakdown) is taken as converged: norm2 stays 0, so k_gm_restart reads a zero true
@@ -401,7 +400,6 @@ void Gmres::slot_with_callables(int slot, int mgs_passes, const double* b, const
                c.red_counter.p);
     launch(k_gm_arnoldi, 1, 1, 0, c.stream, st.p, slot, hist.p);
     launch(k_gm_newvec, g, KB, 0, c.stream, st.p, slot, w.p, V.p, n);
-    launch(k_gm_finish_y, 1, 1, 0, c.stream, st.p);
     launch(k_gm_combine, g, KB, 0, c.stream, st.p, V.p, u.p, n);
     PD_LAUNCH_CHECK();
     read_state();
